@@ -1,0 +1,198 @@
+/*
+ * apmg_cuda.h -- C ABI of libapmg_cuda.so, the sm_100a implementation of the
+ * APMGSRN train-and-query hot path (arXiv 2308.02494).
+ *
+ * The reference (/root/reference/pkg/src/apmg, pure numpy) has no FFI layer:
+ * its boundary is the Python module API.  Each entry point below replaces one
+ * reference function; the replaced symbol is cited as file:line relative to
+ * /root/reference/pkg/src/apmg.  INTEGRATION.md shows the ctypes stub a
+ * maintainer of the reference would add to bind them.
+ *
+ * Conventions
+ *  - Every tensor argument is a DEVICE pointer unless documented otherwise;
+ *    sizes are element counts.  `stream` is a cudaStream_t (NULL = legacy).
+ *  - Functions return 0 on success or a negative APMG_E* code; the message is
+ *    available from apmg_last_error() (thread-local).  Calls are asynchronous
+ *    on `stream` unless documented as synchronising.
+ *  - `dtype` is APMG_F32 or APMG_F64: the element type of the model tensors
+ *    (the reference runs float32 models and float64 copies, model.py:125-136).
+ *  - Device grids are CHANNEL-LAST [M][D][H][W][C]; the reference layout
+ *    [M][C][D][H][W] (model.py:90) is converted by the host wrapper.
+ *  - No entry point falls back to the CPU.
+ */
+#ifndef APMG_CUDA_H
+#define APMG_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APMG_F32 0
+#define APMG_F64 1
+
+#define APMG_OK 0
+#define APMG_E_ARG (-1)        /* invalid argument / shape (ValueError in the reference) */
+#define APMG_E_CUDA (-2)       /* CUDA runtime error */
+#define APMG_E_WORKSPACE (-3)  /* workspace too small */
+#define APMG_E_UNSUPPORTED (-4)
+
+/* Model parameters (ApmgModel, model.py:86-119). hidden must be 64 (model.py:37). */
+typedef struct apmg_model {
+  int32_t dtype;
+  int32_t grids, channels, depth, height, width; /* M, C, D, H, W */
+  int32_t hidden;
+  int32_t flat_top_p;
+  const void* transforms; /* [M][4][4] */
+  const void* grids_cl;   /* [M][D][H][W][C] channel-last */
+  const void* w1;         /* [64][M*C] */
+  const void* w2;         /* [64][64] */
+  const void* w3;         /* [1][64] */
+  double vmin, vmax;
+} apmg_model;
+
+/* ---- library ---------------------------------------------------------- */
+const char* apmg_last_error(void);
+const char* apmg_version(void);
+int apmg_device_sm_count(void);
+/* number of kernels this library launched since load (evidence for bench.py) */
+uint64_t apmg_launch_count(void);
+/* per-kernel CUDA-event timing on the launching stream (bench roofline). */
+int apmg_kernel_timing_enable(int on);
+/* copies up to `cap` records (name, total_ms, launches); returns count.  Synchronises. */
+int apmg_kernel_timing_read(char* names /* cap*64 bytes */, double* total_ms, int64_t* launches, int cap);
+
+/* ---- model forward (model.py:141-166) ----------------------------------- */
+/* ApmgModel.encode (model.py:141-150): pts [n][3] dtype -> feats [n][M*C] dtype */
+int apmg_encode(const apmg_model* m, const void* pts, int64_t n, void* feats, void* stream);
+/* ApmgModel.decode (model.py:152-162): feats [n][M*C] -> out [n] */
+int apmg_decode(const apmg_model* m, const void* feats, int64_t n, void* out, void* stream);
+/* ApmgModel.forward (model.py:164-166): fused encode + decode, pts [n][3] -> out [n] */
+int apmg_forward(const apmg_model* m, const void* pts, int64_t n, void* out, void* stream);
+
+/* ---- reconstruction loss (optim.py:102-155) ------------------------------ */
+size_t apmg_recon_workspace_bytes(const apmg_model* m, int64_t n);
+/* recon_loss_and_grads: loss (device f64 scalar), sq_errors [n] dtype, and the
+ * gradient of the main group, written into grad_main laid out as
+ * [grids_cl (M*D*H*W*C) | w1 (64*M*C) | w2 (4096) | w3 (64)] (dtype).
+ * grad_main must be zero on entry (the grid part is accumulated). */
+int apmg_recon_loss_grads(const apmg_model* m, const void* coords, const void* targets, int64_t n,
+                          void* sq_errors, double* loss, void* grad_main, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* ---- feature density (density.py, optim.py:158-200) ---------------------- */
+size_t apmg_density_workspace_bytes(int32_t grids, int64_t n);
+/* density_loss_and_grads: coords [n][3] dtype, errors [n] f64 -> loss (device f64),
+ * d_transforms [M][4][4] dtype (bottom rows zero).  Also writes the batch sum of
+ * rho to *rho_total (device f64) so the caller can raise the reference's
+ * "degenerate" DensityError (density.py:115). */
+int apmg_density_loss_grads(const apmg_model* m, const void* coords, const double* errors, int64_t n,
+                            double* loss, void* d_transforms, double* rho_total, void* workspace,
+                            size_t workspace_bytes, void* stream);
+/* feature_density (density.py:83-108): transforms [M][4][4] dtype, pts [n][3] f64 -> rho [n] f64 */
+int apmg_feature_density(int32_t dtype, const void* transforms, int32_t grids, int32_t p,
+                         const double* pts, int64_t n, double* rho, void* stream);
+/* target_density (density.py:120-137) elementwise: rho_star[n] */
+int apmg_target_density(const double* rho_scaled, const double* errors, int64_t n, double mean_error,
+                        double eps, double* rho_star, void* stream);
+/* deterministic f64 sum of x[n] (used for scale_density, means, density_loss) */
+size_t apmg_sum_workspace_bytes(int64_t n);
+int apmg_sum_f64(const double* x, int64_t n, double* out, void* workspace, size_t workspace_bytes,
+                 void* stream);
+/* density_loss (density.py:140-148) terms: out[i] = rho_s (log(rho_s+eps) - log rho*) ; caller sums/N */
+int apmg_density_loss_terms(const double* rho_scaled, const double* rho_star, int64_t n, double eps,
+                            double* terms, void* stream);
+/* out[i] = x[i] * scale (scale_density, density.py:111-117, with scale = 1/sum) */
+int apmg_scale_f64(const double* x, int64_t n, const double* divisor, double* out, void* stream);
+
+/* ---- optimizer (optim.py:47-73) ------------------------------------------ */
+/* masked Adam: entries with g == 0 leave p, m, v untouched. lr, bc1 = 1-0.9^t,
+ * bc2 = 1-0.99^t are the reference's Python floats; they are rounded to dtype
+ * exactly as numpy does for a float32 array operand. */
+int apmg_adam_step(int32_t dtype, void* params, const void* grads, void* m, void* v, int64_t n,
+                   double lr, double bc1, double bc2, void* stream);
+
+/* ---- batch generation (trainer.py:175-191, volume.py:147-199) -------------- */
+/* out[i] = lo + (hi-lo) * ((word(offset+i) >> 11) * 2^-53), word j = lane j%4 of
+ * Philox4x64-10(counter = j/4 + 1, key) -- numpy.random.Philox + Generator.uniform. */
+int apmg_philox_uniform(uint64_t key0, uint64_t key1, uint64_t word_offset, int64_t count, double lo,
+                        double hi, double* out, void* stream);
+/* Volume.sample_many: fp64 trilinear of data [D][H][W] f32 at pts [n][3] f64.
+ * *oob (device int) is set to 1 if any coordinate lies outside [-1,1]^3. */
+int apmg_sample_volume(const float* data, int32_t w, int32_t h, int32_t d, const double* pts, int64_t n,
+                       double* out, int32_t* oob, void* stream);
+/* synth_volume (volume.py:275-296): acc = background + sum_b amp_b ez[z] ey[y] ex[x]
+ * (+ Philox uniform noise), rounded to f32.  ex/ey/ez are [nblobs][W|H|D] f64 device arrays. */
+int apmg_synth_volume(int32_t w, int32_t h, int32_t d, int32_t nblobs, const double* ex,
+                      const double* ey, const double* ez, const double* amp, double background,
+                      uint64_t key0, uint64_t key1, double noise, float* out, void* stream);
+
+/* ---- query path (decomposition.py:112-123, 294-304; trainer.py:226-247) ----- */
+/* spatial_hash: pts [n][3] (dtype) -> owner [n] int64; *oob set when |p| > 1 */
+int apmg_spatial_hash(int32_t pts_dtype, const void* pts, int64_t n, int32_t bi, int32_t bj, int32_t bk,
+                      int64_t* owner, int32_t* oob, void* stream);
+/* DecomposedField.forward: models[b] (HOST array of descriptors whose tensor
+ * pointers are device pointers), per-brick affine scale/offset [B][3] (HOST f64),
+ * pts [n][3] f32 -> out [n] f32.  Synchronises (reads per-brick counts). */
+size_t apmg_decomposed_workspace_bytes(int32_t bricks, int64_t n);
+int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
+                            const double* scale, const double* offset, const float* pts, int64_t n,
+                            float* out, void* workspace, size_t workspace_bytes, void* stream);
+/* Lattice sweep of one model over the voxel box [x0,x1]x[y0,y1]x[z0,z1] of a
+ * (W,H,D) lattice (axis_coords, volume.py:161-165), optionally through a
+ * brick affine (scale/offset HOST f64[3] or NULL).  If truth != NULL the f64
+ * sum of squared errors against truth [D][H][W] is ADDED to *sse (device f64);
+ * if recon != NULL predictions are written to recon [D][H][W] f32. */
+int apmg_lattice_sweep(const apmg_model* m, int32_t w, int32_t h, int32_t d, const int32_t box[6],
+                       const double* scale, const double* offset, const float* truth, double* sse,
+                       float* recon, void* stream);
+
+/* ---- device-resident training loop (trainer.py:160-223) -------------------- */
+typedef struct apmg_train_config {
+  int64_t iterations, batch_size;
+  double lr_main, lr_transform;
+  int64_t delay_start, transform_ma_window;
+  double transform_improve_threshold;
+  int64_t hard_stop_iteration; /* ceil(transform_hard_stop_fraction * iterations) */
+  int64_t plateau_window;
+  double plateau_threshold, plateau_factor;
+  int64_t plateau_max_triggers;
+  uint64_t key0, key1; /* Philox key of TrainConfig.seed */
+  int32_t train_transforms, plateau_enabled;
+} apmg_train_config;
+
+typedef struct apmg_train_state apmg_train_state;
+
+size_t apmg_train_workspace_bytes(const apmg_model* m, const apmg_train_config* cfg);
+/* Parameters are updated in place: grad-free main group `main_params` laid out
+ * [grids_cl | w1 | w2 | w3] and `transforms` [M][4][4] (both dtype, device).
+ * bias_table: HOST f64 [iterations][2] = (1-0.9^t, 1-0.99^t) for t = 1..iterations
+ * computed in Python so Adam's bias corrections match the reference bit for bit. */
+int apmg_train_create(apmg_train_state** out, const apmg_model* shape, void* main_params, void* transforms,
+                      const float* volume, int32_t w, int32_t h, int32_t d, const apmg_train_config* cfg,
+                      const double* bias_table, void* workspace, size_t workspace_bytes, void* stream);
+/* enqueue up to n iterations (asynchronous; iterations after a plateau stop are no-ops) */
+int apmg_train_run(apmg_train_state* s, int64_t n, void* stream);
+/* synchronising: iterations_run and whether the loop has ended */
+int apmg_train_status(apmg_train_state* s, int64_t* iterations_run, int32_t* finished, void* stream);
+/* synchronising: copy the log (HOST buffers of length >= iterations; triggers >= plateau_max_triggers) */
+int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_density, double* lr, int64_t* stop_iteration,
+                   int64_t* triggers, int64_t* n_triggers, void* stream);
+int apmg_train_destroy(apmg_train_state* s);
+
+/* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
+/* plateau_step (trainer.py:118-138) on the same code the device controller runs.
+ * history: HOST ring of capacity window+1 (in/out), count in/out; returns 0 none,
+ * 1 reduce_lr, 2 stop. */
+int apmg_host_plateau_step(double* history, int64_t* count, int64_t* triggers, int64_t window,
+                           double threshold, int64_t max_triggers, double current_ma);
+/* transform_stop_check (trainer.py:141-157) */
+int apmg_host_transform_stop(const double* history, int64_t count, int64_t window, double threshold,
+                             int64_t hard_stop_iteration, int64_t iteration);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APMG_CUDA_H */
