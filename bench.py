@@ -1,0 +1,362 @@
+"""Benchmark: APMGSRN training throughput (train points/sec) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 64 grids 32^3 x 2 features, MLP 2x64,
+fit a synthetic 512^3 blob volume (test_acceptance.py:156-164 blob list),
+batch 2^20, density loss on every timed iteration.  One "step" = one training
+iteration (Philox batch + fp64 targets + fused recon fwd/bwd + masked Adam +
+fp64 density step + scheduler), all device-resident.
+
+N > 1 (torchrun): weak scaling -- rank r trains brick r of the 2x2x2
+decomposition of a synthetic 1024^3 volume (configs[3]); each brick is an
+independent model (ghost extent ~513^3), no data-path collective; the timing
+is the max over ranks.
+
+``--impl reference`` times the reference algorithm (the numpy oracle port; the
+reference itself is pure numpy and not installed on the GPU box) on the host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BATCH = 1 << 20
+DIMS1 = (512, 512, 512)
+DIMS_DECOMP = (1024, 1024, 1024)
+M, CH, RES = 64, 2, (32, 32, 32)
+BLOBS = [((0.45, -0.3, 0.2), (0.035, 0.035, 0.035), 1.0), ((-0.2, 0.2, -0.1), (0.6, 0.5, 0.7), 0.35),
+         ((0.3, 0.4, 0.5), (0.45, 0.55, 0.4), 0.25), ((-0.5, -0.5, 0.4), (0.5, 0.4, 0.5), 0.3)]
+METRIC = "train points/sec"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows, self.proc = [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, rank, world, local
+    return None, 0, 1, local
+
+
+def brick_workload(rank, world):
+    """(volume dims, extent or None, description) of this rank's training unit."""
+    from paper_2308_02494_b200.decomposition import plan_partition
+    if world == 1:
+        return DIMS1, None, "C2: single model, synthetic 512^3 volume"
+    plan = plan_partition(DIMS_DECOMP, 2, 2, 2, ghost=1)
+    brick = plan.bricks[rank % plan.brick_count]
+    return DIMS_DECOMP, brick.ghost, f"C4: brick {rank % 8} of 2x2x2 over synthetic 1024^3 (ghost 1)"
+
+
+# algorithmic work per training point -> per-kernel roofline rows
+def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
+    t = ms_per_launch * 1e-3
+    rows = {
+        # fused encoder fwd + MLP fwd/bwd + grid scatter: 8 corners x 64 grids x 2 ch x 4 B gathered
+        # and scattered per point (L2-resident 16 MiB grids) + 12 B coords + 4 B target + 4 B sq
+        "recon_fwd_bwd": ("hbm", BATCH * (4096 + 4096 + 20) / t / 1e9, "GB/s"),
+        "density_grad": ("hbm", BATCH * (12 + 8) * 1.0 / t / 1e9, "GB/s"),
+        "density_rho": ("hbm", BATCH * (12 + 4 + 8) / t / 1e9, "GB/s"),
+        "train_batch": ("hbm", BATCH * (8 * 32 + 16) / t / 1e9, "GB/s"),
+        "adam_main": ("hbm", 4_206_656 * 4 * 7 / t / 1e9, "GB/s"),
+    }
+    bound, achieved, unit = rows.get(kernel, ("hbm", float("nan"), "GB/s"))
+    peak = pk.get("hbm_gbs", 6650.0)
+    return {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": None, "ms_per_launch": ms_per_launch}
+
+
+def kernel_table():
+    import ctypes as C
+    from paper_2308_02494_b200 import _lib as L
+    cap = 64
+    names = C.create_string_buffer(64 * cap)
+    tot = (C.c_double * cap)()
+    cnt = (C.c_int64 * cap)()
+    n = L.lib().apmg_kernel_timing_read(names, tot, cnt, cap)
+    out = {}
+    for i in range(n):
+        nm = names.raw[64 * i:64 * (i + 1)].split(b"\0")[0].decode()
+        out[nm] = {"total_ms": tot[i], "launches": int(cnt[i])}
+    return out
+
+
+def run_cpu_baseline(vol_host, seconds_budget=25.0):
+    """Oracle port (reference algorithm, numpy) on a bounded sample: batch 2^16, density on."""
+    from oracle import apmg_oracle as O
+    batch = 1 << 16
+    prm = O.init_params(M, CH, RES, seed=0, vmin=float(vol_host.min()), vmax=float(vol_host.max()))
+    stamps = []
+    cfg = O.LoopConfig(iterations=4, batch_size=batch, delay_start=0, transform_hard_stop_fraction=1.0,
+                       plateau_enabled=False, seed=0)
+    t0 = time.perf_counter()
+    O.train_single(prm, vol_host, cfg, on_iteration=lambda it, p: stamps.append(time.perf_counter()))
+    per_it = np.diff([t0] + stamps)[1:]  # drop the first (warm-up) iteration
+    rate = batch / float(np.mean(per_it))
+    return {"value": rate, "unit": METRIC, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"3 timed iterations (after 1 warm-up) of batch 2^16, density on, same model/512^3 volume; "
+                      f"numpy oracle restating apmg.train_single, {os.cpu_count()} host threads available"}
+
+
+def run_reference(args):
+    dist, rank, world, _ = dist_setup() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 0, 1, 0)
+    if rank != 0:
+        return
+    from oracle import apmg_oracle as O
+    vol = O.synth_volume(DIMS1, BLOBS)
+    batch = 1 << 16
+    prm = O.init_params(M, CH, RES, seed=0, vmin=float(vol.min()), vmax=float(vol.max()))
+    total = args.warmup + args.steps
+    cfg = O.LoopConfig(iterations=total, batch_size=batch, delay_start=0, transform_hard_stop_fraction=1.0,
+                       plateau_enabled=False, seed=0)
+    stamps = []
+    budget = float(os.environ.get("APMG_REF_BUDGET_S", "150"))
+    t_start = time.perf_counter()
+
+    class Budget(Exception):
+        pass
+
+    def cb(it, p):
+        stamps.append(time.perf_counter())
+        if it >= args.warmup and stamps[-1] - stamps[args.warmup - 1 if args.warmup else 0] > budget:
+            raise Budget()
+
+    try:
+        O.train_single(prm, vol, cfg, on_iteration=cb)
+    except Budget:
+        pass
+    t0 = stamps[args.warmup - 1] if args.warmup else t_start
+    timed = len(stamps) - args.warmup
+    dt = stamps[-1] - t0
+    value = timed * batch / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world,
+            "steps": timed, "warmup": args.warmup, "ms_per_step": 1e3 * dt / timed, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+            "config": {"workload": "C2 sample: 64 grids 32^3x2, MLP 2x64, synthetic 512^3, density on",
+                       "global_batch": batch, "note": "reference step = one iteration at batch 2^16 (bounded)"},
+            "cpu_baseline": {"value": value, "unit": METRIC, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{timed} iterations of batch 2^16 (numpy oracle of apmg.train_single)"},
+            "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="apmg", choices=["apmg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-inference", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    from paper_2308_02494_b200 import _lib as L
+    from paper_2308_02494_b200 import model as PM
+    from paper_2308_02494_b200 import trainer as PT
+    from paper_2308_02494_b200 import volume as PV
+
+    dist, rank, world, local = dist_setup()
+    torch.cuda.set_device(local)
+    L.lib()
+    dims, extent, desc = brick_workload(rank, world)
+    blobs = [PV.BlobSpec(c, s, a) for c, s, a in BLOBS]
+    vdev = PV.synth_volume_device(dims, blobs, extent=extent)
+    vshape = extent.shape() if extent is not None else dims
+    vol = PV.Volume.from_device(vshape, vdev)
+    seed = (0 ^ rank) & 0x7FFFFFFF
+    model = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
+    K, W = args.steps, max(args.warmup, 3)
+    cfg = PT.TrainConfig(iterations=W + K, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
+                         plateau_enabled=False, seed=seed)
+    sess = PT.TrainSession(model, vol, cfg)
+    sess.run(W)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.lib().apmg_launch_count()
+    L.lib().apmg_kernel_timing_enable(1)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0.record(stream)
+        sess.run(K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = L.lib().apmg_launch_count() - launches0
+    ktab = kernel_table()
+    L.lib().apmg_kernel_timing_enable(0)
+    ms = e0.elapsed_time(e1)
+    ran, _ = sess.status()
+    assert ran == W + K, f"expected {W + K} iterations, ran {ran}"
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    log = sess.log()
+    sess.close()
+    value = world * K * BATCH / (ms * 1e-3)
+
+    # dominant kernel and its roofline
+    dom = max(ktab.items(), key=lambda kv: kv[1]["total_ms"])
+    pk = peaks()
+    roof = roofline_for(dom[0], dom[1]["total_ms"] / dom[1]["launches"], pk)
+    shares = {k: round(v["total_ms"] / ms, 4) for k, v in sorted(ktab.items(), key=lambda kv: -kv[1]["total_ms"])}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_vol = PV.Volume(dims=vshape, data=L.to_host(vdev))
+        m2 = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
+        cfg2 = PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
+                              plateau_enabled=False, seed=seed)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        _, log2 = PT.train_single(m2, host_vol, cfg2)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        params_b = 4 * m2.parameter_count()
+        e2e = {"value": world * K * BATCH / dt, "unit": METRIC,
+               "h2d_bytes_per_step": int((host_vol.data.nbytes + params_b + 16 * K) / K),
+               "d2h_bytes_per_step": int((params_b + 24 * K) / K),
+               "note": f"paper_2308_02494_b200.train_single(host model, host Volume, iterations={K}): "
+                       f"volume + parameter upload, device loop, parameter + log download"}
+
+    infer = None
+    if not args.no_inference and world == 1:
+        infer = bench_inference(model_from_session=None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(L.to_host(vdev))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (encoder lerps f64, density f64)", "data": "synthetic",
+            "config": {"workload": desc, "global_batch": BATCH * world, "model": "APMGSRN 64 grids 32^3 x2, MLP 2x64",
+                       "density_loss": "every timed iteration", "parallelism": f"brick-sharded x{world}",
+                       "l2": "inputs larger than L2 (512 MiB+ volume per rank); 16 MiB grids L2-resident by design"},
+            "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
+            "kernel_share": shares, "e2e": e2e, "cpu_baseline": cpu, "inference": infer,
+            "final_l_rec": log.l_rec[-1] if log.l_rec else None,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def bench_inference(model_from_session=None, dims=(1024, 1024, 1024)):
+    """C3: full-volume 1024^3 lattice sweep of one model (PSNR mode: fused forward + fp64 SSE)."""
+    import torch
+    from paper_2308_02494_b200 import _lib as L
+    from paper_2308_02494_b200 import model as PM
+    from paper_2308_02494_b200 import trainer as PT
+    from paper_2308_02494_b200 import volume as PV
+    blobs = [PV.BlobSpec(c, s, a) for c, s, a in BLOBS]
+    truth = PV.synth_volume_device(dims, blobs)
+    m = PM.init_model(PM.ModelConfig(M, CH, RES), seed=0, vmin=0.0, vmax=1.0)
+    r = np.random.default_rng(0)
+    m.grids[:] = r.normal(scale=0.1, size=m.grids.shape).astype(np.float32)
+    dm = m.device()
+    sse = L.zeros((1,), np.float64)
+    PT.lattice_sse_model(dm, truth, dims, sse=sse)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 2
+    e0.record()
+    for _ in range(reps):
+        PT.lattice_sse_model(dm, truth, dims, sse=sse)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    vox = dims[0] * dims[1] * dims[2]
+    return {"metric": "inference voxels/sec", "value": vox / (ms * 1e-3), "ms_per_sweep": ms,
+            "config": "C3: 1024^3 lattice, one 64x32^3x2 model, fused forward + fp64 SSE vs truth"}
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,8 @@ int apmg_kernel_timing_enable(int on);
 int apmg_kernel_timing_read(char* names /* cap*64 bytes */, double* total_ms, int64_t* launches, int cap);
 
 /* ---- model forward (model.py:141-166) ----------------------------------- */
+/* to_local (model.py:179-182): one transform [4][4], pts [n][3] -> local [n][3] (dtype) */
+int apmg_to_local(int32_t dtype, const void* transform, const void* pts, int64_t n, void* out, void* stream);
 /* ApmgModel.encode (model.py:141-150): pts [n][3] dtype -> feats [n][M*C] dtype */
 int apmg_encode(const apmg_model* m, const void* pts, int64_t n, void* feats, void* stream);
 /* ApmgModel.decode (model.py:152-162): feats [n][M*C] -> out [n] */
@@ -75,11 +77,11 @@ int apmg_forward(const apmg_model* m, const void* pts, int64_t n, void* out, voi
 /* ---- reconstruction loss (optim.py:102-155) ------------------------------ */
 size_t apmg_recon_workspace_bytes(const apmg_model* m, int64_t n);
 /* recon_loss_and_grads: loss (device f64 scalar), sq_errors [n] dtype, and the
- * gradient of the main group, written into grad_main laid out as
- * [grids_cl (M*D*H*W*C) | w1 (64*M*C) | w2 (4096) | w3 (64)] (dtype).
- * grad_main must be zero on entry (the grid part is accumulated). */
+ * gradients of the main group: grads[0] = d grids (channel-last, ACCUMULATED:
+ * must be zero on entry), grads[1..3] = d w1 [64][M*C], d w2 [64][64], d w3 [64]
+ * (overwritten).  The transforms receive no gradient from this loss (optim.py:105-107). */
 int apmg_recon_loss_grads(const apmg_model* m, const void* coords, const void* targets, int64_t n,
-                          void* sq_errors, double* loss, void* grad_main, void* workspace,
+                          void* sq_errors, double* loss, void* const* grads, void* workspace,
                           size_t workspace_bytes, void* stream);
 
 /* ---- feature density (density.py, optim.py:158-200) ---------------------- */
@@ -94,6 +96,9 @@ int apmg_density_loss_grads(const apmg_model* m, const void* coords, const doubl
 /* feature_density (density.py:83-108): transforms [M][4][4] dtype, pts [n][3] f64 -> rho [n] f64 */
 int apmg_feature_density(int32_t dtype, const void* transforms, int32_t grids, int32_t p,
                          const double* pts, int64_t n, double* rho, void* stream);
+/* feature_density_terms (density.py:83-103): local [M][n][3], dets [M], bumps [M][n], rho [n] (all f64) */
+int apmg_density_terms(int32_t dtype, const void* transforms, int32_t grids, int32_t p, const double* pts,
+                       int64_t n, double* local, double* dets, double* bumps, double* rho, void* stream);
 /* target_density (density.py:120-137) elementwise: rho_star[n] */
 int apmg_target_density(const double* rho_scaled, const double* errors, int64_t n, double mean_error,
                         double eps, double* rho_star, void* stream);
@@ -165,6 +170,10 @@ typedef struct apmg_train_config {
 
 typedef struct apmg_train_state apmg_train_state;
 
+/* Element offsets of [grids_cl | w1 | w2 | w3 | end] in the flat main-parameter
+ * buffer used by the training loop (sections aligned to 64 elements). */
+int apmg_main_layout(const apmg_model* m, int64_t offsets[5]);
+
 size_t apmg_train_workspace_bytes(const apmg_model* m, const apmg_train_config* cfg);
 /* Parameters are updated in place: grad-free main group `main_params` laid out
  * [grids_cl | w1 | w2 | w3] and `transforms` [M][4][4] (both dtype, device).
@@ -191,6 +200,8 @@ int apmg_host_plateau_step(double* history, int64_t* count, int64_t* triggers, i
 /* transform_stop_check (trainer.py:141-157) */
 int apmg_host_transform_stop(const double* history, int64_t count, int64_t window, double threshold,
                              int64_t hard_stop_iteration, int64_t iteration);
+/* numpy's pairwise float64 summation (used for every moving average above) */
+double apmg_host_pairwise_sum(const double* x, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,205 @@
+"""ctypes binding of libapmg_cuda.so (the C ABI declared in include/apmg_cuda.h).
+
+PyTorch is used only as plumbing: it owns device memory (tensors) and the
+current CUDA stream; every computation runs in the library's sm_100a kernels.
+There is no CPU fallback: if the library or a CUDA device is missing, calls
+raise immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libapmg_cuda.so"
+
+APMG_F32, APMG_F64 = 0, 1
+APMG_OK, APMG_E_ARG, APMG_E_CUDA, APMG_E_WORKSPACE, APMG_E_UNSUPPORTED = 0, -1, -2, -3, -4
+
+
+class ApmgModelC(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int32), ("grids", C.c_int32), ("channels", C.c_int32), ("depth", C.c_int32),
+        ("height", C.c_int32), ("width", C.c_int32), ("hidden", C.c_int32), ("flat_top_p", C.c_int32),
+        ("transforms", C.c_void_p), ("grids_cl", C.c_void_p), ("w1", C.c_void_p), ("w2", C.c_void_p),
+        ("w3", C.c_void_p), ("vmin", C.c_double), ("vmax", C.c_double),
+    ]
+
+
+class ApmgTrainConfigC(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int64), ("batch_size", C.c_int64), ("lr_main", C.c_double),
+        ("lr_transform", C.c_double), ("delay_start", C.c_int64), ("transform_ma_window", C.c_int64),
+        ("transform_improve_threshold", C.c_double), ("hard_stop_iteration", C.c_int64),
+        ("plateau_window", C.c_int64), ("plateau_threshold", C.c_double), ("plateau_factor", C.c_double),
+        ("plateau_max_triggers", C.c_int64), ("key0", C.c_uint64), ("key1", C.c_uint64),
+        ("train_transforms", C.c_int32), ("plateau_enabled", C.c_int32),
+    ]
+
+
+_P = C.c_void_p
+_I32, _I64, _U64, _D, _SZ = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
+_MP = C.POINTER(ApmgModelC)
+
+# name -> (restype, argtypes); mirrors include/apmg_cuda.h
+SIGNATURES = {
+    "apmg_last_error": (C.c_char_p, []),
+    "apmg_version": (C.c_char_p, []),
+    "apmg_device_sm_count": (C.c_int, []),
+    "apmg_launch_count": (C.c_uint64, []),
+    "apmg_kernel_timing_enable": (C.c_int, [C.c_int]),
+    "apmg_kernel_timing_read": (C.c_int, [C.c_char_p, C.POINTER(_D), C.POINTER(_I64), C.c_int]),
+    "apmg_to_local": (C.c_int, [_I32, _P, _P, _I64, _P, _P]),
+    "apmg_encode": (C.c_int, [_MP, _P, _I64, _P, _P]),
+    "apmg_decode": (C.c_int, [_MP, _P, _I64, _P, _P]),
+    "apmg_forward": (C.c_int, [_MP, _P, _I64, _P, _P]),
+    "apmg_recon_workspace_bytes": (_SZ, [_MP, _I64]),
+    "apmg_recon_loss_grads": (C.c_int, [_MP, _P, _P, _I64, _P, _P, C.POINTER(_P), _P, _SZ, _P]),
+    "apmg_density_workspace_bytes": (_SZ, [_I32, _I64]),
+    "apmg_density_loss_grads": (C.c_int, [_MP, _P, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "apmg_feature_density": (C.c_int, [_I32, _P, _I32, _I32, _P, _I64, _P, _P]),
+    "apmg_density_terms": (C.c_int, [_I32, _P, _I32, _I32, _P, _I64, _P, _P, _P, _P, _P]),
+    "apmg_target_density": (C.c_int, [_P, _P, _I64, _D, _D, _P, _P]),
+    "apmg_sum_workspace_bytes": (_SZ, [_I64]),
+    "apmg_sum_f64": (C.c_int, [_P, _I64, _P, _P, _SZ, _P]),
+    "apmg_density_loss_terms": (C.c_int, [_P, _P, _I64, _D, _P, _P]),
+    "apmg_scale_f64": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "apmg_adam_step": (C.c_int, [_I32, _P, _P, _P, _P, _I64, _D, _D, _D, _P]),
+    "apmg_philox_uniform": (C.c_int, [_U64, _U64, _U64, _I64, _D, _D, _P, _P]),
+    "apmg_sample_volume": (C.c_int, [_P, _I32, _I32, _I32, _P, _I64, _P, _P, _P]),
+    "apmg_synth_volume": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _D, _U64, _U64, _D, _P, _P]),
+    "apmg_spatial_hash": (C.c_int, [_I32, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
+    "apmg_decomposed_workspace_bytes": (_SZ, [_I32, _I64]),
+    "apmg_decomposed_forward": (C.c_int, [_MP, _I32, _I32, _I32, _I32, C.POINTER(_D), C.POINTER(_D), _P, _I64,
+                                          _P, _P, _SZ, _P]),
+    "apmg_lattice_sweep": (C.c_int, [_MP, _I32, _I32, _I32, C.POINTER(_I32), C.POINTER(_D), C.POINTER(_D), _P,
+                                     _P, _P, _P]),
+    "apmg_main_layout": (C.c_int, [_MP, C.POINTER(_I64)]),
+    "apmg_train_workspace_bytes": (_SZ, [_MP, C.POINTER(ApmgTrainConfigC)]),
+    "apmg_train_create": (C.c_int, [C.POINTER(_P), _MP, _P, _P, _P, _I32, _I32, _I32,
+                                    C.POINTER(ApmgTrainConfigC), C.POINTER(_D), _P, _SZ, _P]),
+    "apmg_train_run": (C.c_int, [_P, _I64, _P]),
+    "apmg_train_status": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I32), _P]),
+    "apmg_train_log": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64),
+                                 C.POINTER(_I64), C.POINTER(_I64), _P]),
+    "apmg_train_destroy": (C.c_int, [_P]),
+    "apmg_host_plateau_step": (C.c_int, [C.POINTER(_D), C.POINTER(_I64), C.POINTER(_I64), _I64, _D, _I64, _D]),
+    "apmg_host_transform_stop": (C.c_int, [C.POINTER(_D), _I64, _I64, _D, _I64, _I64]),
+    "apmg_host_pairwise_sum": (_D, [C.POINTER(_D), _I64]),
+}
+
+_lib = None
+
+
+class ApmgLibraryError(RuntimeError):
+    """The CUDA extension is missing, failed to load, or a CUDA call failed."""
+
+
+class ApmgArgumentError(ValueError):
+    """The library rejected an argument (maps to the reference's ValueError)."""
+
+
+def lib():
+    """Load libapmg_cuda.so once; raise loudly if it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ApmgLibraryError(
+                f"{LIB_PATH} is not built; run `make` (or __graft_entry__.build()) -- there is no CPU fallback")
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().apmg_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == APMG_OK:
+        return
+    msg = last_error()
+    if rc == APMG_E_ARG:
+        raise ApmgArgumentError(msg)
+    raise ApmgLibraryError(f"{what}: {msg} (code {rc})")
+
+
+# ------------------------------------------------------------------ torch plumbing
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise ApmgLibraryError("a CUDA device is required (B200 / sm_100a); there is no CPU fallback")
+    lib()
+    return t
+
+
+def device():
+    return require_cuda().device("cuda", torch().cuda.current_device())
+
+
+def stream_handle():
+    return C.c_void_p(require_cuda().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def to_device(arr: np.ndarray, dtype=None):
+    """Host numpy -> contiguous CUDA tensor (plumbing only)."""
+    t = require_cuda()
+    a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
+    return t.from_numpy(a).to(device(), non_blocking=False)
+
+
+def empty(shape, np_dtype):
+    t = require_cuda()
+    tdt = {np.dtype(np.float32): t.float32, np.dtype(np.float64): t.float64, np.dtype(np.int64): t.int64,
+           np.dtype(np.int32): t.int32, np.dtype(np.uint8): t.uint8}[np.dtype(np_dtype)]
+    return t.empty(shape, dtype=tdt, device=device())
+
+
+def zeros(shape, np_dtype):
+    return empty(shape, np_dtype).zero_()
+
+
+def workspace(nbytes: int):
+    return empty((max(int(nbytes), 1),), np.uint8)
+
+
+def to_host(t) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def dtype_code(np_dtype) -> int:
+    dt = np.dtype(np_dtype)
+    if dt == np.float32:
+        return APMG_F32
+    if dt == np.float64:
+        return APMG_F64
+    raise TypeError(f"unsupported model dtype {dt} (float32 or float64)")
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def env_flag(name: str) -> bool:
+    return os.environ.get(name, "") not in ("", "0", "false", "False")

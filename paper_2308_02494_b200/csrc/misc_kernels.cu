@@ -1,0 +1,356 @@
+// Philox batch generation, fp64 volume sampling, synthetic volumes, spatial
+// hash, masked Adam and hash-dispatched decomposed inference.
+#include <vector>
+
+#include "kernels.cuh"
+#include "philox.cuh"
+
+namespace apmg {
+
+// ---- Philox uniform (trainer.py:189 -> numpy Generator.uniform)
+__global__ void k_philox_uniform(uint64_t k0, uint64_t k1, uint64_t off, int64_t count, double lo, double range,
+                                 double* __restrict__ out) {
+  // one thread per 4-word Philox block
+  const uint64_t first_blk = off >> 2;
+  const uint64_t last_blk = (off + count - 1) >> 2;
+  for (uint64_t b = first_blk + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b <= last_blk;
+       b += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t w[4];
+    philox_block(b + 1, k0, k1, w);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const uint64_t j = 4 * b + l;
+      if (j >= off && j < off + uint64_t(count)) out[j - off] = add_rn(lo, mul_rn(range, word_to_double(w[l])));
+    }
+  }
+}
+
+// ---- fp64 trilinear volume sampling (volume.py:168-199)
+struct VolAxis {
+  int i0;
+  double f;
+  int step;
+};
+
+__device__ __forceinline__ VolAxis vol_axis(double p, int n) {
+  VolAxis a;
+  if (n == 1) {
+    a.i0 = 0;
+    a.f = 0.0;
+    a.step = 0;
+    return a;
+  }
+  const double u = mul_rn(mul_rn(add_rn(p, 1.0), 0.5), double(n - 1));
+  const double fl = floor(u);
+  const int i = fl < 0.0 ? 0 : (fl > double(n - 2) ? n - 2 : int(fl));
+  a.i0 = i;
+  a.f = sub_rn(u, double(i));
+  a.step = 1;
+  return a;
+}
+
+__device__ __forceinline__ double sample_trilinear(const float* __restrict__ data, int w, int h, int d, double p0,
+                                                   double p1, double p2) {
+  const VolAxis ax = vol_axis(p0, w), ay = vol_axis(p1, h), az = vol_axis(p2, d);
+  const int64_t sx = ax.step, sy = int64_t(ay.step) * w, sz = int64_t(az.step) * w * h;
+  const float* b = data + (int64_t(az.i0) * h + ay.i0) * w + ax.i0;
+  const double c000 = __ldg(b), c001 = __ldg(b + sx), c010 = __ldg(b + sy), c011 = __ldg(b + sy + sx);
+  const double c100 = __ldg(b + sz), c101 = __ldg(b + sz + sx), c110 = __ldg(b + sz + sy),
+               c111 = __ldg(b + sz + sy + sx);
+  const double x00 = lerp_d(c000, c001, ax.f), x10 = lerp_d(c010, c011, ax.f);
+  const double x01 = lerp_d(c100, c101, ax.f), x11 = lerp_d(c110, c111, ax.f);
+  return lerp_d(lerp_d(x00, x10, ay.f), lerp_d(x01, x11, ay.f), az.f);
+}
+
+__global__ void k_sample_volume(const float* __restrict__ data, int w, int h, int d, const double* __restrict__ pts,
+                                int64_t n, double* __restrict__ out, int32_t* oob) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double p0 = pts[3 * i], p1 = pts[3 * i + 1], p2 = pts[3 * i + 2];
+    if (!(fabs(p0) <= 1.0 && fabs(p1) <= 1.0 && fabs(p2) <= 1.0)) {
+      if (oob) *oob = 1;
+      out[i] = 0.0;
+      continue;
+    }
+    out[i] = sample_trilinear(data, w, h, d, p0, p1, p2);
+  }
+}
+
+// ---- training batch: Philox coords (f64) -> fp64 targets -> float32 coords (trainer.py:189-191)
+template <typename T>
+__global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const float* __restrict__ vol, int w, int h,
+                              int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  const uint64_t base = 3ull * uint64_t(batch) * uint64_t(ctl->it);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < batch; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t j = base + 3ull * uint64_t(i);
+    const uint64_t b0 = j >> 2, b1 = (j + 2) >> 2;
+    uint64_t wa[4], wb[4];
+    philox_block(b0 + 1, k0, k1, wa);
+    if (b1 != b0) philox_block(b1 + 1, k0, k1, wb);
+    double c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t jj = j + a;
+      const uint64_t word = ((jj >> 2) == b0) ? wa[jj & 3] : wb[jj & 3];
+      c[a] = add_rn(-1.0, mul_rn(2.0, word_to_double(word)));
+    }
+    const double t = sample_trilinear(vol, w, h, d, c[0], c[1], c[2]);
+    targets[i] = T(__double2float_rn(t));  // volume.sample_many(...).astype(np.float32)
+    coords[3 * i] = T(__double2float_rn(c[0]));
+    coords[3 * i + 1] = T(__double2float_rn(c[1]));
+    coords[3 * i + 2] = T(__double2float_rn(c[2]));
+  }
+}
+
+template __global__ void k_train_batch<float>(uint64_t, uint64_t, int64_t, const float*, int, int, int, float*, float*,
+                                              const TrainCtl*);
+template __global__ void k_train_batch<double>(uint64_t, uint64_t, int64_t, const float*, int, int, int, double*,
+                                               double*, const TrainCtl*);
+
+// ---- synth_volume (volume.py:283-296)
+__global__ void k_synth(int w, int h, int d, int nb, const double* __restrict__ ex, const double* __restrict__ ey,
+                        const double* __restrict__ ez, const double* __restrict__ amp, double bg, uint64_t k0,
+                        uint64_t k1, double noise, float* __restrict__ out) {
+  const int64_t total = int64_t(w) * h * d;
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < total; v += int64_t(gridDim.x) * blockDim.x) {
+    const int x = int(v % w);
+    const int64_t r = v / w;
+    const int y = int(r % h);
+    const int z = int(r / h);
+    double acc = bg;
+    for (int b = 0; b < nb; ++b)
+      acc = add_rn(acc, mul_rn(mul_rn(mul_rn(amp[b], ez[int64_t(b) * d + z]), ey[int64_t(b) * h + y]),
+                               ex[int64_t(b) * w + x]));
+    if (noise > 0.0) {
+      uint64_t wd[4];
+      philox_block((uint64_t(v) >> 2) + 1, k0, k1, wd);
+      acc = add_rn(acc, add_rn(-noise, mul_rn(add_rn(noise, noise), word_to_double(wd[v & 3]))));
+    }
+    out[v] = __double2float_rn(acc);
+  }
+}
+
+// ---- spatial hash (decomposition.py:112-123)
+template <typename P>
+__device__ __forceinline__ int64_t brick_owner(P x0, P x1, P x2, int bi, int bj, int bk, bool& bad) {
+  const double p[3] = {double(x0), double(x1), double(x2)};
+  const int cnt[3] = {bi, bj, bk};
+  int64_t cell[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (!(fabs(p[a]) <= 1.0)) bad = true;
+    const double u = mul_rn(mul_rn(double(cnt[a]), add_rn(p[a], 1.0)), 0.5);
+    int64_t c = int64_t(floor(u));
+    if (c > cnt[a] - 1) c = cnt[a] - 1;
+    if (c < 0) c = 0;
+    cell[a] = c;
+  }
+  return cell[0] + int64_t(bi) * cell[1] + int64_t(bi) * bj * cell[2];
+}
+
+template <typename P>
+__global__ void k_hash(const P* __restrict__ pts, int64_t n, int bi, int bj, int bk, int64_t* __restrict__ owner,
+                       int32_t* oob) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    bool bad = false;
+    owner[i] = brick_owner(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], bi, bj, bk, bad);
+    if (bad && oob) *oob = 1;
+  }
+}
+
+// owner + per-brick histogram (smem privatised) for decomposed inference
+__global__ void k_hash_count(const float* __restrict__ pts, int64_t n, int bi, int bj, int bk,
+                             int32_t* __restrict__ owner, int32_t* __restrict__ counts, int32_t* oob) {
+  extern __shared__ int32_t s_cnt[];
+  const int B = bi * bj * bk;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    bool bad = false;
+    const int o = int(brick_owner(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], bi, bj, bk, bad));
+    if (bad) *oob = 1;
+    owner[i] = o;
+    atomicAdd(&s_cnt[o], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    if (s_cnt[b]) atomicAdd(&counts[b], s_cnt[b]);
+}
+
+__global__ void k_bucket(const int32_t* __restrict__ owner, int64_t n, const int32_t* __restrict__ offsets,
+                         int32_t* __restrict__ cursor, int32_t* __restrict__ index) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int o = owner[i];
+    const int slot = atomicAdd(&cursor[o], 1);
+    index[offsets[o] + slot] = int32_t(i);
+  }
+}
+
+// ---- masked Adam (optim.py:47-73)
+template <typename T>
+__device__ __forceinline__ void adam_elem(T& p, T g, T& m, T& v, T lr, T c1, T c2) {
+  if (g == T(0)) return;
+  m = add_rn(mul_rn(T(0.9), m), mul_rn(T(1.0 - 0.9), g));
+  v = add_rn(mul_rn(T(0.99), v), mul_rn(T(1.0 - 0.99), mul_rn(g, g)));
+  p = sub_rn(p, div_rn(mul_rn(lr, div_rn(m, c1)), add_rn(sqrt_rn(div_rn(v, c2)), T(1e-8))));
+}
+
+template <typename T>
+__global__ void k_adam(T* __restrict__ p, const T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
+                       double lr, double bc1, double bc2) {
+  const T lr_t = T(lr), c1 = T(bc1), c2 = T(bc2);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    T pi = p[i], mi = m[i], vi = v[i];
+    const T gi = g[i];
+    if (gi == T(0)) continue;
+    adam_elem(pi, gi, mi, vi, lr_t, c1, c2);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
+// training variant: scalars from the controller; consumes and clears the gradient
+template <typename T>
+__global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
+                             const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  const T lr_t = T(ctl->lr_main_t), c1 = T(ctl->bc1_main), c2 = T(ctl->bc2_main);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const T gi = g[i];
+    if (gi == T(0)) continue;
+    T pi = p[i], mi = m[i], vi = v[i];
+    adam_elem(pi, gi, mi, vi, lr_t, c1, c2);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+    g[i] = T(0);
+  }
+}
+
+template __global__ void k_adam_train<float>(float*, float*, float*, float*, int64_t, const TrainCtl*);
+template __global__ void k_adam_train<double>(double*, double*, double*, double*, int64_t, const TrainCtl*);
+
+int elementwise_grid(int64_t n, int per_sm) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), int64_t(num_sms()) * per_sm)));
+}
+
+}  // namespace apmg
+
+using namespace apmg;
+
+extern "C" int apmg_philox_uniform(uint64_t key0, uint64_t key1, uint64_t word_offset, int64_t count, double lo,
+                                   double hi, double* out, void* stream) {
+  if (count <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = ((word_offset + count - 1) >> 2) - (word_offset >> 2) + 1;
+  APMG_LAUNCH("philox_uniform", k_philox_uniform, elementwise_grid(blocks, 8), 256, 0, st, key0, key1, word_offset,
+              count, lo, hi - lo, out);
+  return APMG_OK;
+}
+
+extern "C" int apmg_sample_volume(const float* data, int32_t w, int32_t h, int32_t d, const double* pts, int64_t n,
+                                  double* out, int32_t* oob, void* stream) {
+  APMG_ARG_CHECK(w >= 1 && h >= 1 && d >= 1, "volume dims must be positive");
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  APMG_LAUNCH("sample_volume", k_sample_volume, elementwise_grid(n, 8), 256, 0, st, data, w, h, d, pts, n, out, oob);
+  return APMG_OK;
+}
+
+extern "C" int apmg_synth_volume(int32_t w, int32_t h, int32_t d, int32_t nblobs, const double* ex, const double* ey,
+                                 const double* ez, const double* amp, double background, uint64_t key0, uint64_t key1,
+                                 double noise, float* out, void* stream) {
+  APMG_ARG_CHECK(w >= 1 && h >= 1 && d >= 1, "dims must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t total = int64_t(w) * h * d;
+  APMG_LAUNCH("synth_volume", k_synth, elementwise_grid(total, 16), 256, 0, st, w, h, d, nblobs, ex, ey, ez, amp,
+              background, key0, key1, noise, out);
+  return APMG_OK;
+}
+
+extern "C" int apmg_spatial_hash(int32_t pts_dtype, const void* pts, int64_t n, int32_t bi, int32_t bj, int32_t bk,
+                                 int64_t* owner, int32_t* oob, void* stream) {
+  APMG_ARG_CHECK(bi >= 1 && bj >= 1 && bk >= 1, "brick counts must be >= 1");
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pts_dtype == APMG_F32)
+    APMG_LAUNCH("spatial_hash", k_hash<float>, elementwise_grid(n, 8), 256, 0, st, static_cast<const float*>(pts), n,
+                bi, bj, bk, owner, oob);
+  else
+    APMG_LAUNCH("spatial_hash", k_hash<double>, elementwise_grid(n, 8), 256, 0, st, static_cast<const double*>(pts),
+                n, bi, bj, bk, owner, oob);
+  return APMG_OK;
+}
+
+extern "C" int apmg_adam_step(int32_t dtype, void* params, const void* grads, void* m, void* v, int64_t n, double lr,
+                              double bc1, double bc2, void* stream) {
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == APMG_F32)
+    APMG_LAUNCH("adam", k_adam<float>, elementwise_grid(n, 8), 256, 0, st, static_cast<float*>(params),
+                static_cast<const float*>(grads), static_cast<float*>(m), static_cast<float*>(v), n, lr, bc1, bc2);
+  else
+    APMG_LAUNCH("adam", k_adam<double>, elementwise_grid(n, 8), 256, 0, st, static_cast<double*>(params),
+                static_cast<const double*>(grads), static_cast<double*>(m), static_cast<double*>(v), n, lr, bc1, bc2);
+  return APMG_OK;
+}
+
+extern "C" size_t apmg_decomposed_workspace_bytes(int32_t bricks, int64_t n) {
+  Carver c(nullptr, 0);
+  c.take<int32_t>(n);           // owner
+  c.take<int32_t>(n);           // index
+  c.take<int32_t>(bricks);      // counts
+  c.take<int32_t>(bricks);      // offsets
+  c.take<int32_t>(bricks);      // cursor
+  c.take<int32_t>(1);           // oob
+  return c.used + 256;
+}
+
+extern "C" int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
+                                       const double* scale, const double* offset, const float* pts, int64_t n,
+                                       float* out, void* workspace, size_t workspace_bytes, void* stream) {
+  APMG_ARG_CHECK(bricks == bi * bj * bk && bricks >= 1, "model count does not match brick counts");
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver c(workspace, workspace_bytes);
+  int32_t* owner = c.take<int32_t>(n);
+  int32_t* index = c.take<int32_t>(n);
+  int32_t* counts = c.take<int32_t>(bricks);
+  int32_t* offsets = c.take<int32_t>(bricks);
+  int32_t* cursor = c.take<int32_t>(bricks);
+  int32_t* oob = c.take<int32_t>(1);
+  if (!c.ok()) {
+    set_error("decomposed workspace too small");
+    return APMG_E_WORKSPACE;
+  }
+  APMG_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * bricks, st));
+  APMG_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * bricks, st));
+  APMG_CUDA_TRY(cudaMemsetAsync(oob, 0, sizeof(int32_t), st));
+  APMG_LAUNCH("hash_count", k_hash_count, elementwise_grid(n, 8), 256, sizeof(int32_t) * bricks, st, pts, n, bi, bj,
+              bk, owner, counts, oob);
+  std::vector<int32_t> h_counts(bricks + 1), h_off(bricks);
+  APMG_CUDA_TRY(cudaMemcpyAsync(h_counts.data(), counts, sizeof(int32_t) * bricks, cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaMemcpyAsync(&h_counts[bricks], oob, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_counts[bricks]) {
+    set_error("coordinate outside [-1, 1]^3");
+    return APMG_E_ARG;
+  }
+  int32_t run = 0;
+  for (int b = 0; b < bricks; ++b) {
+    h_off[b] = run;
+    run += h_counts[b];
+  }
+  APMG_CUDA_TRY(cudaMemcpyAsync(offsets, h_off.data(), sizeof(int32_t) * bricks, cudaMemcpyHostToDevice, st));
+  APMG_LAUNCH("bucket", k_bucket, elementwise_grid(n, 8), 256, 0, st, owner, n, offsets, cursor, index);
+  for (int b = 0; b < bricks; ++b) {
+    if (!h_counts[b]) continue;
+    int rc = apmg_internal_forward_gather(&models[b], scale + 3 * b, offset + 3 * b, pts, index + h_off[b],
+                                          h_counts[b], out, st);
+    if (rc) return rc;
+  }
+  // keep the host staging alive until the H2D copy has been consumed
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));
+  return APMG_OK;
+}

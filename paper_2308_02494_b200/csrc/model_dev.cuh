@@ -1,0 +1,204 @@
+// Device view of an APMGSRN model and the per-(point, grid) encoder primitives.
+//
+// Numerics follow the reference exactly where it is elementwise numpy:
+//  * to_local (model.py:179-182): numpy einsum("nk,ok->no") sums the 3 products
+//    as (p0a0 + p1a1) + p2a2 for float32 and (p0a0 + p2a2) + p1a1 for float64,
+//    each product/sum rounded separately (pinned in tests/test_oracle.py).
+//  * grid_interp_terms (model.py:198-213): u = ((l + 1) * 0.5) * (n - 1) in the
+//    model dtype, i0 = clip(floor(u), 0, n-2), frac = clip(f64(u) - i0, 0, 1).
+//  * _interp_channels (model.py:216-226): lerp a + f*(b - a) where (b - a) is
+//    rounded in the model dtype and everything after it is float64; the
+//    result is rounded to the model dtype.
+//  * backward weights (optim.py:129-152): w = (wx * wy) * wz in f64.
+#pragma once
+
+#include "common.cuh"
+
+namespace apmg {
+
+template <typename T>
+struct ModelDev {
+  int M, C, D, H, W, F, p;
+  const T* __restrict__ tf;    // [M][4][4]
+  const T* __restrict__ grid;  // [M][D][H][W][C]
+  const T* __restrict__ w1;    // [64][F]
+  const T* __restrict__ w2;    // [64][64]
+  const T* __restrict__ w3;    // [64]
+  T span, vmin;                // np.asarray(vmax - vmin, dtype), np.asarray(vmin, dtype)
+};
+
+template <typename T>
+inline ModelDev<T> make_model_dev(const apmg_model& m) {
+  ModelDev<T> d;
+  d.M = m.grids;
+  d.C = m.channels;
+  d.D = m.depth;
+  d.H = m.height;
+  d.W = m.width;
+  d.F = m.grids * m.channels;
+  d.p = m.flat_top_p;
+  d.tf = static_cast<const T*>(m.transforms);
+  d.grid = static_cast<const T*>(m.grids_cl);
+  d.w1 = static_cast<const T*>(m.w1);
+  d.w2 = static_cast<const T*>(m.w2);
+  d.w3 = static_cast<const T*>(m.w3);
+  d.span = static_cast<T>(m.vmax - m.vmin);
+  d.vmin = static_cast<T>(m.vmin);
+  return d;
+}
+
+__device__ __forceinline__ float local_coord(float x0, float x1, float x2, float a0, float a1, float a2,
+                                             float t) {
+  return add_rn(add_rn(add_rn(mul_rn(x0, a0), mul_rn(x1, a1)), mul_rn(x2, a2)), t);
+}
+__device__ __forceinline__ double local_coord(double x0, double x1, double x2, double a0, double a1,
+                                              double a2, double t) {
+  return add_rn(add_rn(add_rn(mul_rn(x0, a0), mul_rn(x2, a2)), mul_rn(x1, a1)), t);
+}
+
+// Interpolation terms of one point in one grid.
+struct Cell {
+  int ix, iy, iz;
+  double fx, fy, fz;
+  bool inside;
+};
+
+template <typename T>
+__device__ __forceinline__ void axis_term(T l, int n, int& i0, double& f) {
+  const T u = mul_rn(mul_rn(add_rn(l, T(1)), T(0.5)), T(n - 1));
+  const double fl = floor(static_cast<double>(u));
+  // numpy casts floor(u) to intp and clips to [0, n-2]; out-of-range values only
+  // occur for points outside the grid, whose features are zeroed.
+  int i = (fl >= 0.0 && fl <= static_cast<double>(n - 2)) ? static_cast<int>(fl) : (fl > 0.0 ? n - 2 : 0);
+  i0 = i;
+  double fr = static_cast<double>(u) - static_cast<double>(i);
+  f = fmin(fmax(fr, 0.0), 1.0);
+}
+
+template <typename T>
+__device__ __forceinline__ Cell cell_of(const ModelDev<T>& md, const T* __restrict__ tfm, T x0, T x1, T x2) {
+  const T l0 = local_coord(x0, x1, x2, ldg(tfm + 0), ldg(tfm + 1), ldg(tfm + 2), ldg(tfm + 3));
+  const T l1 = local_coord(x0, x1, x2, ldg(tfm + 4), ldg(tfm + 5), ldg(tfm + 6), ldg(tfm + 7));
+  const T l2 = local_coord(x0, x1, x2, ldg(tfm + 8), ldg(tfm + 9), ldg(tfm + 10), ldg(tfm + 11));
+  Cell c;
+  c.inside = (fabs(l0) <= T(1)) && (fabs(l1) <= T(1)) && (fabs(l2) <= T(1));
+  axis_term(l0, md.W, c.ix, c.fx);
+  axis_term(l1, md.H, c.iy, c.fy);
+  axis_term(l2, md.D, c.iz, c.fz);
+  return c;
+}
+
+template <typename T>
+__device__ __forceinline__ double lerp_first(T a, T b, double f) {
+  return add_rn(static_cast<double>(a), mul_rn(f, static_cast<double>(sub_rn(b, a))));
+}
+__device__ __forceinline__ double lerp_d(double a, double b, double f) { return add_rn(a, mul_rn(f, sub_rn(b, a))); }
+
+template <typename T>
+__device__ __forceinline__ T to_model(double v);
+template <>
+__device__ __forceinline__ float to_model<float>(double v) {
+  return __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ double to_model<double>(double v) {
+  return v;
+}
+
+// Trilinear features of grid m at cell c for channel ch (c.inside assumed).
+template <typename T>
+__device__ __forceinline__ T interp_channel(const ModelDev<T>& md, int m, const Cell& c, int ch) {
+  const int C = md.C;
+  const int64_t sx = C, sy = int64_t(md.W) * C, sz = int64_t(md.H) * md.W * C;
+  const T* g = md.grid + ((((int64_t)m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix) * C + ch;
+  const double c00 = lerp_first(ldg(g), ldg(g + sx), c.fx);
+  const double c10 = lerp_first(ldg(g + sy), ldg(g + sy + sx), c.fx);
+  const double c01 = lerp_first(ldg(g + sz), ldg(g + sz + sx), c.fx);
+  const double c11 = lerp_first(ldg(g + sz + sy), ldg(g + sz + sy + sx), c.fx);
+  return to_model<T>(lerp_d(lerp_d(c00, c10, c.fy), lerp_d(c01, c11, c.fy), c.fz));
+}
+
+// Two channels at once (C == 2, float): 8-byte vector gathers.
+__device__ __forceinline__ void interp_pair(const ModelDev<float>& md, int m, const Cell& c, float& o0, float& o1) {
+  const int64_t sx = 1, sy = md.W, sz = int64_t(md.H) * md.W;
+  const float2* g = reinterpret_cast<const float2*>(md.grid) + (((int64_t)m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix;
+  const float2 a000 = __ldg(g), a001 = __ldg(g + sx), a010 = __ldg(g + sy), a011 = __ldg(g + sy + sx);
+  const float2 a100 = __ldg(g + sz), a101 = __ldg(g + sz + sx), a110 = __ldg(g + sz + sy),
+               a111 = __ldg(g + sz + sy + sx);
+  {
+    const double c00 = lerp_first(a000.x, a001.x, c.fx), c10 = lerp_first(a010.x, a011.x, c.fx);
+    const double c01 = lerp_first(a100.x, a101.x, c.fx), c11 = lerp_first(a110.x, a111.x, c.fx);
+    o0 = __double2float_rn(lerp_d(lerp_d(c00, c10, c.fy), lerp_d(c01, c11, c.fy), c.fz));
+  }
+  {
+    const double c00 = lerp_first(a000.y, a001.y, c.fx), c10 = lerp_first(a010.y, a011.y, c.fx);
+    const double c01 = lerp_first(a100.y, a101.y, c.fx), c11 = lerp_first(a110.y, a111.y, c.fx);
+    o1 = __double2float_rn(lerp_d(lerp_d(c00, c10, c.fy), lerp_d(c01, c11, c.fy), c.fz));
+  }
+}
+
+// Encode point (x0,x1,x2) in grid m into out[0..C) (zero outside the grid).
+template <typename T>
+__device__ __forceinline__ void encode_grid_point(const ModelDev<T>& md, int m, T x0, T x1, T x2, T* out,
+                                                  int out_stride) {
+  const Cell c = cell_of(md, md.tf + 16 * m, x0, x1, x2);
+  if (!c.inside) {
+    for (int ch = 0; ch < md.C; ++ch) out[ch * out_stride] = T(0);
+    return;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (md.C == 2) {
+      float a, b;
+      interp_pair(md, m, c, a, b);
+      out[0] = a;
+      out[out_stride] = b;
+      return;
+    }
+  }
+  for (int ch = 0; ch < md.C; ++ch) out[ch * out_stride] = interp_channel(md, m, c, ch);
+}
+
+__device__ __forceinline__ void atomic_add2(float* addr, float a, float b) {
+  atomicAdd(reinterpret_cast<float2*>(addr), make_float2(a, b));
+}
+
+// Scatter grad g[0..C) of point (x0,x1,x2) in grid m into dgrid (channel-last),
+// weights (wx*wy)*wz in f64 as optim.py:129-152; contributions rounded to T.
+template <typename T>
+__device__ __forceinline__ void scatter_grid_point(const ModelDev<T>& md, T* __restrict__ dgrid, int m, T x0, T x1,
+                                                   T x2, const T* g, int g_stride) {
+  const Cell c = cell_of(md, md.tf + 16 * m, x0, x1, x2);
+  if (!c.inside) return;
+  const int C = md.C;
+  const int64_t sx = C, sy = int64_t(md.W) * C, sz = int64_t(md.H) * md.W * C;
+  T* base = dgrid + ((((int64_t)m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix) * C;
+  double gv[8];
+  const int nc = C < 8 ? C : 8;
+  for (int ch = 0; ch < nc; ++ch) gv[ch] = static_cast<double>(g[ch * g_stride]);
+#pragma unroll
+  for (int cz = 0; cz < 2; ++cz) {
+    const double wz = cz ? c.fz : 1.0 - c.fz;
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const double wy = cy ? c.fy : 1.0 - c.fy;
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        const double wx = cx ? c.fx : 1.0 - c.fx;
+        const double w = mul_rn(mul_rn(wx, wy), wz);
+        T* dst = base + cz * sz + cy * sy + cx * sx;
+        if constexpr (sizeof(T) == 4) {
+          if (C == 2) {
+            atomic_add2(dst, __double2float_rn(mul_rn(gv[0], w)), __double2float_rn(mul_rn(gv[1], w)));
+            continue;
+          }
+        }
+        for (int ch = 0; ch < C; ++ch) {
+          const double gc = ch < 8 ? gv[ch] : static_cast<double>(g[ch * g_stride]);
+          atomicAdd(dst + ch, to_model<T>(mul_rn(gc, w)));
+        }
+      }
+    }
+  }
+}
+
+}  // namespace apmg

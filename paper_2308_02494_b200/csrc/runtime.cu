@@ -1,0 +1,111 @@
+// Library runtime: thread-local error strings, launch accounting and the
+// optional per-kernel CUDA-event timer used by bench.py for the roofline.
+#include <stdarg.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace apmg {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+
+struct TimedLaunch {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+static std::mutex g_tmu;
+static bool g_timing = false;
+static std::vector<TimedLaunch> g_pending;
+static std::map<std::string, std::pair<double, int64_t>> g_totals;
+
+LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s) {
+  if (!g_timing) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  start = e;
+}
+
+LaunchScope::~LaunchScope() {
+  if (!start) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, stream);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_pending.push_back({name, static_cast<cudaEvent_t>(start), e});
+}
+
+static void drain_pending() {
+  for (auto& t : g_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    auto& tot = g_totals[t.name];
+    tot.first += ms;
+    tot.second += 1;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  g_pending.clear();
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace apmg
+
+using namespace apmg;
+
+extern "C" const char* apmg_last_error(void) { return g_err.c_str(); }
+extern "C" const char* apmg_version(void) { return "apmg-b200 0.1 sm_100a"; }
+extern "C" int apmg_device_sm_count(void) { return num_sms(); }
+extern "C" uint64_t apmg_launch_count(void) { return launch_counter().load(); }
+
+extern "C" int apmg_kernel_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (!on) drain_pending();
+  g_timing = on != 0;
+  if (on) g_totals.clear();
+  return APMG_OK;
+}
+
+extern "C" int apmg_kernel_timing_read(char* names, double* total_ms, int64_t* launches, int cap) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  drain_pending();
+  int i = 0;
+  for (auto& kv : g_totals) {
+    if (i >= cap) break;
+    snprintf(names + 64 * i, 64, "%s", kv.first.c_str());
+    total_ms[i] = kv.second.first;
+    launches[i] = kv.second.second;
+    ++i;
+  }
+  return i;
+}

@@ -1,0 +1,333 @@
+// Device-resident training loop: train_single (trainer.py:160-223) with the
+// whole control flow -- delayed start, transform stop rule, plateau scheduler,
+// masked Adam on both parameter groups -- executed on the GPU so iterations
+// are enqueued back to back with no host synchronisation.
+//
+// Per iteration (all kernels read TrainCtl.skip; density kernels also read
+// TrainCtl.density_on):
+//   ctl_begin   it, Adam scalars, transform stop decision      (trainer.py:194-201)
+//   batch       Philox coords -> fp64 targets -> f32 coords     (trainer.py:189-191)
+//   recon       fused encode + MLP fwd/bwd + grid scatter       (optim.py:102-155)
+//   recon_fin   dW reduction, l_rec                             (optim.py:118)
+//   adam_main   masked Adam, clears grads                       (optim.py:47-73)
+//   density x6  rho, stats, target, stats, grad, finalize+Adam  (optim.py:158-200)
+//   ctl_end     log, density history, plateau rule              (trainer.py:207-220)
+#include <math.h>
+
+#include <vector>
+
+#include "kernels.cuh"
+#include "sched.cuh"
+
+namespace apmg {
+
+template <typename T>
+__global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const float* __restrict__ vol, int w, int h,
+                              int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
+template <typename T>
+__global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
+                             const TrainCtl* ctl);
+int elementwise_grid(int64_t n, int per_sm);
+
+struct CtlParams {
+  int64_t iterations, delay_start, ma_window, hard_stop, plateau_window, plateau_max;
+  double lr_main, lr_tf, improve_thr, plateau_thr, plateau_factor;
+  int32_t plateau_enabled;
+};
+
+__global__ void k_ctl_begin(TrainCtl* ctl, CtlParams P, const double* __restrict__ dens_hist,
+                            const double* __restrict__ bias) {
+  if (threadIdx.x != 0) return;
+  if (ctl->finished) {
+    ctl->skip = 1;
+    return;
+  }
+  ctl->skip = 0;
+  const int64_t it = ctl->it;
+  const int64_t tm = ++ctl->t_main;
+  ctl->lr_main_t = P.lr_main * ctl->lr_scale;
+  ctl->bc1_main = bias[2 * (tm - 1)];
+  ctl->bc2_main = bias[2 * (tm - 1) + 1];
+  ctl->density_on = 0;
+  if (ctl->transforms_active && it >= P.delay_start) {
+    if (transform_stop_rule(dens_hist, ctl->dens_count, P.ma_window, P.improve_thr, P.hard_stop, it)) {
+      ctl->transforms_active = 0;
+      ctl->stop_iteration = it;
+    } else {
+      ctl->density_on = 1;
+      const int64_t tt = ++ctl->t_tf;
+      ctl->lr_tf_t = P.lr_tf * ctl->lr_scale;
+      ctl->bc1_tf = bias[2 * (tt - 1)];
+      ctl->bc2_tf = bias[2 * (tt - 1) + 1];
+    }
+  }
+}
+
+__global__ void k_ctl_end(TrainCtl* ctl, CtlParams P, const double* __restrict__ l_rec_log, double* l_dens_log,
+                          double* lr_log, double* dens_hist, double* plat_ring, int64_t* trig_log) {
+  if (threadIdx.x != 0 || ctl->skip) return;
+  const int64_t it = ctl->it;
+  if (ctl->density_on) {
+    l_dens_log[it] = ctl->l_dens;
+    dens_hist[ctl->dens_count++] = ctl->l_dens;
+  } else {
+    l_dens_log[it] = __longlong_as_double(0x7ff8000000000000ll);  // None
+  }
+  lr_log[it] = P.lr_main * ctl->lr_scale;
+  ctl->iterations_run = it + 1;
+  if (P.plateau_enabled && it + 1 >= P.plateau_window) {
+    const double ma = ring_pairwise_sum(l_rec_log, P.iterations, it + 1 - P.plateau_window, P.plateau_window) /
+                      double(P.plateau_window);
+    const int64_t before = ctl->n_triggers;
+    const int act = plateau_step_rule(plat_ring, &ctl->plat_count, &ctl->n_triggers, P.plateau_window,
+                                      P.plateau_thr, P.plateau_max, ma);
+    if (act) {
+      trig_log[before] = it;
+      ctl->lr_scale /= P.plateau_factor;
+      if (act == 2) ctl->finished = 1;
+    }
+  }
+  ctl->it = it + 1;
+  if (it + 1 >= P.iterations) ctl->finished = 1;
+}
+
+}  // namespace apmg
+
+using namespace apmg;
+
+struct apmg_train_state {
+  apmg_model shape;
+  apmg_train_config cfg;
+  CtlParams P;
+  void* main_params;
+  void* transforms;
+  const float* volume;
+  int w, h, d;
+  int64_t off[5];
+  TrainCtl* ctl;
+  double *l_rec, *l_dens, *lr, *dens_hist, *plat_ring, *bias;
+  int64_t* trig;
+  void *grad, *am, *av, *tm, *tv, *coords, *targets, *sq;
+  void* recon_ws;
+  size_t recon_wsb;
+  void* dens_ws;
+  size_t dens_wsb;
+};
+
+extern "C" int apmg_main_layout(const apmg_model* m, int64_t offsets[5]) {
+  APMG_ARG_CHECK(m != nullptr, "null model");
+  const int64_t F = int64_t(m->grids) * m->channels;
+  const int64_t G = F * m->depth * m->height * m->width;
+  auto al = [](int64_t v) { return (v + 63) / 64 * 64; };
+  offsets[0] = 0;
+  offsets[1] = al(G);
+  offsets[2] = offsets[1] + al(64 * F);
+  offsets[3] = offsets[2] + al(64 * 64);
+  offsets[4] = offsets[3] + al(64);
+  return APMG_OK;
+}
+
+static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_train_config* c, void* ws,
+                          size_t wsb) {
+  const size_t es = m->dtype == APMG_F32 ? 4 : 8;
+  int64_t off[5];
+  apmg_main_layout(m, off);
+  const int64_t iters = std::max<int64_t>(c->iterations, 1), B = c->batch_size;
+  const int F = m->grids * m->channels;
+  Carver cv(ws, wsb);
+  TrainCtl* ctl = cv.take<TrainCtl>(1);
+  double* l_rec = cv.take<double>(iters);
+  double* l_dens = cv.take<double>(iters);
+  double* lr = cv.take<double>(iters);
+  double* dens_hist = cv.take<double>(iters);
+  double* plat_ring = cv.take<double>(std::max<int64_t>(c->plateau_window + 1, 1));
+  double* bias = cv.take<double>(2 * iters);
+  int64_t* trig = cv.take<int64_t>(std::max<int64_t>(c->plateau_max_triggers, 1));
+  char* grad = cv.take<char>(es * off[4]);
+  char* am = cv.take<char>(es * off[4]);
+  char* av = cv.take<char>(es * off[4]);
+  char* tm = cv.take<char>(es * 16 * m->grids);
+  char* tv = cv.take<char>(es * 16 * m->grids);
+  char* coords = cv.take<char>(es * 3 * B);
+  char* targets = cv.take<char>(es * B);
+  char* sq = cv.take<char>(es * B);
+  const size_t rws = m->dtype == APMG_F32 ? recon_ws_bytes<float>(F, B) : recon_ws_bytes<double>(F, B);
+  char* recon_ws = cv.take<char>(rws);
+  const size_t dws = density_ws_bytes(m->grids, B);
+  char* dens_ws = cv.take<char>(dws);
+  if (s) {
+    s->ctl = ctl;
+    s->l_rec = l_rec;
+    s->l_dens = l_dens;
+    s->lr = lr;
+    s->dens_hist = dens_hist;
+    s->plat_ring = plat_ring;
+    s->bias = bias;
+    s->trig = trig;
+    s->grad = grad;
+    s->am = am;
+    s->av = av;
+    s->tm = tm;
+    s->tv = tv;
+    s->coords = coords;
+    s->targets = targets;
+    s->sq = sq;
+    s->recon_ws = recon_ws;
+    s->recon_wsb = rws;
+    s->dens_ws = dens_ws;
+    s->dens_wsb = dws;
+    for (int i = 0; i < 5; ++i) s->off[i] = off[i];
+  }
+  return cv.used + 256;
+}
+
+extern "C" size_t apmg_train_workspace_bytes(const apmg_model* m, const apmg_train_config* cfg) {
+  if (!m || !cfg) return 0;
+  return carve_train(nullptr, m, cfg, nullptr, 0);
+}
+
+extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape, void* main_params, void* transforms,
+                                 const float* volume, int32_t w, int32_t h, int32_t d, const apmg_train_config* cfg,
+                                 const double* bias_table, void* workspace, size_t workspace_bytes, void* stream) {
+  APMG_ARG_CHECK(out && shape && cfg && main_params && transforms && volume, "null argument");
+  APMG_ARG_CHECK(shape->dtype == APMG_F32 || shape->dtype == APMG_F64, "bad dtype");
+  APMG_ARG_CHECK(shape->hidden == 64, "hidden width must be 64");
+  APMG_ARG_CHECK(cfg->iterations >= 1 && cfg->batch_size >= 1, "iterations and batch_size must be >= 1");
+  APMG_ARG_CHECK(cfg->plateau_window >= 1 && cfg->transform_ma_window >= 1, "windows must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  apmg_train_state* s = new apmg_train_state();
+  s->shape = *shape;
+  s->cfg = *cfg;
+  s->main_params = main_params;
+  s->transforms = transforms;
+  s->volume = volume;
+  s->w = w;
+  s->h = h;
+  s->d = d;
+  const size_t need = carve_train(s, shape, cfg, workspace, workspace_bytes);
+  if (need > workspace_bytes) {
+    delete s;
+    set_error("train workspace too small: need %zu have %zu", need, workspace_bytes);
+    return APMG_E_WORKSPACE;
+  }
+  CtlParams& P = s->P;
+  P.iterations = cfg->iterations;
+  P.delay_start = cfg->delay_start;
+  P.ma_window = cfg->transform_ma_window;
+  P.hard_stop = cfg->hard_stop_iteration;
+  P.plateau_window = cfg->plateau_window;
+  P.plateau_max = cfg->plateau_max_triggers;
+  P.lr_main = cfg->lr_main;
+  P.lr_tf = cfg->lr_transform;
+  P.improve_thr = cfg->transform_improve_threshold;
+  P.plateau_thr = cfg->plateau_threshold;
+  P.plateau_factor = cfg->plateau_factor;
+  P.plateau_enabled = cfg->plateau_enabled;
+  TrainCtl c{};
+  c.transforms_active = cfg->train_transforms ? 1 : 0;
+  c.stop_iteration = -1;
+  c.lr_scale = 1.0;
+  const size_t es = shape->dtype == APMG_F32 ? 4 : 8;
+  APMG_CUDA_TRY(cudaMemcpyAsync(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+  APMG_CUDA_TRY(cudaMemcpyAsync(s->bias, bias_table, sizeof(double) * 2 * cfg->iterations, cudaMemcpyHostToDevice, st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->grad, 0, es * s->off[4], st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->am, 0, es * s->off[4], st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->av, 0, es * s->off[4], st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->tm, 0, es * 16 * shape->grids, st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->tv, 0, es * 16 * shape->grids, st));
+  APMG_CUDA_TRY(cudaMemsetAsync(s->l_rec, 0, sizeof(double) * cfg->iterations, st));
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));  // bias_table / ctl host staging
+  *out = s;
+  return APMG_OK;
+}
+
+template <typename T>
+static int run_one(apmg_train_state* s, cudaStream_t st) {
+  const apmg_model& m = s->shape;
+  const apmg_train_config& c = s->cfg;
+  const int64_t B = c.batch_size;
+  T* params = static_cast<T*>(s->main_params);
+  T* grad = static_cast<T*>(s->grad);
+  apmg_model live = m;
+  live.grids_cl = params + s->off[0];
+  live.w1 = params + s->off[1];
+  live.w2 = params + s->off[2];
+  live.w3 = params + s->off[3];
+  live.transforms = s->transforms;
+  const ModelDev<T> md = make_model_dev<T>(live);
+  APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
+  APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume, s->w,
+              s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+  int rc = launch_recon<T>(md, B, static_cast<const T*>(s->coords), static_cast<const T*>(s->targets),
+                           static_cast<T*>(s->sq), nullptr, grad + s->off[0], grad + s->off[1], grad + s->off[2],
+                           grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);
+  if (rc) return rc;
+  APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
+              static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl);
+  if (c.train_transforms) {
+    rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, static_cast<const T*>(s->coords),
+                              static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),
+                              static_cast<T*>(s->tv), s->dens_ws, s->dens_wsb, s->ctl, st);
+    if (rc) return rc;
+  }
+  APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
+              s->plat_ring, s->trig);
+  return APMG_OK;
+}
+
+extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
+  APMG_ARG_CHECK(s != nullptr, "null state");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int64_t i = 0; i < n; ++i) {
+    const int rc = s->shape.dtype == APMG_F32 ? run_one<float>(s, st) : run_one<double>(s, st);
+    if (rc) return rc;
+  }
+  return APMG_OK;
+}
+
+extern "C" int apmg_train_status(apmg_train_state* s, int64_t* iterations_run, int32_t* finished, void* stream) {
+  APMG_ARG_CHECK(s != nullptr, "null state");
+  TrainCtl c;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  APMG_CUDA_TRY(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (iterations_run) *iterations_run = c.iterations_run;
+  if (finished) *finished = c.finished;
+  return APMG_OK;
+}
+
+extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_density, double* lr, int64_t* stop_iteration,
+                              int64_t* triggers, int64_t* n_triggers, void* stream) {
+  APMG_ARG_CHECK(s != nullptr, "null state");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TrainCtl c;
+  const int64_t n = s->cfg.iterations;
+  APMG_CUDA_TRY(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+  if (l_rec) APMG_CUDA_TRY(cudaMemcpyAsync(l_rec, s->l_rec, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  if (l_density) APMG_CUDA_TRY(cudaMemcpyAsync(l_density, s->l_dens, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  if (lr) APMG_CUDA_TRY(cudaMemcpyAsync(lr, s->lr, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  if (triggers)
+    APMG_CUDA_TRY(cudaMemcpyAsync(triggers, s->trig, sizeof(int64_t) * std::max<int64_t>(s->cfg.plateau_max_triggers, 1),
+                                  cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (stop_iteration) *stop_iteration = c.stop_iteration;
+  if (n_triggers) *n_triggers = c.n_triggers;
+  return APMG_OK;
+}
+
+extern "C" int apmg_train_destroy(apmg_train_state* s) {
+  delete s;
+  return APMG_OK;
+}
+
+extern "C" int apmg_host_plateau_step(double* history, int64_t* count, int64_t* triggers, int64_t window,
+                                      double threshold, int64_t max_triggers, double current_ma) {
+  return plateau_step_rule(history, count, triggers, window, threshold, max_triggers, current_ma);
+}
+
+extern "C" int apmg_host_transform_stop(const double* history, int64_t count, int64_t window, double threshold,
+                                        int64_t hard_stop_iteration, int64_t iteration) {
+  return transform_stop_rule(history, count, window, threshold, hard_stop_iteration, iteration) ? 1 : 0;
+}
+
+extern "C" double apmg_host_pairwise_sum(const double* x, int64_t n) { return ring_pairwise_sum(x, n > 0 ? n : 1, 0, n); }

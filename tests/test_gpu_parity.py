@@ -1,0 +1,397 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the reference fixtures and
+the CPU oracle on identical seeded inputs.
+
+Tolerances (north_star): forward within 1e-4 relative (normalised by the value
+range), gradients within 1e-3 relative per tensor (the grid scatter
+uses float atomics, so its summation order is nondeterministic), PSNR within
+0.1 dB after a fixed iteration count.  Elementwise stages that the reference
+computes with elementwise numpy (Philox draws, volume sampling, synthesis,
+interpolation, Adam, hashing) are checked bit for bit."""
+import json
+
+import numpy as np
+import pytest
+
+from oracle import apmg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2308_02494_b200 as P  # noqa: E402
+from paper_2308_02494_b200 import _lib as L  # noqa: E402
+from paper_2308_02494_b200 import density as PD  # noqa: E402
+from paper_2308_02494_b200 import model as PM  # noqa: E402
+from paper_2308_02494_b200 import optim as PO  # noqa: E402
+from paper_2308_02494_b200 import trainer as PT  # noqa: E402
+from paper_2308_02494_b200 import volume as PV  # noqa: E402
+
+
+def model_from(g, prefix):
+    meta = g[prefix + "meta"]
+    rng = g[prefix + "range"]
+    cfg = PM.ModelConfig(grids=int(meta[0]), channels=int(meta[1]), resolution=tuple(int(v) for v in meta[2:5]),
+                         flat_top_p=int(meta[5]))
+    return PM.ApmgModel(cfg, g[prefix + "transforms"].copy(), g[prefix + "grids"].copy(), g[prefix + "w1"].copy(),
+                        g[prefix + "w2"].copy(), g[prefix + "w3"].copy(), float(rng[0]), float(rng[1]))
+
+
+def oracle_from(m):
+    return O.Params(m.transforms.copy(), m.grids.copy(), m.w1.copy(), m.w2.copy(), m.w3.copy(), m.vmin, m.vmax,
+                    m.config.flat_top_p)
+
+
+def tensor_rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def forward_rel(a, b, span):
+    """|a-b| / max(|b|, 1e-3 * range) (SURVEY 7.3 normaliser)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-3 * span)))
+
+
+# ------------------------------------------------------------------ elementwise stages, bit exact
+def test_philox_uniform_bit_exact(golden):
+    g = golden("philox")
+    for key in [k for k in g if k.endswith("_key")]:
+        tag = key[:-4]
+        b = int(tag.split("_")[1][1:])
+        draws = g[tag + "_draws"]
+        k0, k1 = (int(v) for v in g[key])
+        out = L.empty((draws.size,), np.float64)
+        L.check(L.lib().apmg_philox_uniform(k0, k1, 0, draws.size, -1.0, 1.0, L.ptr(out), L.stream_handle()))
+        assert np.array_equal(L.to_host(out).reshape(draws.shape), draws)
+        # an offset start (iteration 1 of the stream) lands on the same words
+        out1 = L.empty((3 * b,), np.float64)
+        L.check(L.lib().apmg_philox_uniform(k0, k1, 3 * b, 3 * b, -1.0, 1.0, L.ptr(out1), L.stream_handle()))
+        assert np.array_equal(L.to_host(out1).reshape(b, 3), draws[1])
+
+
+def test_volume_sampling_bit_exact(golden):
+    g = golden("volume")
+    for tag in ("v1", "v2", "v3"):
+        vol = PV.Volume(dims=tuple(int(v) for v in g[tag + "_dims"]), data=g[tag + "_data"])
+        assert np.array_equal(vol.sample_many(g["pts"]), g[tag + "_samples"])
+    with pytest.raises(PV.VolumeError, match="outside"):
+        vol.sample_many(np.array([[1.2, 0.0, 0.0]]))
+
+
+def test_synth_volume_bit_exact(golden):
+    g = golden("volume")
+    blobs = [PV.BlobSpec(center=(0.2, -0.1, 0.3), sigma=(0.35, 0.3, 0.4)),
+             PV.BlobSpec(center=(-0.5, 0.4, -0.2), sigma=(0.1, 0.2, 0.15), amplitude=0.7)]
+    assert np.array_equal(PV.synth_volume((7, 6, 5), blobs, background=0.25).data, g["v1_data"])
+    assert np.array_equal(PV.synth_volume((9, 8, 10), blobs, seed=3, noise=0.05).data, g["v2_data"])
+    assert np.array_equal(PV.synth_volume((5, 1, 4), blobs).data, g["v3_data"])
+    assert np.array_equal(PV.synth_volume((64, 48, 40), blobs, background=0.1).data, g["big_data"])
+
+
+@pytest.mark.parametrize("prefix", ["a32_", "a64_", "b32_", "c32_", "d32_"])
+def test_encode_bit_exact_and_forward(golden, prefix):
+    g = golden("encode_forward")
+    m = model_from(g, prefix)
+    feats = m.encode(g[prefix + "pts"])
+    assert feats.dtype == g[prefix + "feats"].dtype
+    assert np.array_equal(feats, g[prefix + "feats"])  # to_local + interpolation reproduce numpy exactly
+    out = m.forward(g[prefix + "pts"])
+    span = m.vmax - m.vmin
+    assert forward_rel(out, g[prefix + "out"], span) <= 1e-4
+    assert forward_rel(m.decode(feats), g[prefix + "out"], span) <= 1e-4
+    # the fused forward and decode(encode) agree exactly (same per-point accumulation order)
+    assert np.array_equal(out, m.decode(feats))
+
+
+def test_forward_identities():
+    cfg = PM.ModelConfig(grids=3, channels=2, resolution=(4, 4, 4))
+    m = PM.init_model(cfg, seed=1, vmin=-4.0, vmax=9.0)
+    m.grids[:] = 0
+    pts = np.random.default_rng(1).uniform(-1, 1, (20, 3)).astype(np.float32)
+    assert np.array_equal(m.forward(pts), np.full(20, np.float32(-4.0)))
+    m.vmin = m.vmax = 2.5
+    m.grids[:] = np.random.default_rng(2).normal(size=m.grids.shape)
+    assert np.array_equal(m.forward(pts), np.full(20, np.float32(2.5)))
+    cfg2 = PM.ModelConfig(grids=2, channels=1, resolution=(2, 2, 2))
+    m2 = PM.init_model(cfg2, seed=0)
+    m2.transforms[:] = np.eye(4)
+    m2.grids[0] = 3.0
+    m2.grids[1] = -2.0
+    assert m2.encode(np.zeros((1, 3))).tolist() == [[3.0, -2.0]]
+    assert np.array_equal(PM.encode_grid(np.ones((3, 2, 2, 2)), np.array([[2.0, 0.0, 0.0]])), np.zeros((1, 3)))
+    assert PM.encode_grid(np.arange(8.0).reshape(1, 2, 2, 2), np.zeros((1, 3)))[0, 0] == pytest.approx(3.5)
+
+
+def test_encode_grid_matches_bruteforce():
+    rng = np.random.default_rng(21)
+    grid = rng.normal(size=(2, 4, 3, 5))
+    pts = rng.uniform(-1, 1, size=(1000, 3))
+    out = PM.encode_grid(grid, pts)
+    prm = O.Params(np.eye(4)[None], grid[None], np.zeros((64, 2)), np.zeros((64, 64)), np.zeros((1, 64)))
+    assert np.array_equal(out, O.encode(prm, pts))
+
+
+@pytest.mark.parametrize("prefix", ["a32_", "a64_", "b32_", "c64_"])
+def test_recon_loss_and_grads(golden, prefix):
+    g = golden("recon")
+    m = model_from(g, prefix)
+    loss, sq, grads = PO.recon_loss_and_grads(m, g[prefix + "coords"], g[prefix + "targets"])
+    assert loss == pytest.approx(float(g[prefix + "loss"]), rel=1e-5)
+    assert tensor_rel(sq, g[prefix + "sq"]) <= 1e-5
+    assert "transforms" not in grads
+    for k in ("grids", "w1", "w2", "w3"):
+        assert grads[k].shape == g[prefix + "g_" + k].shape
+        assert tensor_rel(grads[k], g[prefix + "g_" + k]) <= 1e-3, k
+    # untouched grid cells get exactly-zero gradients (Adam masking relies on it)
+    ref = g[prefix + "g_grids"]
+    assert np.array_equal(grads["grids"] == 0, ref == 0)
+
+
+def test_recon_errors_and_saddle():
+    cfg = PM.ModelConfig(grids=4, channels=1, resolution=(4, 4, 4))
+    m = PM.init_model(cfg, seed=0).astype(np.float64)
+    with pytest.raises(ValueError, match="empty"):
+        PO.recon_loss_and_grads(m, np.zeros((0, 3)), np.zeros(0))
+    m.w1[:] = 0
+    m.w2[:] = 0
+    m.w3[:] = 0
+    coords = np.random.default_rng(2).uniform(-1, 1, (32, 3))
+    loss, _, grads = PO.recon_loss_and_grads(m, coords, np.ones(32))
+    assert loss == pytest.approx(1.0)
+    for k in ("w1", "w2", "w3", "grids"):
+        assert not grads[k].any()
+
+
+@pytest.mark.parametrize("prefix", ["a32_", "a64_", "b32_", "u64_"])
+def test_density_loss_and_grads(golden, prefix):
+    g = golden("density")
+    m = model_from(g, prefix)
+    loss, dg = PO.density_loss_and_grads(m, g[prefix + "coords"], g[prefix + "errors"])
+    ref_loss = float(g[prefix + "loss"])
+    assert loss == pytest.approx(ref_loss, rel=1e-9, abs=1e-15)
+    assert tensor_rel(dg["transforms"], g[prefix + "g_transforms"]) <= 1e-6
+    assert not dg["transforms"][:, 3, :].any()
+    rho = PD.feature_density(m.transforms, g[prefix + "coords"], m.config.flat_top_p)
+    np.testing.assert_allclose(rho, g[prefix + "rho"], rtol=1e-13, atol=0)
+    rs = PD.scale_density(rho)
+    star = PD.target_density(rs, g[prefix + "errors"], float(g[prefix + "errors"].mean()))
+    np.testing.assert_allclose(star, g[prefix + "rho_star"], rtol=1e-12, atol=1e-300)
+
+
+def test_density_closed_forms():
+    eye = np.tile(np.eye(4), (1, 1, 1))
+    assert PD.feature_density(eye, np.zeros((1, 3)), 10)[0] == 1.0
+    g2 = eye.copy()
+    g2[0, :3, :3] *= 2.0
+    assert PD.feature_density(g2, np.zeros((1, 3)), 10)[0] == pytest.approx(8.0, abs=1e-9)
+    assert PD.feature_density(eye, np.array([[1.0, 1.0, 1.0]]), 10)[0] == pytest.approx(np.exp(-3.0), rel=1e-12)
+    assert PD.feature_density(eye, np.array([[5.0, 0.0, 0.0]]), 10)[0] == 0.0
+    rs = np.array([0.2, 0.3, 0.5])
+    assert np.array_equal(PD.target_density(rs, np.full(3, 0.125), 0.125), rs + PD.EPSILON)
+    assert PD.density_loss(np.array([0.5]), np.array([0.25]), epsilon=0.0) == pytest.approx(0.5 * np.log(2.0))
+    with pytest.raises(PD.DensityError, match="degenerate"):
+        PD.scale_density(np.zeros(4))
+    cfg = PM.ModelConfig(grids=1, channels=1, resolution=(4, 4, 4))
+    m = PM.init_model(cfg, seed=0).astype(np.float64)
+    with pytest.raises(ValueError, match=">= 2"):
+        PO.density_loss_and_grads(m, np.zeros((1, 3)), np.ones(1))
+
+
+@pytest.mark.parametrize("prefix", ["f32_", "f64_"])
+def test_adam_bit_exact(golden, prefix):
+    g = golden("adam")
+    params = {"w": g[prefix + "p0"].copy()}
+    st = PO.AdamState(params)
+    for step in range(len(g[prefix + "grads"])):
+        PO.adam_step(params, {"w": g[prefix + "grads"][step]}, st, float(g[prefix + "lrs"][step]))
+        assert np.array_equal(params["w"], g[prefix + "traj"][step])
+        assert np.array_equal(st.m["w"], g[prefix + "m"][step])
+        assert np.array_equal(st.v["w"], g[prefix + "v"][step])
+
+
+def test_spatial_hash_exact(golden):
+    g = golden("hash_decomp")
+    for key in [k for k in g if k.startswith("hash_") and k.endswith("_pts")]:
+        tag = key[5:-4]
+        counts = tuple(int(v) for v in tag.split("x"))
+        assert np.array_equal(P.spatial_hash(g[key], *counts), g["hash_" + tag + "_owner"])
+    assert P.spatial_hash(np.array([[1.0, 1.0, 1.0]]), 2, 2, 2)[0] == 7
+    assert P.spatial_hash(np.array([[0.0, -1.0, -1.0]]), 2, 1, 1)[0] == 1
+    with pytest.raises(P.DecompositionError, match="outside"):
+        P.spatial_hash(np.array([[1.0001, 0.0, 0.0]]), 2, 2, 2)
+
+
+def _field_from_golden(g):
+    man = json.loads(bytes(g["dec_manifest"]).decode())
+    hdr = P.VolumeHeader.from_json(man["volume_header"])
+    plan = P.plan_partition(hdr.dims, man["I"], man["J"], man["K"], man["ghost"])
+    manifest = P.DecompositionManifest(plan=plan, volume_header=hdr, bricks=man["bricks"])
+    models = [model_from(g, f"dec_m{i}_") for i in range(int(g["dec_count"]))]
+    return P.DecomposedField(manifest, models)
+
+
+def test_decomposed_forward_and_psnr(golden):
+    g = golden("hash_decomp")
+    field = _field_from_golden(g)
+    assert np.array_equal(field._scale, g["dec_scale"]) and np.array_equal(field._offset, g["dec_offset"])
+    out = field.forward(g["dec_pts"])
+    span = field.vmax - field.vmin
+    assert forward_rel(out, g["dec_out"], span) <= 1e-4
+    # every point equals its owner's model evaluated on the brick-local coordinate, bit for bit
+    owners = O.brick_of(g["dec_pts"], field.manifest.plan.counts)
+    for n in range(0, 2000, 97):
+        b = owners[n]
+        loc = (g["dec_pts"][n].astype(np.float64) * field._scale[b] + field._offset[b]).astype(np.float32)
+        assert out[n] == field.models[b].forward(loc[None, :])[0]
+    perm = np.random.default_rng(4).permutation(len(g["dec_pts"]))
+    assert np.array_equal(field.forward(g["dec_pts"])[perm], field.forward(g["dec_pts"][perm]))
+    vol = P.Volume(dims=g["dec_vol"].shape[::-1], data=g["dec_vol"])
+    assert P.psnr(field, vol) == pytest.approx(float(g["dec_psnr"]), abs=1e-5)
+
+
+def test_psnr_matches_reference(golden):
+    g = golden("psnr")
+    m = model_from(g, "m_")
+    vol = P.Volume(dims=g["vol"].shape[::-1], data=g["vol"])
+    assert P.psnr(m, vol) == pytest.approx(float(g["psnr"]), abs=1e-5)
+    vol9 = PV.synth_volume((9, 9, 9), [PV.BlobSpec(center=(0.2, -0.1, 0.3), sigma=(0.35, 0.3, 0.4))])
+    assert P.psnr(lambda p: vol9.sample_many(p), vol9) == PT.PSNR_CAP_DB
+
+
+# ------------------------------------------------------------------ training loop
+def _log_close(log, g, prefix, rtol):
+    assert log.iterations_run == int(g[prefix + "iters"])
+    np.testing.assert_allclose(log.l_rec, g[prefix + "l_rec"], rtol=rtol)
+    ref_ld = g[prefix + "l_density"]
+    got_ld = np.array([np.nan if v is None else v for v in log.l_density])
+    assert np.array_equal(np.isnan(got_ld), np.isnan(ref_ld))
+    np.testing.assert_allclose(got_ld[~np.isnan(ref_ld)], ref_ld[~np.isnan(ref_ld)], rtol=rtol)
+    np.testing.assert_array_equal(log.lr, g[prefix + "lr"])
+
+
+def test_train_single_small_trajectory(golden):
+    g = golden("train_small")
+    m = model_from(g, "init_")
+    vol = P.Volume(dims=(16, 16, 16), data=g["blob_data"])
+    cfg = P.TrainConfig(iterations=40, batch_size=64, delay_start=5, seed=9, plateau_enabled=False)
+    m, log = P.train_single(m, vol, cfg)
+    _log_close(log, g, "log_", rtol=1e-3)
+    fin = model_from(g, "final_")
+    for k in ("transforms", "w1", "w2", "w3", "grids"):
+        assert tensor_rel(getattr(m, k), getattr(fin, k)) <= 1e-3, k
+    assert P.psnr(m, vol) == pytest.approx(float(g["psnr"]), abs=0.1)
+
+
+def test_train_hard_stop_frozen_transforms(golden):
+    g = golden("train_small")
+    m = model_from(g, "init_")
+    vol = P.Volume(dims=(16, 16, 16), data=g["blob_data"])
+    snaps = {}
+    cfg = P.TrainConfig(iterations=100, batch_size=32, delay_start=10, transform_hard_stop_fraction=0.5,
+                        plateau_enabled=False, seed=3)
+    _, log = P.train_single(m, vol, cfg, on_iteration=lambda it, mm: snaps.update({it: mm.transforms.tobytes()}))
+    assert log.transform_stop_iteration == 50 == int(g["hslog_stop"])
+    assert snaps[9] == snaps[0] and snaps[10] != snaps[9] and snaps[49] != snaps[10]
+    for it in range(50, 100):
+        assert snaps[it] == snaps[50]
+    _log_close(log, g, "hslog_", rtol=1e-3)
+
+
+def test_train_constant_volume_plateau(golden):
+    g = golden("train_small")
+    const = P.Volume(dims=(8, 8, 8), data=np.full((8, 8, 8), 3.25, dtype=np.float32))
+    cfg_m = PM.ModelConfig(grids=4, channels=1, resolution=(4, 4, 4), seed=9)
+    m = PM.init_model(cfg_m, seed=0, vmin=const.vmin, vmax=const.vmax)
+    m, log = P.train_single(m, const, P.TrainConfig(iterations=4000, batch_size=64, seed=1))
+    assert all(v == 0.0 for v in log.l_rec)
+    assert log.plateau_trigger_iterations == list(g["const_triggers"])
+    assert log.iterations_run == int(g["const_iters"])
+    np.testing.assert_array_equal(log.lr, g["const_lr"])
+    pts = np.random.default_rng(0).uniform(-1, 1, (50, 3)).astype(np.float32)
+    assert np.array_equal(m.forward(pts), np.full(50, np.float32(3.25)))
+
+
+def test_train_c1_psnr_parity(golden):
+    """C1-shaped run (64 grids 32^3 x2, 128^3 blob field, 200 its x 2^14, delay 50):
+    final PSNR within 0.1 dB of the reference CPU run (tests/golden/train_c1.npz)."""
+    g = golden("train_c1")
+    iters, batch, delay = (int(v) for v in g["config"])
+    blobs = [PV.BlobSpec(center=(0.45, -0.3, 0.2), sigma=(0.035, 0.035, 0.035)),
+             PV.BlobSpec(center=(-0.2, 0.2, -0.1), sigma=(0.6, 0.5, 0.7), amplitude=0.35),
+             PV.BlobSpec(center=(0.3, 0.4, 0.5), sigma=(0.45, 0.55, 0.4), amplitude=0.25),
+             PV.BlobSpec(center=(-0.5, -0.5, 0.4), sigma=(0.5, 0.4, 0.5), amplitude=0.3)]
+    vol = PV.synth_volume((128, 128, 128), blobs)
+    m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                      vmax=vol.vmax)
+    cfg = P.TrainConfig(iterations=iters, batch_size=batch, delay_start=delay, seed=0, plateau_enabled=False)
+    m, log = P.train_single(m, vol, cfg)
+    p = P.psnr(m, vol)
+    assert abs(p - float(g["psnr"])) <= 0.1, (p, float(g["psnr"]))
+    np.testing.assert_allclose(log.l_rec[:20], g["log_l_rec"][:20], rtol=2e-3)
+    assert log.transform_stop_iteration == int(g["log_stop"])
+
+
+def test_fd_gradient_suite_f64():
+    """Acceptance criterion 1 on the GPU kernels: f64 analytic grads vs central FD <= 1e-3."""
+    rng = np.random.default_rng(1)
+    worst_rec = worst_den = 0.0
+    for seed in (0, 1):
+        cfg = PM.ModelConfig(grids=4, channels=1, resolution=(4, 4, 4))
+        m = PM.init_model(cfg, seed=seed, vmin=-0.5, vmax=1.5).astype(np.float64)
+        r2 = np.random.default_rng(seed + 900)
+        m.grids[:] = r2.normal(scale=0.5, size=m.grids.shape)
+        m.w1[:] = r2.normal(scale=0.25, size=m.w1.shape)
+        m.w2[:] = r2.normal(scale=0.25, size=m.w2.shape)
+        m.w3[:] = r2.normal(scale=0.25, size=m.w3.shape)
+        coords = rng.uniform(-1, 1, (64, 3))
+        targets = rng.normal(size=64)
+        errors = rng.uniform(0.01, 1.0, 64)
+
+        def rec_fn(params, m=m, coords=coords, targets=targets):
+            trial = m.copy()
+            for key in params:
+                getattr(trial, key)[:] = params[key]
+            loss, _, grads = PO.recon_loss_and_grads(trial, coords, targets)
+            return loss, grads
+
+        worst_rec = max(worst_rec, PO.finite_diff_check(
+            rec_fn, {"grids": m.grids, "w1": m.w1, "w2": m.w2, "w3": m.w3}, step=1e-5, samples_per_tensor=20,
+            rng=np.random.default_rng(seed)))
+        p = m.config.flat_top_p
+        star = PD.target_density(PD.scale_density(PD.feature_density(m.transforms, coords, p)), errors,
+                                 float(errors.mean()))
+
+        def den_fn(params, m=m, coords=coords, errors=errors, star=star, p=p):
+            trial = m.copy()
+            trial.transforms[:] = params["transforms"]
+            loss = PD.density_loss(PD.scale_density(PD.feature_density(trial.transforms, coords, p)), star)
+            _, grads = PO.density_loss_and_grads(trial, coords, errors)
+            return loss, grads
+
+        worst_den = max(worst_den, PO.finite_diff_check(
+            den_fn, {"transforms": m.transforms}, step=1e-5, samples_per_tensor=24,
+            rng=np.random.default_rng(seed + 50)))
+    assert worst_rec <= 1e-3 and worst_den <= 1e-3, (worst_rec, worst_den)
+
+
+# ------------------------------------------------------------------ full-size properties
+def test_full_size_forward_and_recon_vs_oracle():
+    """BASELINE config shape (64 grids 32^3 x2) on 2^20 points: forward on a seeded
+    subset vs the oracle; the recon loss over the full batch equals the mean of the
+    returned squared errors and decreases the loss after one Adam step."""
+    cfg = PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32))
+    m = PM.init_model(cfg, seed=0, vmin=0.0, vmax=1.0)
+    r = np.random.default_rng(5)
+    m.grids[:] = r.normal(scale=0.3, size=m.grids.shape).astype(np.float32)
+    pts = r.uniform(-1, 1, (1 << 20, 3)).astype(np.float32)
+    out = m.forward(pts)
+    ref = O.forward(oracle_from(m), pts[:4096])
+    assert forward_rel(out[:4096], ref, 1.0) <= 1e-4
+    tgt = r.uniform(0, 1, 1 << 20).astype(np.float32)
+    loss, sq, grads = PO.recon_loss_and_grads(m, pts, tgt)
+    assert loss == pytest.approx(float(np.mean(sq, dtype=np.float64)), rel=1e-9)
+    assert forward_rel(np.sqrt(sq), np.abs(out - tgt), 1.0) <= 1e-4

@@ -1,0 +1,199 @@
+"""CPU-only tests: the C-ABI library loads and exports every declared symbol,
+the scheduler rules compiled into it match the oracle, host-side planning
+(partition, manifest, model I/O) matches the reference fixtures, and the
+multi-rank brick sharding works over gloo with world_size 2."""
+import json
+import os
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import apmg_oracle as O
+from paper_2308_02494_b200 import _lib as L
+from paper_2308_02494_b200 import decomposition as D
+from paper_2308_02494_b200 import model as PM
+from paper_2308_02494_b200 import trainer as T
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "apmg_cuda.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(apmg_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = L.lib()
+    syms = header_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in L.SIGNATURES, f"{s} missing from the ctypes binding"
+    assert lib.apmg_version().startswith(b"apmg-b200")
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(L.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_pairwise_sum_matches_numpy():
+    import ctypes as C
+    rng = np.random.default_rng(0)
+    for n in (1, 7, 8, 9, 127, 128, 129, 500, 1000, 2000, 4097):
+        x = rng.normal(size=n) * 10 ** rng.uniform(-3, 3, size=n)
+        got = L.lib().apmg_host_pairwise_sum(x.ctypes.data_as(C.POINTER(C.c_double)), n)
+        assert got == x.sum()
+
+
+def test_plateau_rule_matches_oracle():
+    rng = np.random.default_rng(1)
+    for trial in range(20):
+        window = int(rng.integers(2, 12))
+        a = T.PlateauState(lr=0.01, window=window, threshold=1e-4, factor=10.0, max_triggers=3)
+        b = O.Plateau(window, 1e-4, 10.0, 3, lr=0.01)
+        v = 1.0
+        for _ in range(120):
+            v *= float(rng.choice([1.0, 0.99999, 0.9, 1.01]))
+            ra, rb = T.plateau_step(a, v), O.plateau_advance(b, v)
+            assert ra == rb
+            assert a.triggers == b.triggers and a.history == b.history
+            if ra == "stop":
+                break
+
+
+def test_plateau_reference_cases():
+    st = T.PlateauState(lr=0.01, window=5, threshold=1e-4, factor=10, max_triggers=3)
+    actions = [T.plateau_step(st, 1.0) for _ in range(18)]
+    assert actions[5] == "reduce_lr" and actions.count("reduce_lr") == 2 and actions[17] == "stop"
+    assert st.lr == pytest.approx(0.01 / 1000)
+
+
+def test_transform_stop_rule_matches_oracle():
+    cfg = T.TrainConfig(iterations=10_000)
+    ocfg = O.LoopConfig(iterations=10_000)
+    assert T.transform_stop_check([1.0] * 2000, cfg, 600)
+    assert not T.transform_stop_check([1.0] * 1999, cfg, 600)
+    hist = [0.99 ** (i / 1000) for i in range(2000)]
+    assert not T.transform_stop_check(hist, cfg, 600)
+    improving = [1.0 / (i + 1) for i in range(3000)]
+    assert not T.transform_stop_check(improving, cfg, 7999) and T.transform_stop_check(improving, cfg, 8000)
+    rng = np.random.default_rng(2)
+    for _ in range(30):
+        n = int(rng.integers(1900, 2600))
+        h = list(np.cumprod(1 + rng.normal(scale=1e-4, size=n) - 2e-8))
+        it = int(rng.integers(500, 9000))
+        assert T.transform_stop_check(h, cfg, it) == O.transform_should_stop(h, ocfg, it)
+
+
+def test_train_config_validation():
+    with pytest.raises(ValueError, match="delay_start"):
+        T.TrainConfig(iterations=100, delay_start=100)
+    assert T.TrainConfig(iterations=0).iterations == 0
+    assert T.TrainConfig(iterations=100, delay_start=10,
+                         transform_hard_stop_fraction=0.5).hard_stop_iteration == 50
+
+
+def test_partition_matches_reference_fixture(golden):
+    g = golden("hash_decomp")
+    man = json.loads(bytes(g["dec_manifest"]).decode())
+    plan = D.plan_partition(tuple(man["volume_header"]["dims"]), man["I"], man["J"], man["K"], man["ghost"])
+    for brick, entry in zip(plan.bricks, man["bricks"]):
+        assert list(brick.core.lo) == entry["core_lo"] and list(brick.core.hi) == entry["core_hi"]
+        assert list(brick.ghost.lo) == entry["ghost_lo"] and list(brick.ghost.hi) == entry["ghost_hi"]
+    assert [D._brick_seed(7, b) for b in range(plan.brick_count)] == [e["seed"] for e in man["bricks"]]
+    plan = D.plan_partition((10, 3, 3), 4, 1, 1, ghost=0)
+    assert [plan.bricks[i].core.shape()[0] for i in range(4)] == [3, 3, 2, 2]
+    with pytest.raises(D.DecompositionError, match="exceed"):
+        D.plan_partition((4, 4, 4), 5, 1, 1)
+
+
+def test_core_tiling_covers_every_voxel_once():
+    dims = (7, 5, 6)
+    plan = D.plan_partition(dims, 3, 2, 2, ghost=2)
+    counts = np.zeros(dims[::-1], dtype=int)
+    for brick in plan.bricks:
+        (x0, y0, z0), (x1, y1, z1) = brick.core.lo, brick.core.hi
+        counts[z0:z1 + 1, y0:y1 + 1, x0:x1 + 1] += 1
+    assert np.array_equal(counts, np.ones_like(counts))
+
+
+def test_model_io_bit_compatible(tmp_path, golden):
+    g = golden("encode_forward")
+    meta = g["a32_meta"]
+    cfg = PM.ModelConfig(grids=int(meta[0]), channels=int(meta[1]), resolution=tuple(int(v) for v in meta[2:5]))
+    m = PM.ApmgModel(cfg, g["a32_transforms"], g["a32_grids"], g["a32_w1"], g["a32_w2"], g["a32_w3"], -0.25, 1.75)
+    PM.save_model(m, tmp_path / "m.apmg")
+    back = PM.load_model(tmp_path / "m.apmg")
+    for k in ("transforms", "grids", "w1", "w2", "w3"):
+        assert getattr(back, k).tobytes() == getattr(m, k).tobytes()
+    raw = bytearray((tmp_path / "m.apmg").read_bytes())
+    raw[:4] = b"NOPE"
+    (tmp_path / "bad.apmg").write_bytes(bytes(raw))
+    with pytest.raises(PM.ModelError, match="magic"):
+        PM.load_model(tmp_path / "bad.apmg")
+    (tmp_path / "t.apmg").write_bytes(bytes(raw[:len(raw) // 2]).replace(b"NOPE", b"APMG"))
+    with pytest.raises(PM.ModelError, match="truncated"):
+        PM.load_model(tmp_path / "t.apmg")
+
+
+def test_init_model_matches_reference(golden):
+    g = golden("train_small")
+    cfg = PM.ModelConfig(grids=4, channels=1, resolution=(4, 4, 4), seed=9)
+    m = PM.init_model(cfg, seed=9, vmin=float(g["init_range"][0]), vmax=float(g["init_range"][1]))
+    for k in ("transforms", "grids", "w1", "w2", "w3"):
+        assert np.array_equal(getattr(m, k), g["init_" + k])
+
+
+def test_brick_rank_assignment():
+    assert D.brick_ranks(8, 1) == [list(range(8))]
+    assert D.brick_ranks(8, 2) == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    assert D.brick_ranks(64, 8)[3] == [3, 11, 19, 27, 35, 43, 51, 59]
+
+
+def _gloo_worker(rank, world, port, out_dir, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hdr = D.VolumeHeader(dims=(16, 16, 16))
+        plan = D.plan_partition(hdr.dims, 2, 2, 2, ghost=1)
+        ran = []
+
+        def fake_trainer(job):  # host-only stand-in for the per-brick GPU job
+            ran.append(job["flat_index"])
+            return job["flat_index"], {"model_path": Path(job["model_path"]).name, "seed": job["seed"],
+                                       "rank": rank, "psnr": 40.0 + job["flat_index"]}
+
+        man = D.train_decomposed("unused.raw", hdr, plan, D.ModelConfig(2, 1, (4, 4, 4)),
+                                 T.TrainConfig(iterations=10, batch_size=8, delay_start=1, seed=7), out_dir,
+                                 brick_trainer=fake_trainer)
+        q.put((rank, ran, [b["rank"] for b in man.bricks], [b["seed"] for b in man.bricks]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_decomposed_sharding_gloo_world2(tmp_path):
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, str(tmp_path), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == [0, 2, 4, 6] and res[1][1] == [1, 3, 5, 7]
+    assert res[0][2] == [0, 1] * 4 == res[1][2]
+    assert res[0][3] == [(7 ^ b) & 0x7FFFFFFF for b in range(8)]
+    man = json.loads((tmp_path / "manifest.json").read_text())
+    assert [b["psnr"] for b in man["bricks"]] == [40.0 + b for b in range(8)]
