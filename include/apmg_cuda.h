@@ -191,6 +191,10 @@ int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_density, double
                    int64_t* triggers, int64_t* n_triggers, void* stream);
 int apmg_train_destroy(apmg_train_state* s);
 
+/* ---- tcgen05 self-test (one CTA, one GEMM; see csrc/umma_debug.cu) ---------- */
+int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
+                         float* D, void* stream);
+
 /* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
 /* plateau_step (trainer.py:118-138) on the same code the device controller runs.
  * history: HOST ring of capacity window+1 (in/out), count in/out; returns 0 none,

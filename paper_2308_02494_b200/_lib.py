@@ -88,6 +88,7 @@ SIGNATURES = {
     "apmg_host_plateau_step": (C.c_int, [C.POINTER(_D), C.POINTER(_I64), C.POINTER(_I64), _I64, _D, _I64, _D]),
     "apmg_host_transform_stop": (C.c_int, [C.POINTER(_D), _I64, _I64, _D, _I64, _I64]),
     "apmg_host_pairwise_sum": (_D, [C.POINTER(_D), _I64]),
+    "apmg_debug_umma_gemm": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -37,6 +37,10 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
 template <typename T>
 size_t recon_ws_bytes(int F, int64_t n);
 
+bool recon_tc_eligible(const ModelDev<float>& md);
+int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
+                    float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
+
 template <typename T, typename TE>
 int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, double* loss, T* dtf, double* rho_total,
                    T* adam_m, T* adam_v, void* ws, size_t wsb, const TrainCtl* ctl, cudaStream_t st);

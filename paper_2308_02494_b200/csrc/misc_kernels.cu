@@ -107,6 +107,88 @@ template __global__ void k_train_batch<float>(uint64_t, uint64_t, int64_t, const
 template __global__ void k_train_batch<double>(uint64_t, uint64_t, int64_t, const float*, int, int, int, double*,
                                                double*, const TrainCtl*);
 
+// ---- spatial bucketing of the batch (order-free: the losses and gradients are sums over
+// points, so a permutation changes nothing but the summation order).  Points are binned
+// into the Morton-ordered cells of a 32^3 lattice over [-1,1]^3 so that a 64-point tile of
+// the recon kernel covers a compact region: its corner gathers hit L1 and its grid
+// scatters land on a handful of cells.
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+  v &= 0x3ff;
+  v = (v | (v << 16)) & 0x030000FF;
+  v = (v | (v << 8)) & 0x0300F00F;
+  v = (v | (v << 4)) & 0x030C30C3;
+  v = (v | (v << 2)) & 0x09249249;
+  return v;
+}
+
+__device__ __forceinline__ uint32_t bucket_of(float x, float y, float z) {
+  const int bx = min(31, max(0, int((x + 1.0f) * 16.0f)));
+  const int by = min(31, max(0, int((y + 1.0f) * 16.0f)));
+  const int bz = min(31, max(0, int((z + 1.0f) * 16.0f)));
+  return spread3(bx) | (spread3(by) << 1) | (spread3(bz) << 2);
+}
+
+template <typename T>
+__global__ void k_bucket_count(const T* __restrict__ coords, int64_t n, uint32_t* __restrict__ key,
+                               int32_t* __restrict__ counts, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t k = bucket_of(float(coords[3 * i]), float(coords[3 * i + 1]), float(coords[3 * i + 2]));
+    key[i] = k;
+    atomicAdd(&counts[k], 1);
+  }
+}
+
+// in-place exclusive scan of kBuckets counts (one block of 1024 threads)
+constexpr int kBuckets = 32768;
+__global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  __shared__ int32_t part[1024];
+  const int t = threadIdx.x, per = kBuckets / 1024;
+  int32_t local[kBuckets / 1024];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    local[i] = counts[t * per + i];
+    s += local[i];
+  }
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int32_t v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int32_t run = part[t] - s;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    counts[t * per + i] = run;
+    run += local[i];
+  }
+}
+
+template <typename T>
+__global__ void k_bucket_scatter(const T* __restrict__ coords, const T* __restrict__ targets,
+                                 const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cursor,
+                                 T* __restrict__ coords_out, T* __restrict__ targets_out, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pos = atomicAdd(&cursor[key[i]], 1);
+    coords_out[3 * pos] = coords[3 * i];
+    coords_out[3 * pos + 1] = coords[3 * i + 1];
+    coords_out[3 * pos + 2] = coords[3 * i + 2];
+    targets_out[pos] = targets[i];
+  }
+}
+
+template __global__ void k_bucket_count<float>(const float*, int64_t, uint32_t*, int32_t*, const TrainCtl*);
+template __global__ void k_bucket_count<double>(const double*, int64_t, uint32_t*, int32_t*, const TrainCtl*);
+template __global__ void k_bucket_scatter<float>(const float*, const float*, const uint32_t*, int64_t, int32_t*, float*,
+                                                 float*, const TrainCtl*);
+template __global__ void k_bucket_scatter<double>(const double*, const double*, const uint32_t*, int64_t, int32_t*,
+                                                  double*, double*, const TrainCtl*);
+
 // ---- synth_volume (volume.py:283-296)
 __global__ void k_synth(int w, int h, int d, int nb, const double* __restrict__ ex, const double* __restrict__ ey,
                         const double* __restrict__ ez, const double* __restrict__ amp, double bg, uint64_t k0,

@@ -467,11 +467,22 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
     set_error("recon workspace too small: need %zu, have %zu", c.used, wsb);
     return APMG_E_WORKSPACE;
   }
-  ReconArgs<T> a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl};
-  if (dws)
-    APMG_LAUNCH("recon_fwd_bwd", (k_recon<T, true>), grid, kTileThreads, smem, st, a);
-  else
-    APMG_LAUNCH("recon_fwd_bwd", (k_recon<T, false>), grid, kTileThreads, smem, st, a);
+  bool done = false;
+  if constexpr (sizeof(T) == 4) {
+    if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
+      grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms())));
+      rc = launch_recon_tc(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
+      if (rc) return rc;
+      done = true;
+    }
+  }
+  if (!done) {
+    ReconArgs<T> a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl};
+    if (dws)
+      APMG_LAUNCH("recon_fwd_bwd", (k_recon<T, true>), grid, kTileThreads, smem, st, a);
+    else
+      APMG_LAUNCH("recon_fwd_bwd", (k_recon<T, false>), grid, kTileThreads, smem, st, a);
+  }
   const int fin_grid = int(ceil_div(int64_t(DW), 256));
   APMG_LAUNCH("recon_finalize", k_recon_finalize<T>, fin_grid, 256, 0, st, grid, md.F, part_dw, part_loss, n, dw1,
               dw2, dw3, loss, const_cast<TrainCtl*>(ctl), l_rec_log);

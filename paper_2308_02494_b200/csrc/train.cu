@@ -13,6 +13,7 @@
 //   density x6  rho, stats, target, stats, grad, finalize+Adam  (optim.py:158-200)
 //   ctl_end     log, density history, plateau rule              (trainer.py:207-220)
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -28,6 +29,20 @@ template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
                              const TrainCtl* ctl);
 int elementwise_grid(int64_t n, int per_sm);
+constexpr int kBuckets = 32768;
+template <typename T>
+__global__ void k_bucket_count(const T* __restrict__ coords, int64_t n, uint32_t* __restrict__ key,
+                               int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl);
+template <typename T>
+__global__ void k_bucket_scatter(const T* __restrict__ coords, const T* __restrict__ targets,
+                                 const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cursor,
+                                 T* __restrict__ coords_out, T* __restrict__ targets_out, const TrainCtl* ctl);
+
+static bool sort_enabled() {
+  const char* e = getenv("APMG_SORT");
+  return !(e && e[0] == '0');
+}
 
 struct CtlParams {
   int64_t iterations, delay_start, ma_window, hard_stop, plateau_window, plateau_max;
@@ -107,7 +122,10 @@ struct apmg_train_state {
   TrainCtl* ctl;
   double *l_rec, *l_dens, *lr, *dens_hist, *plat_ring, *bias;
   int64_t* trig;
-  void *grad, *am, *av, *tm, *tv, *coords, *targets, *sq;
+  void *grad, *am, *av, *tm, *tv, *coords, *targets, *sq, *coords_raw, *targets_raw;
+  uint32_t* key;
+  int32_t* counts;
+  bool sort;
   void* recon_ws;
   size_t recon_wsb;
   void* dens_ws;
@@ -151,6 +169,10 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   char* coords = cv.take<char>(es * 3 * B);
   char* targets = cv.take<char>(es * B);
   char* sq = cv.take<char>(es * B);
+  char* coords_raw = cv.take<char>(es * 3 * B);
+  char* targets_raw = cv.take<char>(es * B);
+  uint32_t* key = cv.take<uint32_t>(B);
+  int32_t* counts = cv.take<int32_t>(kBuckets);
   const size_t rws = m->dtype == APMG_F32 ? recon_ws_bytes<float>(F, B) : recon_ws_bytes<double>(F, B);
   char* recon_ws = cv.take<char>(rws);
   const size_t dws = density_ws_bytes(m->grids, B);
@@ -172,6 +194,10 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
     s->coords = coords;
     s->targets = targets;
     s->sq = sq;
+    s->coords_raw = coords_raw;
+    s->targets_raw = targets_raw;
+    s->key = key;
+    s->counts = counts;
     s->recon_ws = recon_ws;
     s->recon_wsb = rws;
     s->dens_ws = dens_ws;
@@ -204,6 +230,7 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   s->w = w;
   s->h = h;
   s->d = d;
+  s->sort = sort_enabled();
   const size_t need = carve_train(s, shape, cfg, workspace, workspace_bytes);
   if (need > workspace_bytes) {
     delete s;
@@ -256,8 +283,21 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   live.transforms = s->transforms;
   const ModelDev<T> md = make_model_dev<T>(live);
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
-  APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume, s->w,
-              s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+  if (s->sort) {
+    // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
+    APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
+                s->w, s->h, s->d, static_cast<T*>(s->coords_raw), static_cast<T*>(s->targets_raw), s->ctl);
+    APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
+    APMG_LAUNCH("bucket_count", k_bucket_count<T>, elementwise_grid(B, 8), 256, 0, st,
+                static_cast<const T*>(s->coords_raw), B, s->key, s->counts, s->ctl);
+    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
+    APMG_LAUNCH("bucket_scatter", k_bucket_scatter<T>, elementwise_grid(B, 8), 256, 0, st,
+                static_cast<const T*>(s->coords_raw), static_cast<const T*>(s->targets_raw), s->key, B, s->counts,
+                static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+  } else {
+    APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
+                s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+  }
   int rc = launch_recon<T>(md, B, static_cast<const T*>(s->coords), static_cast<const T*>(s->targets),
                            static_cast<T*>(s->sq), nullptr, grad + s->off[0], grad + s->off[1], grad + s->off[2],
                            grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);

@@ -1,0 +1,151 @@
+// tcgen05 (5th-gen tensor core) building blocks for sm_100a, written against the
+// PTX ISA directly: shared-memory matrix descriptors, instruction descriptors,
+// kind::tf32 MMA issue, commit-to-mbarrier, TMEM allocation and loads.
+//
+// Operand layout ("CM layout"): a row-major matrix X[R][C] of 32-bit values is
+// stored as 8x16-byte core matrices,
+//     offset(r, c) = (c/4)*SC + (r/8)*128 + (r%8)*16 + (c%4)*4,   SC = R*16,
+// which is simultaneously
+//   * the canonical K-major SWIZZLE_NONE layout with rows = M/N and cols = K
+//     (SBO = 128 B between 8-row groups, LBO = SC between the two 16-B K chunks
+//     of one K=8 tf32 MMA), and
+//   * the canonical MN-major SWIZZLE_NONE layout with cols = M/N and rows = K
+//     (SBO = SC between 4-element MN chunks, LBO = 128 B between 8-row K groups).
+// So one buffer feeds both X and X^T products without a transpose, and a
+// thread owning a row writes whole 16-byte chunks (conflict-free).
+#pragma once
+
+#include <stdint.h>
+
+namespace apmg {
+namespace umma {
+
+__host__ __device__ constexpr uint32_t cm_offset(int r, int c, int R) {
+  return uint32_t((c >> 2) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (c & 3) * 4);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// SWIZZLE_NONE shared-memory descriptor (Blackwell version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version = 1 (sm_100)
+  // base_offset = 0, lbo_mode = 0, layout_type (bits 61-63) = 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// Descriptor of a CM-layout buffer used K-major (rows = M or N) at K-step kk (K=8 each).
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int R, int kk) {
+  return smem_desc(base + uint32_t(kk) * 2u * uint32_t(R * 16), uint32_t(R * 16), 128u);
+}
+// Descriptor of a CM-layout buffer used MN-major (cols = M or N, rows = K) at K-step kk.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int R, int kk) {
+  return smem_desc(base + uint32_t(kk) * 128u, 128u, uint32_t(R * 16));
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                      // c_format = F32
+         | (2u << 7)                    // a_format = TF32
+         | (2u << 10)                   // b_format = TF32
+         | (uint32_t(a_mn) << 15)       // a_major (0 = K, 1 = MN)
+         | (uint32_t(b_mn) << 16)       // b_major
+         | (uint32_t(N >> 3) << 17)     // n_dim
+         | (uint32_t(M >> 4) << 24);    // m_dim
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// same, with the explicit (all-enabled) disable-output-lane mask operand
+__device__ __forceinline__ void mma_tf32_mask(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  const uint32_t a = smem_u32(mbar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// whole warp: allocate `cols` TMEM columns, address written to *dst (smem)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread (thread t <-> lane base + t)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// round-to-nearest TF32 (the value the tensor core multiplies exactly) and the exact residual
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = tf32_rn(x);
+  lo = x - hi;
+}
+
+// TMEM address of (lane, column) relative to the allocation base
+__device__ __forceinline__ uint32_t taddr(uint32_t base, uint32_t lane, uint32_t col) {
+  return base + (lane << 16) + col;
+}
+
+}  // namespace umma
+}  // namespace apmg

@@ -115,7 +115,8 @@ def density_loss_and_grads(model: ApmgModel, coords, errors):
     total = L.empty((1,), np.float64)
     dtf = L.zeros((model.config.grids, 4, 4), model.dtype)
     ws = L.workspace(L.lib().apmg_density_workspace_bytes(model.config.grids, n))
-    L.check(L.lib().apmg_density_loss_grads(C.byref(dm.desc), L.ptr(coords_m), L.ptr(L.to_device(errors)), n,
+    errors_d = L.to_device(errors)
+    L.check(L.lib().apmg_density_loss_grads(C.byref(dm.desc), L.ptr(coords_m), L.ptr(errors_d), n,
                                             L.ptr(loss), L.ptr(dtf), L.ptr(total), L.ptr(ws), ws.numel(),
                                             L.stream_handle()), "density_loss_and_grads")
     if not float(total.item()) > 0.0:

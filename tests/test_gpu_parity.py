@@ -398,3 +398,31 @@ def test_full_size_forward_and_recon_vs_oracle():
     loss, sq, grads = PO.recon_loss_and_grads(m, pts, tgt)
     assert loss == pytest.approx(float(np.mean(sq, dtype=np.float64)), rel=1e-9)
     assert forward_rel(np.sqrt(sq), np.abs(out - tgt), 1.0) <= 1e-4
+
+
+@pytest.mark.parametrize("res", [(8, 8, 8), (32, 32, 32)])
+def test_recon_tensor_core_path_vs_oracle(res, monkeypatch):
+    """The flagship shape (64 grids x 2 channels -> 128 features) runs the tcgen05/mma
+    tensor-core recon kernel; check it against the oracle and against the SIMT kernel."""
+    cfg = PM.ModelConfig(grids=64, channels=2, resolution=res)
+    m = PM.init_model(cfg, seed=3, vmin=-0.5, vmax=1.5)
+    r = np.random.default_rng(4)
+    m.grids[:] = r.normal(scale=0.5, size=m.grids.shape).astype(np.float32)
+    m.w1[:] = r.normal(scale=0.15, size=m.w1.shape).astype(np.float32)
+    m.w2[:] = r.normal(scale=0.2, size=m.w2.shape).astype(np.float32)
+    m.w3[:] = r.normal(scale=0.3, size=m.w3.shape).astype(np.float32)
+    m.transforms[:, :3, :3] += r.normal(scale=0.1, size=(64, 3, 3)).astype(np.float32)
+    n = 3000  # not a multiple of the 64-point tile
+    pts = r.uniform(-1, 1, (n, 3)).astype(np.float32)
+    tgt = r.normal(size=n).astype(np.float32)
+    loss, sq, grads = PO.recon_loss_and_grads(m, pts, tgt)
+    rl, rsq, rg = O.recon_loss_and_grads(oracle_from(m), pts, tgt)
+    assert loss == pytest.approx(rl, rel=1e-5)
+    assert tensor_rel(sq, rsq) <= 1e-5
+    for k in ("grids", "w1", "w2", "w3"):
+        assert tensor_rel(grads[k], rg[k]) <= 1e-3, (k, tensor_rel(grads[k], rg[k]))
+    monkeypatch.setenv("APMG_MLP", "simt")
+    loss_s, sq_s, grads_s = PO.recon_loss_and_grads(m, pts, tgt)
+    assert loss_s == pytest.approx(loss, rel=1e-5)
+    for k in ("grids", "w1", "w2", "w3"):
+        assert tensor_rel(grads[k], grads_s[k]) <= 1e-3, k

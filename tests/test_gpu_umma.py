@@ -1,0 +1,44 @@
+"""tcgen05 bring-up: the CM-layout operand staging, smem/instruction descriptors,
+kind::tf32 MMA and TMEM readback used by the fused MLP, one GEMM per config,
+against float64 numpy (3xTF32 split and single TF32)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2308_02494_b200 import _lib as L  # noqa: E402
+
+
+def run(cfg, K, N, split3, seed=0):
+    rng = np.random.default_rng(seed + 17 * cfg + K + N)
+    M = 128 if cfg >= 2 else 64
+    if cfg == 0 or cfg == 3:
+        A = rng.normal(size=(M, K)).astype(np.float32)
+        B = rng.normal(size=(N, K)).astype(np.float32)
+        ref = A.astype(np.float64) @ B.astype(np.float64).T
+    elif cfg == 1:
+        A = rng.normal(size=(M, K)).astype(np.float32)
+        B = rng.normal(size=(K, N)).astype(np.float32)
+        ref = A.astype(np.float64) @ B.astype(np.float64)
+    else:
+        A = rng.normal(size=(K, 128)).astype(np.float32)
+        B = rng.normal(size=(K, N)).astype(np.float32)
+        ref = A.astype(np.float64).T @ B.astype(np.float64)
+    d = L.zeros((M, N), np.float32)
+    a_d, b_d = L.to_device(A), L.to_device(B)  # both alive at launch (no allocator reuse)
+    L.check(L.lib().apmg_debug_umma_gemm(cfg, K, N, split3, L.ptr(a_d), L.ptr(b_d), L.ptr(d),
+                                         L.stream_handle()), "umma")
+    got = L.to_host(d).astype(np.float64)
+    return float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("cfg,K,N", [(0, 128, 64), (0, 64, 64), (1, 64, 64), (1, 64, 128), (2, 64, 64),
+                                     (2, 64, 80), (3, 64, 64), (0, 8, 16)])
+def test_umma_gemm_configs(cfg, K, N):
+    e3 = run(cfg, K, N, 1)
+    e1 = run(cfg, K, N, 0)
+    assert e3 < 2e-6, (cfg, K, N, e3, e1)
+    assert e1 < 3e-3, (cfg, K, N, e3, e1)
