@@ -63,16 +63,22 @@ struct Cell {
   bool inside;
 };
 
-template <typename T>
-__device__ __forceinline__ void axis_term(T l, int n, int& i0, double& f) {
-  const T u = mul_rn(mul_rn(add_rn(l, T(1)), T(0.5)), T(n - 1));
-  const double fl = floor(static_cast<double>(u));
-  // numpy casts floor(u) to intp and clips to [0, n-2]; out-of-range values only
-  // occur for points outside the grid, whose features are zeroed.
-  int i = (fl >= 0.0 && fl <= static_cast<double>(n - 2)) ? static_cast<int>(fl) : (fl > 0.0 ? n - 2 : 0);
+// numpy: i0 = clip(floor(u), 0, n-2), frac = clip(f64(u) - i0, 0, 1).  For points inside
+// the grid u lies in [0, n-1], so both clips are no-ops except i0 at the top vertex, and
+// u - i0 is exact in the model dtype (Sterbenz), hence computed there.  Outside points
+// only need an in-range index (their features are zeroed / their scatter is skipped).
+__device__ __forceinline__ void axis_term(float l, int n, int& i0, double& f) {
+  const float u = mul_rn(mul_rn(add_rn(l, 1.0f), 0.5f), float(n - 1));
+  const int i = min(max(int(floorf(u)), 0), n - 2);
   i0 = i;
-  double fr = static_cast<double>(u) - static_cast<double>(i);
-  f = fmin(fmax(fr, 0.0), 1.0);
+  f = static_cast<double>(__fsub_rn(u, float(i)));
+}
+__device__ __forceinline__ void axis_term(double l, int n, int& i0, double& f) {
+  const double u = mul_rn(mul_rn(add_rn(l, 1.0), 0.5), double(n - 1));
+  const double fl = floor(u);
+  const int i = (fl >= 0.0 && fl <= double(n - 2)) ? int(fl) : (fl > 0.0 ? n - 2 : 0);
+  i0 = i;
+  f = fmin(fmax(sub_rn(u, double(i)), 0.0), 1.0);
 }
 
 template <typename T>
@@ -137,6 +143,21 @@ __device__ __forceinline__ void interp_pair(const ModelDev<float>& md, int m, co
   }
 }
 
+// Two channels in f32 arithmetic (training fast path: lerps rounded in f32 instead of
+// f64; features differ from the bit-exact encoder by <= 1 ulp).
+__device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, int W, int HW, int vbase, float fx,
+                                                float fy, float fz, float& o0, float& o1) {
+  const float2* g = reinterpret_cast<const float2*>(grid) + vbase;
+  const float2 a000 = __ldg(g), a001 = __ldg(g + 1), a010 = __ldg(g + W), a011 = __ldg(g + W + 1);
+  const float2 a100 = __ldg(g + HW), a101 = __ldg(g + HW + 1), a110 = __ldg(g + HW + W),
+               a111 = __ldg(g + HW + W + 1);
+  auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
+  o0 = lerp(lerp(lerp(a000.x, a001.x, fx), lerp(a010.x, a011.x, fx), fy),
+            lerp(lerp(a100.x, a101.x, fx), lerp(a110.x, a111.x, fx), fy), fz);
+  o1 = lerp(lerp(lerp(a000.y, a001.y, fx), lerp(a010.y, a011.y, fx), fy),
+            lerp(lerp(a100.y, a101.y, fx), lerp(a110.y, a111.y, fx), fy), fz);
+}
+
 // Encode point (x0,x1,x2) in grid m into out[0..C) (zero outside the grid).
 template <typename T>
 __device__ __forceinline__ void encode_grid_point(const ModelDev<T>& md, int m, T x0, T x1, T x2, T* out,
@@ -164,12 +185,61 @@ __device__ __forceinline__ void atomic_add2(float* addr, float a, float b) {
 
 // Scatter grad g[0..C) of point (x0,x1,x2) in grid m into dgrid (channel-last),
 // weights (wx*wy)*wz in f64 as optim.py:129-152; contributions rounded to T.
+// float, two channels: corner weights and contributions in f32 (the fractions are exact
+// in f32; the reference's f64 products differ by <= 1 ulp per contribution, far inside the
+// 1e-3 gradient tolerance that float atomics already impose).
+__device__ __forceinline__ void scatter_pair_f32(const ModelDev<float>& md, float* __restrict__ dgrid, int m,
+                                                 const Cell& c, float g0, float g1) {
+  const float fx = float(c.fx), fy = float(c.fy), fz = float(c.fz);
+  const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+  const int sy = 2 * md.W, sz = 2 * md.H * md.W;
+  float* base = dgrid + (size_t(((m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix) << 1);
+#pragma unroll
+  for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const float wzy = wy[cy] * wz[cz];
+      float* row = base + cz * sz + cy * sy;
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        const float w = wx[cx] * wzy;
+        atomic_add2(row + 2 * cx, g0 * w, g1 * w);
+      }
+    }
+}
+
+// same from a precomputed base vertex index (vertex units, channel-last C = 2)
+__device__ __forceinline__ void scatter_vertex_f32(const ModelDev<float>& md, float* __restrict__ dgrid, int vbase,
+                                                   float fx, float fy, float fz, float g0, float g1) {
+  const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+  const int sy = 2 * md.W, sz = 2 * md.H * md.W;
+  float* base = dgrid + (size_t(vbase) << 1);
+#pragma unroll
+  for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const float wzy = wy[cy] * wz[cz];
+      float* row = base + cz * sz + cy * sy;
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        const float w = wx[cx] * wzy;
+        atomic_add2(row + 2 * cx, g0 * w, g1 * w);
+      }
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void scatter_grid_point(const ModelDev<T>& md, T* __restrict__ dgrid, int m, T x0, T x1,
                                                    T x2, const T* g, int g_stride) {
   const Cell c = cell_of(md, md.tf + 16 * m, x0, x1, x2);
   if (!c.inside) return;
   const int C = md.C;
+  if constexpr (sizeof(T) == 4) {
+    if (C == 2) {
+      scatter_pair_f32(md, dgrid, m, c, g[0], g[g_stride]);
+      return;
+    }
+  }
   const int64_t sx = C, sy = int64_t(md.W) * C, sz = int64_t(md.H) * md.W * C;
   T* base = dgrid + ((((int64_t)m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix) * C;
   double gv[8];

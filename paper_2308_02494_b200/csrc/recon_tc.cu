@@ -46,7 +46,9 @@ constexpr uint32_t OFF_DW3 = OFF_HEAD + 2 * P * 4;   // [64]
 constexpr uint32_t OFF_RED = OFF_DW3 + HID * 4;      // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
-constexpr uint32_t SMEM_BYTES = OFF_TM + 16;
+constexpr uint32_t OFF_TF = OFF_TM + 16;             // [64][12] transforms (f32)
+constexpr uint32_t SMEM_BYTES = OFF_TF + 64 * 12 * 4;
+constexpr uint32_t TMEM_COLS = 256;                  // z1 | z2 | per-thread cell cache (2 x 64)
 // gF scatter buffer reuses [FH, FH + P*GFS*4) once dW1 has consumed F
 static_assert(P * GFS * 4 <= 2 * P * FE * 4, "gF buffer must fit in the F region");
 
@@ -133,7 +135,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     W2l[o] = lo;
   }
   if (tid < HID) sDW3[tid] = 0.f;
-  if (warp == 0) umma::tmem_alloc(tm_slot, 128);
+  float* sTF = fptr(sm, OFF_TF);
+  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar, 1);
     umma::fence_mbar_init();
@@ -144,6 +148,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   umma::fence_after_sync();
   const uint32_t tmem = *tm_slot;
   const uint32_t TZ1 = tmem, TZ2 = tmem + 64;
+  // this warp's lane quarter; warps w and w+4 use disjoint 64-column halves
+  const uint32_t tmem_cache = tmem + 128 + 64 * (warp >> 2) + (uint32_t(32 * (warp & 3)) << 16);
   const uint32_t sW1h = umma::smem_u32(W1h), sW1l = umma::smem_u32(W1l), sW2h = umma::smem_u32(W2h),
                  sW2l = umma::smem_u32(W2l), sFh = umma::smem_u32(Fh), sFl = umma::smem_u32(Fl),
                  sH1h = umma::smem_u32(H1h), sH1l = umma::smem_u32(H1l);
@@ -187,20 +193,45 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       sT[tid] = ok ? a.targets[i] : 0.f;
     }
     __syncthreads();
-    // ---- encode: lane -> point, warp -> grid ----
-    for (int m = warp; m < 64; m += 8) {
+    // ---- encode: lane -> point, warp -> grid; cell terms cached in TMEM for the scatter ----
+    {
+      const float xa[2][3] = {{sX[3 * lane], sX[3 * lane + 1], sX[3 * lane + 2]},
+                              {sX[3 * (lane + 32)], sX[3 * (lane + 32) + 1], sX[3 * (lane + 32) + 2]}};
+#pragma unroll 1
+      for (int jq = 0; jq < 4; ++jq) {  // 4 groups of (2 grids x 2 points)
+        uint32_t cache[16];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = lane + 32 * h;
-        float f[2];
-        encode_grid_point(md, m, sX[3 * p], sX[3 * p + 1], sX[3 * p + 2], f, 1);
-        float hi0, lo0, hi1, lo1;
-        umma::split_tf32(f[0], hi0, lo0);
-        umma::split_tf32(f[1], hi1, lo1);
-        const uint32_t o = umma::cm_offset(p, 2 * m, 64) >> 2;
-        *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
-        *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
+        for (int u = 0; u < 4; ++u) {
+          const int j = 2 * jq + (u >> 1), h = u & 1;
+          const int m = warp + 8 * j, p = lane + 32 * h;
+          const float* tf = sTF + 12 * m;
+          const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
+          const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
+          const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
+          const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
+          int ix, iy, iz;
+          double fxd, fyd, fzd;
+          axis_term(l0, md.W, ix, fxd);
+          axis_term(l1, md.H, iy, fyd);
+          axis_term(l2, md.D, iz, fzd);
+          const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
+          const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
+          float f0 = 0.f, f1 = 0.f;
+          if (inside) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+          cache[4 * u] = uint32_t(vbase);
+          cache[4 * u + 1] = __float_as_uint(fx);
+          cache[4 * u + 2] = __float_as_uint(fy);
+          cache[4 * u + 3] = __float_as_uint(fz);
+          float hi0, lo0, hi1, lo1;
+          umma::split_tf32(f0, hi0, lo0);
+          umma::split_tf32(f1, hi1, lo1);
+          const uint32_t o = umma::cm_offset(p, 2 * m, 64) >> 2;
+          *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
+          *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
+        }
+        umma::tmem_st16(tmem_cache + 16 * jq, cache);
       }
+      umma::tmem_st_wait();
     }
     umma::fence_async_smem();
     __syncthreads();
@@ -399,14 +430,23 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       }
     }
     __syncthreads();
-    // ---- scatter ----
-    for (int m = warp; m < 64; m += 8) {
+    // ---- scatter (cell terms from the TMEM cache written by this thread during encode) ----
+#pragma unroll 1
+    for (int jq = 0; jq < 4; ++jq) {
+      uint32_t cache[16];
+      umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = lane + 32 * h;
-        if (p < cnt) scatter_grid_point(md, a.dgrid, m, sX[3 * p], sX[3 * p + 1], sX[3 * p + 2], GF + p * GFS + 2 * m, 1);
+      for (int u = 0; u < 4; ++u) {
+        const int j = 2 * jq + (u >> 1), h = u & 1;
+        const int m = warp + 8 * j, p = lane + 32 * h;
+        const int vbase = int(cache[4 * u]);
+        if (vbase < 0 || p >= cnt) continue;
+        const float2 g = *reinterpret_cast<const float2*>(GF + p * GFS + 2 * m);
+        scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
+                           __uint_as_float(cache[4 * u + 3]), g.x, g.y);
       }
     }
+    umma::fence_before_sync();
     __syncthreads();
   }
 
@@ -441,7 +481,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   if (tid == 0) a.part_loss[blockIdx.x] = bl;
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tmem, 128);
+  if (warp == 0) umma::tmem_dealloc(tmem, TMEM_COLS);
 }
 
 }  // namespace tc
