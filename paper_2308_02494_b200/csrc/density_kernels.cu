@@ -283,6 +283,132 @@ __global__ void k_dens_finalize(T* __restrict__ tf, int M, int p, const double* 
   }
 }
 
+// ---- float-model fast path: the per-(point, grid) bump work in f32 (SFU exp), the
+// per-point target/loss pipeline and all reductions in f64.  Bumps below the f32
+// range (q > ~87) flush to zero instead of ~1e-38..1e-304; their share of rho and of
+// the gradient is below f32 resolution of the sums they enter.
+__device__ __forceinline__ void bump32(const float* a, float x0, float x1, float x2, int p, float& bump, float* l,
+                                       float* lp) {
+  l[0] = fmaf(a[0], x0, fmaf(a[1], x1, fmaf(a[2], x2, a[3])));
+  l[1] = fmaf(a[4], x0, fmaf(a[5], x1, fmaf(a[6], x2, a[7])));
+  l[2] = fmaf(a[8], x0, fmaf(a[9], x1, fmaf(a[10], x2, a[11])));
+  float q = 0.f;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const float s = l[d] * l[d];
+    float r;  // s^(p-1)
+    if (p == 10) {
+      const float s2 = s * s, s4 = s2 * s2, s8 = s4 * s4;
+      r = s8 * s;
+    } else {
+      r = 1.f;
+      for (int e = 0; e < p - 1; ++e) r *= s;
+    }
+    lp[d] = l[d] * r;  // local^(2p-1)
+    q = fmaf(r, s, q);
+  }
+  bump = (q <= 700.f) ? __expf(-q) : 0.f;
+}
+
+__device__ void stage_transforms32(const float* __restrict__ tf, int M, float* s_tf) {
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    double a[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) a[e] = double(tf[16 * m + e]);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) s_tf[13 * m + e] = float(a[e]);
+    const double c0 = a[5] * a[10] - a[6] * a[9], c1 = a[6] * a[8] - a[4] * a[10], c2 = a[4] * a[9] - a[5] * a[8];
+    s_tf[13 * m + 12] = float(fabs(a[0] * c0 + a[1] * c1 + a[2] * c2));
+  }
+}
+
+template <typename TE>
+__global__ void __launch_bounds__(kDensThreads) k_dens_rho32(const float* __restrict__ tf, int M, int p,
+                                                             const float* __restrict__ x, const TE* __restrict__ err,
+                                                             int64_t n, double* __restrict__ rho,
+                                                             double* __restrict__ part, const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  extern __shared__ float s_tf32[];
+  __shared__ double red[32];
+  stage_transforms32(tf, M, s_tf32);
+  __syncthreads();
+  double srho = 0.0, serr = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float x0 = x[3 * i], x1 = x[3 * i + 1], x2 = x[3 * i + 2];
+    float r = 0.f;
+    for (int m = 0; m < M; ++m) {
+      const float* a = s_tf32 + 13 * m;
+      float b, l[3], lp[3];
+      bump32(a, x0, x1, x2, p, b, l, lp);
+      r = fmaf(a[12], b, r);
+    }
+    rho[i] = double(r);
+    srho += double(r);
+    if (err) serr += double(err[i]);
+  }
+  srho = block_sum(srho, red);
+  serr = block_sum(serr, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = srho;
+    part[2 * blockIdx.x + 1] = serr;
+  }
+}
+
+// d_rho = (d_s - sum(d_s rho_s)) / sum(rho) per point, once (optim.py:182-183), as f32
+__global__ void k_dens_drho32(const double* __restrict__ d_s, int64_t n, const double* __restrict__ stats,
+                              float* __restrict__ drho, const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  const double total = stats[0], S = stats[3];
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    drho[i] = float((d_s[i] - S) / total);
+}
+
+__global__ void __launch_bounds__(kDensThreads) k_dens_grad32(const float* __restrict__ tf, int M, int p,
+                                                              const float* __restrict__ x, int64_t n,
+                                                              const float* __restrict__ drho,
+                                                              double* __restrict__ part, const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  __shared__ double red[32];
+  __shared__ float a[13];
+  const int m = blockIdx.y;
+  if (threadIdx.x == 0) stage_transforms32(tf + 16 * m, 1, a);
+  __syncthreads();
+  const float adet = a[12];
+  float acc[13];
+#pragma unroll
+  for (int e = 0; e < 13; ++e) acc[e] = 0.f;
+  const int64_t chunk = ceil_div(n, int64_t(gridDim.x));
+  const int64_t lo = blockIdx.x * chunk, hi = min64(n, lo + chunk);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float x0 = x[3 * i], x1 = x[3 * i + 1], x2 = x[3 * i + 2];
+    float b, l[3], lp[3];
+    bump32(a, x0, x1, x2, p, b, l, lp);
+    if (!(b > 0.f)) continue;
+    const float w = drho[i] * b;
+    const float s = adet * w;
+    acc[0] += w;
+    const float sl0 = s * lp[0], sl1 = s * lp[1], sl2 = s * lp[2];
+    acc[1] = fmaf(sl0, x0, acc[1]);
+    acc[2] = fmaf(sl0, x1, acc[2]);
+    acc[3] = fmaf(sl0, x2, acc[3]);
+    acc[4] = fmaf(sl1, x0, acc[4]);
+    acc[5] = fmaf(sl1, x1, acc[5]);
+    acc[6] = fmaf(sl1, x2, acc[6]);
+    acc[7] = fmaf(sl2, x0, acc[7]);
+    acc[8] = fmaf(sl2, x1, acc[8]);
+    acc[9] = fmaf(sl2, x2, acc[9]);
+    acc[10] += sl0;
+    acc[11] += sl1;
+    acc[12] += sl2;
+  }
+  double* dst = part + (int64_t(blockIdx.x) * M + m) * 13;
+#pragma unroll
+  for (int e = 0; e < 13; ++e) {
+    const double v = block_sum(double(acc[e]), red);
+    if (threadIdx.x == 0) dst[e] = v;
+  }
+}
+
 struct DensPlan {
   int nb1, chunks;
 };
@@ -324,16 +450,38 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
     set_error("density workspace too small: need %zu, have %zu", c.used, wsb);
     return APMG_E_WORKSPACE;
   }
-  const size_t smem1 = size_t(13) * M * sizeof(double);
-  APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_rho<T, TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem1)));
-  APMG_LAUNCH("density_rho", (k_dens_rho<T, TE>), d.nb1, kDensThreads, smem1, st, tf, M, p, x, err, n, rho, part1,
-              ctl);
+  const char* e64 = getenv("APMG_DENSITY64");  // force the all-fp64 per-pair path (A/B tests)
+  const bool fast32 = (sizeof(T) == 4) && !(e64 && e64[0] == '1');
+  if constexpr (sizeof(T) == 4) {
+    if (fast32) {
+      const size_t smem32 = size_t(13) * M * sizeof(float);
+      APMG_CUDA_TRY(
+          cudaFuncSetAttribute(k_dens_rho32<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem32)));
+      APMG_LAUNCH("density_rho", k_dens_rho32<TE>, d.nb1, kDensThreads, smem32, st, tf, M, p, x, err, n, rho, part1,
+                  ctl);
+    }
+  }
+  if (!fast32) {
+    const size_t smem1 = size_t(13) * M * sizeof(double);
+    APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_rho<T, TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem1)));
+    APMG_LAUNCH("density_rho", (k_dens_rho<T, TE>), d.nb1, kDensThreads, smem1, st, tf, M, p, x, err, n, rho, part1,
+                ctl);
+  }
   APMG_LAUNCH("density_stats", k_dens_stats1, 1, 1024, 0, st, part1, d.nb1, n, stats, ctl);
   APMG_LAUNCH("density_target", k_dens_target<TE>, d.nb1, kDensThreads, 0, st, rho, err, n, stats, d_s, part2, ctl);
   APMG_LAUNCH("density_stats", k_dens_stats2, 1, 1024, 0, st, part2, d.nb1, n, stats, loss,
               const_cast<TrainCtl*>(ctl));
-  APMG_LAUNCH("density_grad", k_dens_grad<T>, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, d_s, stats,
-              part3, ctl);
+  if constexpr (sizeof(T) == 4) {
+    if (fast32) {
+      float* drho = reinterpret_cast<float*>(rho);  // rho is dead once the target pass has run
+      APMG_LAUNCH("density_drho", k_dens_drho32, d.nb1, kDensThreads, 0, st, d_s, n, stats, drho, ctl);
+      APMG_LAUNCH("density_grad", k_dens_grad32, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, drho, part3,
+                  ctl);
+    }
+  }
+  if (!fast32)
+    APMG_LAUNCH("density_grad", k_dens_grad<T>, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, d_s, stats,
+                part3, ctl);
   APMG_LAUNCH("density_finalize", k_dens_finalize<T>, int(ceil_div(M, 64)), 64, 0, st, tf, M, p, part3, d.chunks,
               dtf, adam_m, adam_v, ctl);
   if (rho_total) APMG_CUDA_TRY(cudaMemcpyAsync(rho_total, stats, sizeof(double), cudaMemcpyDeviceToDevice, st));

@@ -47,12 +47,16 @@ constexpr uint32_t OFF_RED = OFF_DW3 + HID * 4;      // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 16;             // [64][12] transforms (f32)
-constexpr uint32_t SMEM_BYTES = OFF_TF + 64 * 12 * 4;
+constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;    // [64]
+constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
 constexpr uint32_t TMEM_COLS = 256;                  // z1 | z2 | per-thread cell cache (2 x 64)
 // gF scatter buffer reuses [FH, FH + P*GFS*4) once dW1 has consumed F
 static_assert(P * GFS * 4 <= 2 * P * FE * 4, "gF buffer must fit in the F region");
 
 __device__ __forceinline__ float* fptr(unsigned char* sm, uint32_t off) { return reinterpret_cast<float*>(sm + off); }
+
+// float index of column c in a 64-row CM buffer (row part: (r/8)*32 + (r%8)*4)
+__device__ __forceinline__ uint32_t cm_col(int c) { return uint32_t((c >> 2) * 256 + (c & 3)); }
 
 // dz1 storage (stride 64, XOR swizzle on 4-float groups to keep fragment loads conflict-free)
 __device__ __forceinline__ int dz1_idx(int p, int i) { return p * 64 + (i ^ ((p & 7) << 2)); }
@@ -89,6 +93,7 @@ struct Args {
   float* part_dw;
   double* part_loss;
   const TrainCtl* ctl;
+  int aggregate;  // warp-aggregated scatter (APMG_SCATTER_AGG=0 disables, for A/B)
 };
 
 __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
@@ -137,6 +142,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   if (tid < HID) sDW3[tid] = 0.f;
   float* sTF = fptr(sm, OFF_TF);
   for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  float* sW3 = fptr(sm, OFF_W3);
+  if (tid < HID) sW3[tid] = md.w3[tid];
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar, 1);
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         h2v[c] = fmaxf(h2v[c], 0.f);
-        part = fmaf(h2v[c], __ldg(md.w3 + ep_col0 + c), part);
+        part = fmaf(h2v[c], sW3[ep_col0 + c], part);
       }
       sHead[(warp >> 2) * P + ep_row] = part;
     }
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       for (int c = 0; c < 32; ++c) {
         const float hv = h2v[c];
         dw3_acc[c] = fmaf(g, hv, dw3_acc[c]);
-        DZ2[ep_row * DZS + ep_col0 + c] = hv > 0.f ? __fmul_rn(g, __ldg(md.w3 + ep_col0 + c)) : 0.f;
+        DZ2[ep_row * DZS + ep_col0 + c] = hv > 0.f ? __fmul_rn(g, sW3[ep_col0 + c]) : 0.f;
       }
     }
     __syncthreads();
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int ncol = 8 * (nt0 + t) + gid;  // i
-          const uint32_t o0 = umma::cm_offset(k0, ncol, 64) >> 2, o1 = umma::cm_offset(k0 + 4, ncol, 64) >> 2;
+          const uint32_t o0 = kk * 32 + tig * 4 + cm_col(ncol), o1 = o0 + 16;
           const uint32_t bh[2] = {__float_as_uint(W2h[o0]), __float_as_uint(W2h[o1])};
           const uint32_t bl[2] = {__float_as_uint(W2l[o0]), __float_as_uint(W2l[o1])};
           mma_tf32_16x8x8(d[t], ah, bh);
@@ -374,8 +381,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int ic = 8 * (4 * (warp & 1) + t) + gid;
-          const uint32_t bv[2] = {__float_as_uint(H1h[umma::cm_offset(pk, ic, 64) >> 2]),
-                                  __float_as_uint(H1h[umma::cm_offset(pk + 4, ic, 64) >> 2])};
+          const uint32_t ob = kk * 32 + tig * 4 + cm_col(ic);
+          const uint32_t bv[2] = {__float_as_uint(H1h[ob]), __float_as_uint(H1h[ob + 16])};
           mma_tf32_16x8x8(acc2[t], av, bv);
         }
       }
@@ -388,8 +395,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const int kc = 8 * (8 * (warp & 1) + t) + gid;
-          const uint32_t bv[2] = {__float_as_uint(Fh[umma::cm_offset(pk, kc, 64) >> 2]),
-                                  __float_as_uint(Fh[umma::cm_offset(pk + 4, kc, 64) >> 2])};
+          const uint32_t ob = kk * 32 + tig * 4 + cm_col(kc);
+          const uint32_t bv[2] = {__float_as_uint(Fh[ob]), __float_as_uint(Fh[ob + 16])};
           mma_tf32_16x8x8(acc1[t], av, bv);
         }
       }
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const int kc = 8 * (nt0 + t) + gid;  // feature column
-          const uint32_t o0 = umma::cm_offset(k0, kc, 64) >> 2, o1 = umma::cm_offset(k0 + 4, kc, 64) >> 2;
+          const uint32_t o0 = kk * 32 + tig * 4 + cm_col(kc), o1 = o0 + 16;
           const uint32_t bh[2] = {__float_as_uint(W1h[o0]), __float_as_uint(W1h[o1])};
           const uint32_t bl[2] = {__float_as_uint(W1l[o0]), __float_as_uint(W1l[o1])};
           mma_tf32_16x8x8(d[t], ah, bh);
@@ -440,10 +447,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         const int j = 2 * jq + (u >> 1), h = u & 1;
         const int m = warp + 8 * j, p = lane + 32 * h;
         const int vbase = int(cache[4 * u]);
-        if (vbase < 0 || p >= cnt) continue;
-        const float2 g = *reinterpret_cast<const float2*>(GF + p * GFS + 2 * m);
-        scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
-                           __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+        const bool valid = vbase >= 0 && p < cnt;
+        float2 g = make_float2(0.f, 0.f);
+        if (valid) g = *reinterpret_cast<const float2*>(GF + p * GFS + 2 * m);
+        if (a.aggregate)
+          scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+                                  __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+        else if (valid)
+          scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
+                             __uint_as_float(cache[4 * u + 3]), g.x, g.y);
       }
     }
     umma::fence_before_sync();
@@ -501,7 +513,8 @@ int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, c
                                        int(tc::SMEM_BYTES)));
     attr = true;
   }
-  tc::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl};
+  const char* ea = getenv("APMG_SCATTER_AGG");
+  tc::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1};
   APMG_LAUNCH("recon_fwd_bwd_tc", tc::k_recon_tc, grid, tc::NT, tc::SMEM_BYTES, st, a);
   return APMG_OK;
 }

@@ -175,8 +175,11 @@ def test_density_loss_and_grads(golden, prefix):
     m = model_from(g, prefix)
     loss, dg = PO.density_loss_and_grads(m, g[prefix + "coords"], g[prefix + "errors"])
     ref_loss = float(g[prefix + "loss"])
-    assert loss == pytest.approx(ref_loss, rel=1e-9, abs=1e-15)
-    assert tensor_rel(dg["transforms"], g[prefix + "g_transforms"]) <= 1e-6
+    # float models evaluate the per-(point, grid) bumps in f32 (fp64 per-point pipeline and
+    # reductions); float64 models run the all-fp64 path
+    f32 = m.dtype == np.float32
+    assert loss == pytest.approx(ref_loss, rel=1e-6 if f32 else 1e-9, abs=1e-15)
+    assert tensor_rel(dg["transforms"], g[prefix + "g_transforms"]) <= (1e-4 if f32 else 1e-6)
     assert not dg["transforms"][:, 3, :].any()
     rho = PD.feature_density(m.transforms, g[prefix + "coords"], m.config.flat_top_p)
     np.testing.assert_allclose(rho, g[prefix + "rho"], rtol=1e-13, atol=0)
