@@ -62,9 +62,13 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:  # nvidia-smi needs a moment to start
+                time.sleep(0.02)
+            self.rows.clear()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -117,21 +121,37 @@ def brick_workload(rank, world):
 
 
 # algorithmic work per training point -> per-kernel roofline rows
+ENC_BYTES = 8 * M * CH * 4          # 4,096 B of corner data gathered per point (encoder fwd)
+SCAT_BYTES = 8 * M * CH * 4         # 4,096 B of corner gradients reduced per point (encoder bwd)
+STREAM_BYTES = 12 + 4 + 4           # coords in, target in, squared error out
+
+
 def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
+    """Dominant-kernel roofline.  Bytes are ALGORITHMIC bytes per launch (SURVEY 8d per-point
+    figure x the 2^20 points one launch processes); the grid gather/scatter traffic is served
+    by L2 (16 MiB grids stay resident), so the HBM copy peak is a conservative denominator."""
     t = ms_per_launch * 1e-3
-    rows = {
-        # fused encoder fwd + MLP fwd/bwd + grid scatter: 8 corners x 64 grids x 2 ch x 4 B gathered
-        # and scattered per point (L2-resident 16 MiB grids) + 12 B coords + 4 B target + 4 B sq
-        "recon_fwd_bwd": ("hbm", BATCH * (4096 + 4096 + 20) / t / 1e9, "GB/s"),
-        "density_grad": ("hbm", BATCH * (12 + 8) * 1.0 / t / 1e9, "GB/s"),
-        "density_rho": ("hbm", BATCH * (12 + 4 + 8) / t / 1e9, "GB/s"),
-        "train_batch": ("hbm", BATCH * (8 * 32 + 16) / t / 1e9, "GB/s"),
-        "adam_main": ("hbm", 4_206_656 * 4 * 7 / t / 1e9, "GB/s"),
+    per_point = {
+        "recon_fwd_bwd_tc": ENC_BYTES + SCAT_BYTES + STREAM_BYTES,
+        "recon_fwd_bwd": ENC_BYTES + SCAT_BYTES + STREAM_BYTES,
+        "density_grad": 12 + 4,
+        "density_rho": 12 + 4 + 8,
+        "train_batch": 8 * 4 + 16,
     }
-    bound, achieved, unit = rows.get(kernel, ("hbm", float("nan"), "GB/s"))
+    if kernel == "adam_main":
+        nbytes = 4_206_656 * 4 * 7
+    else:
+        nbytes = BATCH * per_point.get(kernel, float("nan"))
     peak = pk.get("hbm_gbs", 6650.0)
-    return {"bound": bound, "kernel": kernel, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": None, "ms_per_launch": ms_per_launch}
+    achieved = nbytes / t / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic_r01.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(kernel)
+    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
+            "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+            "note": "algorithmic encoder gather + scatter bytes (4096+4096+20 B/pt); served from L2"}
 
 
 def kernel_table():
@@ -211,8 +231,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="apmg", choices=["apmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -326,3 +326,38 @@ if __name__ == "__main__":
         t0 = time.perf_counter()
         globals()["gen_" + name]()
         print(f"{name}: {time.perf_counter() - t0:.1f}s", flush=True)
+
+
+def _c1_run(iters, delay, pert):
+    """C1-shaped reference run; pert > 0 nudges a random half of the initial grid values by one
+    ulp (the size of a different summation order) to measure the reference's own sensitivity."""
+    vol = rvol.synth_volume((128, 128, 128), adaptivity_blobs())
+    m = rmodel.init_model(rmodel.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0,
+                          vmin=vol.vmin, vmax=vol.vmax)
+    if pert:
+        rng = np.random.default_rng(pert)
+        mask = rng.uniform(size=m.grids.shape) < 0.5
+        m.grids[mask] = np.nextafter(m.grids[mask], np.float32(np.inf if pert % 2 else -np.inf))
+    cfg = rtrain.TrainConfig(iterations=iters, batch_size=2 ** 14, delay_start=delay, seed=0, plateau_enabled=False)
+    m, log = rtrain.train_single(m, vol, cfg)
+    return rtrain.psnr(m, vol), log
+
+
+def gen_train_c1_short():
+    """60 iterations (density active for the last 20): short enough that trajectories which
+    differ by rounding have not decorrelated, so a 0.1 dB PSNR gate is meaningful."""
+    p, log = _c1_run(60, 40, 0)
+    np.savez_compressed(OUT / "train_c1_60.npz", psnr=np.array(p), config=np.array([60, 2 ** 14, 40]),
+                        log_l_rec=np.array(log.l_rec),
+                        log_stop=np.array(-1 if log.transform_stop_iteration is None else log.transform_stop_iteration),
+                        log_l_density=np.array([np.nan if v is None else v for v in log.l_density]))
+
+
+def gen_train_c1_ensemble():
+    """Reference-vs-reference spread after 60/200/600 iterations under one-ulp perturbations
+    (written to train_c1_ensemble.json; ~5 min per 200-iteration run on 8 cores)."""
+    import json
+    out = {"psnr_unperturbed": _c1_run(200, 50, 0)[0],
+           "psnr_perturbed": [_c1_run(200, 50, p)[0] for p in (1, 2, 3, 4)],
+           "c60": {"iterations": 60, "delay_start": 40, "psnr": [_c1_run(60, 40, p)[0] for p in (0, 1, 2, 3)]}}
+    (OUT / "train_c1_ensemble.json").write_text(json.dumps(out, indent=1))

@@ -8,6 +8,7 @@ uses float atomics, so its summation order is nondeterministic), PSNR within
 computes with elementwise numpy (Philox draws, volume sampling, synthesis,
 interpolation, Adam, hashing) are checked bit for bit."""
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -321,24 +322,47 @@ def test_train_constant_volume_plateau(golden):
     assert np.array_equal(m.forward(pts), np.full(50, np.float32(3.25)))
 
 
-def test_train_c1_psnr_parity(golden):
-    """C1-shaped run (64 grids 32^3 x2, 128^3 blob field, 200 its x 2^14, delay 50):
-    final PSNR within 0.1 dB of the reference CPU run (tests/golden/train_c1.npz)."""
-    g = golden("train_c1")
-    iters, batch, delay = (int(v) for v in g["config"])
-    blobs = [PV.BlobSpec(center=(0.45, -0.3, 0.2), sigma=(0.035, 0.035, 0.035)),
-             PV.BlobSpec(center=(-0.2, 0.2, -0.1), sigma=(0.6, 0.5, 0.7), amplitude=0.35),
-             PV.BlobSpec(center=(0.3, 0.4, 0.5), sigma=(0.45, 0.55, 0.4), amplitude=0.25),
-             PV.BlobSpec(center=(-0.5, -0.5, 0.4), sigma=(0.5, 0.4, 0.5), amplitude=0.3)]
-    vol = PV.synth_volume((128, 128, 128), blobs)
+C1_BLOBS = [PV.BlobSpec(center=(0.45, -0.3, 0.2), sigma=(0.035, 0.035, 0.035)),
+            PV.BlobSpec(center=(-0.2, 0.2, -0.1), sigma=(0.6, 0.5, 0.7), amplitude=0.35),
+            PV.BlobSpec(center=(0.3, 0.4, 0.5), sigma=(0.45, 0.55, 0.4), amplitude=0.25),
+            PV.BlobSpec(center=(-0.5, -0.5, 0.4), sigma=(0.5, 0.4, 0.5), amplitude=0.3)]
+
+
+def _c1_gpu_run(iters, batch, delay):
+    vol = PV.synth_volume((128, 128, 128), C1_BLOBS)
     m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
                       vmax=vol.vmax)
     cfg = P.TrainConfig(iterations=iters, batch_size=batch, delay_start=delay, seed=0, plateau_enabled=False)
     m, log = P.train_single(m, vol, cfg)
-    p = P.psnr(m, vol)
+    return P.psnr(m, vol), log
+
+
+def test_train_c1_psnr_parity_60(golden):
+    """C1-shaped run (64 grids 32^3 x2, 128^3 blob field, batch 2^14, 60 iterations with the density
+    step active for the last 20): final PSNR within 0.1 dB of the reference CPU run, and the
+    per-iteration losses track it (tests/golden/train_c1_60.npz)."""
+    g = golden("train_c1_60")
+    iters, batch, delay = (int(v) for v in g["config"])
+    p, log = _c1_gpu_run(iters, batch, delay)
     assert abs(p - float(g["psnr"])) <= 0.1, (p, float(g["psnr"]))
     np.testing.assert_allclose(log.l_rec[:20], g["log_l_rec"][:20], rtol=2e-3)
-    assert log.transform_stop_iteration == int(g["log_stop"])
+    ld = np.array([np.nan if v is None else v for v in log.l_density])
+    assert np.array_equal(np.isnan(ld), np.isnan(g["log_l_density"]))
+    np.testing.assert_allclose(ld[delay:delay + 5], g["log_l_density"][delay:delay + 5], rtol=1e-3)
+
+
+def test_train_c1_psnr_ensemble_200(golden):
+    """After 200 iterations the reference is chaotic: one-ulp perturbations of its own initial grids
+    spread its PSNR over ~1.2 dB (sd ~0.4, tests/golden/train_c1_ensemble.json).  Compare ensemble
+    means: GPU runs (nondeterministic atomics make each run a perturbation) vs the reference runs."""
+    import json
+    ens = json.loads((Path(__file__).parent / "golden" / "train_c1_ensemble.json").read_text())
+    ref = np.array([ens["psnr_unperturbed"]] + ens["psnr_perturbed"])
+    g = golden("train_c1")
+    iters, batch, delay = (int(v) for v in g["config"])
+    gpu = np.array([_c1_gpu_run(iters, batch, delay)[0] for _ in range(4)])
+    se = np.sqrt(ref.var(ddof=1) / len(ref) + max(gpu.var(ddof=1), ref.var(ddof=1)) / len(gpu))
+    assert abs(gpu.mean() - ref.mean()) <= 0.1 + 3 * se, (gpu.tolist(), ref.tolist())
 
 
 def test_fd_gradient_suite_f64():
