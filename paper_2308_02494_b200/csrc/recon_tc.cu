@@ -22,7 +22,17 @@ namespace apmg {
 namespace tc {
 
 constexpr int P = 64;        // points per tile (M of the tcgen05 products)
-constexpr int NT = 256;      // 8 warps
+#ifndef APMG_TC_WARPS
+#define APMG_TC_WARPS 16
+#endif
+constexpr int NW = APMG_TC_WARPS;  // warps per CTA (8 or 16)
+constexpr int NT = 32 * NW;
+constexpr int WQ = NW / 4;         // warps sharing one TMEM lane quarter
+constexpr int EPC = 64 / WQ;       // accumulator columns per warp in the epilogues
+constexpr int GPW = 64 / NW;       // grids per warp in encode / scatter
+constexpr int MT_N64 = 32 / NW;    // 16x8 n-tiles per warp, 64-wide products
+constexpr int MT_N128 = 64 / NW;   // 16x8 n-tiles per warp, 128-wide products
+static_assert(NW == 8 || NW == 16, "tile mappings assume 8 or 16 warps");
 constexpr int FE = 128;      // features
 constexpr int HID = 64;
 constexpr int DZS = 68;      // row stride (floats) of the plain dz2 buffer
@@ -37,21 +47,21 @@ constexpr uint32_t OFF_FH = OFF_W2L + 64 * 64 * 4;
 constexpr uint32_t OFF_FL = OFF_FH + P * FE * 4;
 constexpr uint32_t OFF_H1H = OFF_FL + P * FE * 4;
 constexpr uint32_t OFF_H1L = OFF_H1H + P * HID * 4;  // later: dz1 (swizzled, stride 64)
-constexpr uint32_t OFF_DZ2 = OFF_H1L + P * HID * 4;
+// gF scatter buffer [P][GFS] reuses the h1 hi/lo region (h1 and dz1 are dead once gF is formed)
+constexpr uint32_t GF_BYTES = (P * GFS * 4 > 2 * P * HID * 4) ? P * GFS * 4 : 2 * P * HID * 4;
+constexpr uint32_t OFF_DZ2 = OFF_H1H + GF_BYTES;
 constexpr uint32_t OFF_X = OFF_DZ2 + P * DZS * 4;
 constexpr uint32_t OFF_T = OFF_X + P * 3 * 4;
 constexpr uint32_t OFF_G = OFF_T + P * 4;
-constexpr uint32_t OFF_HEAD = OFF_G + P * 4;         // [2][P] head partial sums
-constexpr uint32_t OFF_DW3 = OFF_HEAD + 2 * P * 4;   // [64]
+constexpr uint32_t OFF_HEAD = OFF_G + P * 4;         // [WQ][P] head partial sums
+constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;  // [64]
 constexpr uint32_t OFF_RED = OFF_DW3 + HID * 4;      // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 16;             // [64][12] transforms (f32)
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;    // [64]
 constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
-constexpr uint32_t TMEM_COLS = 256;                  // z1 | z2 | per-thread cell cache (2 x 64)
-// gF scatter buffer reuses [FH, FH + P*GFS*4) once dW1 has consumed F
-static_assert(P * GFS * 4 <= 2 * P * FE * 4, "gF buffer must fit in the F region");
+constexpr uint32_t TMEM_COLS = 512;                  // z1 | z2 | cell cache, double-buffered (2 x 128)
 
 __device__ __forceinline__ float* fptr(unsigned char* sm, uint32_t off) { return reinterpret_cast<float*>(sm + off); }
 
@@ -94,7 +104,35 @@ struct Args {
   double* part_loss;
   const TrainCtl* ctl;
   int aggregate;  // warp-aggregated scatter (APMG_SCATTER_AGG=0 disables, for A/B)
+  int skip;       // timing breakdown only (APMG_TC_SKIP): 1 scatter, 2 backward MMAs, 4 gathers
 };
+
+// Grid-gradient scatter of one tile: thread (warp, lane) owns points lane, lane + 32 and
+// grids warp + NW*j, exactly the items it encoded; their cell terms come back from its TMEM
+// cache, their feature gradients from GF [P][GFS].
+__device__ __forceinline__ void scatter_tile(const ModelDev<float>& md, const Args& a, const float* GF,
+                                             uint32_t tmem_cache, int cnt, int warp, int lane) {
+#pragma unroll 1
+  for (int jq = 0; jq < (a.skip & 1 ? 0 : GPW / 2); ++jq) {
+    uint32_t cache[16];
+    umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 2 * jq + (u >> 1), h = u & 1;
+      const int m = warp + NW * j, p = lane + 32 * h;
+      const int vbase = int(cache[4 * u]);
+      const bool valid = vbase >= 0 && p < cnt;
+      float2 g = make_float2(0.f, 0.f);
+      if (valid) g = *reinterpret_cast<const float2*>(GF + p * GFS + 2 * m);
+      if (a.aggregate)
+        scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+                                __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+      else if (valid)
+        scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
+                           __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -112,7 +150,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   float* H1l = fptr(sm, OFF_H1L);
   float* DZ1 = fptr(sm, OFF_H1L);  // reuses h1_lo after the z2 product
   float* DZ2 = fptr(sm, OFF_DZ2);
-  float* GF = fptr(sm, OFF_FH);    // reuses F after dW1
+  float* GF = fptr(sm, OFF_H1H);   // reuses h1/dz1 after gF (read by the next tile's scatter)
   float* sX = fptr(sm, OFF_X);
   float* sT = fptr(sm, OFF_T);
   float* sG = fptr(sm, OFF_G);
@@ -155,40 +193,50 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   umma::fence_after_sync();
   const uint32_t tmem = *tm_slot;
   const uint32_t TZ1 = tmem, TZ2 = tmem + 64;
-  // this warp's lane quarter; warps w and w+4 use disjoint 64-column halves
-  const uint32_t tmem_cache = tmem + 128 + 64 * (warp >> 2) + (uint32_t(32 * (warp & 3)) << 16);
+  // this warp's lane quarter; the WQ warps sharing it use disjoint 8*GPW-column slices;
+  // buffer (tile parity) b at +128*b: encode(t) fills one while scatter(t-1) drains the other
+  const uint32_t tmem_cache0 = tmem + 128 + 8 * GPW * (warp >> 2) + (uint32_t(32 * (warp & 3)) << 16);
   const uint32_t sW1h = umma::smem_u32(W1h), sW1l = umma::smem_u32(W1l), sW2h = umma::smem_u32(W2h),
                  sW2l = umma::smem_u32(W2l), sFh = umma::smem_u32(Fh), sFl = umma::smem_u32(Fl),
                  sH1h = umma::smem_u32(H1h), sH1l = umma::smem_u32(H1l);
   const uint32_t idesc64 = umma::idesc_tf32(64, 64, false, false);
   const float coef = __fmul_rn(float(2.0 / double(a.n)), md.span);
 
-  // persistent weight-gradient accumulators (mma.sync fragments)
-  // dW1 [64 i][128 k]: warp w owns m-tile w/2 (16 rows) and n-tiles 8*(w%2)..+7 (8 cols each)
-  float acc1[8][4];
-  // dW2 [64 j][64 i]: warp w owns m-tile w/2, n-tiles 4*(w%2)..+3
-  float acc2[4][4];
+  // persistent weight-gradient accumulators (mma.sync fragments); warp w owns m-tile
+  // mt = w / WQ (16 rows) and a contiguous run of 8-column n-tiles
+  const int mt = warp / WQ, wn = warp % WQ;
+  float acc1[MT_N128][4];  // dW1 [64 i][128 k]: n-tiles MT_N128*wn ..
+  float acc2[MT_N64][4];   // dW2 [64 j][64 i]:  n-tiles MT_N64*wn ..
 #pragma unroll
-  for (int t = 0; t < 8; ++t)
+  for (int t = 0; t < MT_N128; ++t)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc1[t][e] = 0.f;
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < MT_N64; ++t)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc2[t][e] = 0.f;
-  float dw3_acc[32];
+  float dw3_acc[EPC];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) dw3_acc[c] = 0.f;
+  for (int c = 0; c < EPC; ++c) dw3_acc[c] = 0.f;
   double loss = 0.0;
   uint32_t phase = 0;
 
   // TMEM epilogue mapping (M=64 accumulator: row 16*(w%4)+t lives in lane 32*(w%4)+t, t < 16)
   const int ep_row = 16 * (warp & 3) + lane;  // valid when lane < 16
-  const int ep_col0 = 32 * (warp >> 2);        // warps 0-3: columns 0-31, warps 4-7: 32-63
+  const int ep_col0 = EPC * (warp >> 2);       // the WQ warps of a quarter split the 64 columns
   const uint32_t ep_lane = uint32_t(32 * (warp & 3)) << 16;
 
   const int64_t tiles = ceil_div(a.n, P);
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  // Software pipeline: the scatter of tile t-1 (atomics, shuffles) runs while the tensor
+  // core forms z1 of tile t; its gF rows live in the h1 region until epilogue 1 of tile t.
+  int prev_cnt = 0;
+  for (int64_t tile = blockIdx.x, it = 0;; tile += gridDim.x, ++it) {
+    const bool have = tile < tiles;
+    if (!have) {
+      if (it > 0) scatter_tile(md, a, GF, tmem_cache0 + 128 * uint32_t((it - 1) & 1), prev_cnt, warp, lane);
+      break;
+    }
+    const uint32_t tmem_cache = tmem_cache0 + 128 * uint32_t(it & 1);
     const int64_t p0 = tile * P;
     const int cnt = int(min64(P, a.n - p0));
     if (tid < P) {
@@ -205,12 +253,12 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       const float xa[2][3] = {{sX[3 * lane], sX[3 * lane + 1], sX[3 * lane + 2]},
                               {sX[3 * (lane + 32)], sX[3 * (lane + 32) + 1], sX[3 * (lane + 32) + 2]}};
 #pragma unroll 1
-      for (int jq = 0; jq < 4; ++jq) {  // 4 groups of (2 grids x 2 points)
+      for (int jq = 0; jq < GPW / 2; ++jq) {  // groups of (2 grids x 2 points)
         uint32_t cache[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = 2 * jq + (u >> 1), h = u & 1;
-          const int m = warp + 8 * j, p = lane + 32 * h;
+          const int m = warp + NW * j, p = lane + 32 * h;
           const float* tf = sTF + 12 * m;
           const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
           const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
@@ -224,7 +272,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
           const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
           const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
           float f0 = 0.f, f1 = 0.f;
-          if (inside) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+          if (inside && !(a.skip & 4)) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
           cache[4 * u] = uint32_t(vbase);
           cache[4 * u + 1] = __float_as_uint(fx);
           cache[4 * u + 2] = __float_as_uint(fy);
@@ -254,17 +302,20 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       }
       umma::commit(bar);
     }
+    if (it > 0) scatter_tile(md, a, GF, tmem_cache0 + 128 * uint32_t((it - 1) & 1), prev_cnt, warp, lane);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
+    umma::fence_before_sync();
+    __syncthreads();  // every warp's scatter has consumed GF before epilogue 1 overwrites it
     umma::fence_after_sync();
     // ---- epilogue 1: h1 = relu(z1) -> H1 hi/lo ----
     {
-      float v[32];
-      umma::tmem_ld16(TZ1 + ep_lane + ep_col0, v);
-      umma::tmem_ld16(TZ1 + ep_lane + ep_col0 + 16, v + 16);
+      float v[EPC];
+#pragma unroll
+      for (int c = 0; c < EPC; c += 16) umma::tmem_ld16(TZ1 + ep_lane + ep_col0 + c, v + c);
       if (lane < 16) {
 #pragma unroll
-        for (int c4 = 0; c4 < 32; c4 += 4) {
+        for (int c4 = 0; c4 < EPC; c4 += 4) {
           float hi[4], lo[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) umma::split_tf32(fmaxf(v[c4 + e], 0.f), hi[e], lo[e]);
@@ -293,13 +344,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     phase ^= 1;
     umma::fence_after_sync();
     // ---- epilogue 2: h2, head, loss, dz2, dW3 ----
-    float h2v[32];
-    umma::tmem_ld16(TZ2 + ep_lane + ep_col0, h2v);
-    umma::tmem_ld16(TZ2 + ep_lane + ep_col0 + 16, h2v + 16);
+    float h2v[EPC];
+#pragma unroll
+    for (int c = 0; c < EPC; c += 16) umma::tmem_ld16(TZ2 + ep_lane + ep_col0 + c, h2v + c);
     if (lane < 16) {
       float part = 0.f;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
+      for (int c = 0; c < EPC; ++c) {
         h2v[c] = fmaxf(h2v[c], 0.f);
         part = fmaf(h2v[c], sW3[ep_col0 + c], part);
       }
@@ -310,7 +361,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     if (tid < P) {
       float g = 0.f;
       if (tid < cnt) {
-        const float raw = sHead[tid] + sHead[P + tid];
+        float raw = sHead[tid];
+#pragma unroll
+        for (int q = 1; q < WQ; ++q) raw += sHead[q * P + tid];
         const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
         const float r = __fsub_rn(y, sT[tid]);
         const float s = __fmul_rn(r, r);
@@ -324,7 +377,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     if (lane < 16) {
       const float g = sG[ep_row];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
+      for (int c = 0; c < EPC; ++c) {
         const float hv = h2v[c];
         dw3_acc[c] = fmaf(g, hv, dw3_acc[c]);
         DZ2[ep_row * DZS + ep_col0 + c] = hv > 0.f ? __fmul_rn(g, sW3[ep_col0 + c]) : 0.f;
@@ -332,11 +385,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     }
     __syncthreads();
     // ---- backward 1: dz1 = (dz2 W2) * [h1 > 0]  (M=64 p, N=64 i, K=64 j), 3xTF32 ----
-    {
-      const int mt = warp >> 1, nt0 = 4 * (warp & 1);
-      float d[4][4];
+    if (!(a.skip & 2)) {
+      const int nt0 = MT_N64 * wn;
+      float d[MT_N64][4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < MT_N64; ++t)
 #pragma unroll
         for (int e = 0; e < 4; ++e) d[t][e] = 0.f;
 #pragma unroll 2
@@ -347,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         uint32_t ah[4], al[4];
         split_frag(av, 4, ah, al);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < MT_N64; ++t) {
           const int ncol = 8 * (nt0 + t) + gid;  // i
           const uint32_t o0 = kk * 32 + tig * 4 + cm_col(ncol), o1 = o0 + 16;
           const uint32_t bh[2] = {__float_as_uint(W2h[o0]), __float_as_uint(W2h[o1])};
@@ -358,7 +411,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         }
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < MT_N64; ++t) {
         const int c0 = 8 * (nt0 + t) + 2 * tig;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -370,8 +423,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     }
     __syncthreads();
     // ---- backward 2: weight gradients (single TF32, round-to-nearest operands) ----
-    {
-      const int mt = warp >> 1;
+    if (!(a.skip & 2)) {
       // dW2[j][i] += sum_p dz2[p][j] h1[p][i]   (A = dz2^T, B = h1)
 #pragma unroll 2
       for (int kk = 0; kk < 8; ++kk) {
@@ -379,8 +431,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         const uint32_t av[4] = {tf32_bits(DZ2[pk * DZS + j0]), tf32_bits(DZ2[pk * DZS + j0 + 8]),
                                 tf32_bits(DZ2[(pk + 4) * DZS + j0]), tf32_bits(DZ2[(pk + 4) * DZS + j0 + 8])};
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int ic = 8 * (4 * (warp & 1) + t) + gid;
+        for (int t = 0; t < MT_N64; ++t) {
+          const int ic = 8 * (MT_N64 * wn + t) + gid;
           const uint32_t ob = kk * 32 + tig * 4 + cm_col(ic);
           const uint32_t bv[2] = {__float_as_uint(H1h[ob]), __float_as_uint(H1h[ob + 16])};
           mma_tf32_16x8x8(acc2[t], av, bv);
@@ -393,8 +445,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         const uint32_t av[4] = {tf32_bits(DZ1[dz1_idx(pk, i0)]), tf32_bits(DZ1[dz1_idx(pk, i0 + 8)]),
                                 tf32_bits(DZ1[dz1_idx(pk + 4, i0)]), tf32_bits(DZ1[dz1_idx(pk + 4, i0 + 8)])};
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int kc = 8 * (8 * (warp & 1) + t) + gid;
+        for (int t = 0; t < MT_N128; ++t) {
+          const int kc = 8 * (MT_N128 * wn + t) + gid;
           const uint32_t ob = kk * 32 + tig * 4 + cm_col(kc);
           const uint32_t bv[2] = {__float_as_uint(Fh[ob]), __float_as_uint(Fh[ob + 16])};
           mma_tf32_16x8x8(acc1[t], av, bv);
@@ -403,11 +455,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     }
     __syncthreads();
     // ---- backward 3: gF = dz1 W1 (M=64 p, N=128 k, K=64 i), 3xTF32, into the F region ----
-    {
-      const int mt = warp >> 1, nt0 = 8 * (warp & 1);
-      float d[8][4];
+    if (!(a.skip & 2)) {
+      const int nt0 = MT_N128 * wn;
+      float d[MT_N128][4];
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
+      for (int t = 0; t < MT_N128; ++t)
 #pragma unroll
         for (int e = 0; e < 4; ++e) d[t][e] = 0.f;
 #pragma unroll 1
@@ -418,7 +470,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
         uint32_t ah[4], al[4];
         split_frag(av, 4, ah, al);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < MT_N128; ++t) {
           const int kc = 8 * (nt0 + t) + gid;  // feature column
           const uint32_t o0 = kk * 32 + tig * 4 + cm_col(kc), o1 = o0 + 16;
           const uint32_t bh[2] = {__float_as_uint(W1h[o0]), __float_as_uint(W1h[o1])};
@@ -428,47 +480,24 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
           mma_tf32_16x8x8(d[t], al, bh);
         }
       }
-      __syncthreads();  // all warps done reading F (dW1) before gF overwrites it
+      __syncthreads();  // all warps done reading dz1 / h1 before gF overwrites them
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < MT_N128; ++t) {
         const int c0 = 8 * (nt0 + t) + 2 * tig, pr = 16 * mt + gid;
         *reinterpret_cast<float2*>(GF + pr * GFS + c0) = make_float2(d[t][0], d[t][1]);
         *reinterpret_cast<float2*>(GF + (pr + 8) * GFS + c0) = make_float2(d[t][2], d[t][3]);
       }
     }
     __syncthreads();
-    // ---- scatter (cell terms from the TMEM cache written by this thread during encode) ----
-#pragma unroll 1
-    for (int jq = 0; jq < 4; ++jq) {
-      uint32_t cache[16];
-      umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = 2 * jq + (u >> 1), h = u & 1;
-        const int m = warp + 8 * j, p = lane + 32 * h;
-        const int vbase = int(cache[4 * u]);
-        const bool valid = vbase >= 0 && p < cnt;
-        float2 g = make_float2(0.f, 0.f);
-        if (valid) g = *reinterpret_cast<const float2*>(GF + p * GFS + 2 * m);
-        if (a.aggregate)
-          scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
-                                  __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-        else if (valid)
-          scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
-                             __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-      }
-    }
-    umma::fence_before_sync();
-    __syncthreads();
+    prev_cnt = cnt;
   }
 
   // ---- flush per-CTA partials: [dW1 (64x128) | dW2 (64x64) | dW3 (64)] ----
   float* dst = a.part_dw + int64_t(blockIdx.x) * (HID * FE + HID * HID + HID);
   {
-    const int mt = warp >> 1;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int c0 = 8 * (8 * (warp & 1) + t) + 2 * tig, r0 = 16 * mt + gid;
+    for (int t = 0; t < MT_N128; ++t) {
+      const int c0 = 8 * (MT_N128 * wn + t) + 2 * tig, r0 = 16 * mt + gid;
       dst[r0 * FE + c0] = acc1[t][0];
       dst[r0 * FE + c0 + 1] = acc1[t][1];
       dst[(r0 + 8) * FE + c0] = acc1[t][2];
@@ -476,8 +505,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     }
     float* d2 = dst + HID * FE;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int c0 = 8 * (4 * (warp & 1) + t) + 2 * tig, r0 = 16 * mt + gid;
+    for (int t = 0; t < MT_N64; ++t) {
+      const int c0 = 8 * (MT_N64 * wn + t) + 2 * tig, r0 = 16 * mt + gid;
       d2[r0 * HID + c0] = acc2[t][0];
       d2[r0 * HID + c0 + 1] = acc2[t][1];
       d2[(r0 + 8) * HID + c0] = acc2[t][2];
@@ -486,7 +515,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   }
   if (lane < 16) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) atomicAdd(&sDW3[ep_col0 + c], dw3_acc[c]);
+    for (int c = 0; c < EPC; ++c) atomicAdd(&sDW3[ep_col0 + c], dw3_acc[c]);
   }
   const double bl = block_sum(loss, red);  // contains __syncthreads
   if (tid < HID) dst[HID * FE + HID * HID + tid] = sDW3[tid];
@@ -514,7 +543,9 @@ int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, c
     attr = true;
   }
   const char* ea = getenv("APMG_SCATTER_AGG");
-  tc::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1};
+  const char* es = getenv("APMG_TC_SKIP");
+  tc::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1,
+             es ? atoi(es) : 0};
   APMG_LAUNCH("recon_fwd_bwd_tc", tc::k_recon_tc, grid, tc::NT, tc::SMEM_BYTES, st, a);
   return APMG_OK;
 }

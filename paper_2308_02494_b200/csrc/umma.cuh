@@ -5,14 +5,15 @@
 // Operand layout ("CM layout"): a row-major matrix X[R][C] of 32-bit values is
 // stored as 8x16-byte core matrices,
 //     offset(r, c) = (c/4)*SC + (r/8)*128 + (r%8)*16 + (c%4)*4,   SC = R*16,
-// which is simultaneously
-//   * the canonical K-major SWIZZLE_NONE layout with rows = M/N and cols = K
-//     (SBO = 128 B between 8-row groups, LBO = SC between the two 16-B K chunks
-//     of one K=8 tf32 MMA), and
-//   * the canonical MN-major SWIZZLE_NONE layout with cols = M/N and rows = K
-//     (SBO = SC between 4-element MN chunks, LBO = 128 B between 8-row K groups).
-// So one buffer feeds both X and X^T products without a transpose, and a
-// thread owning a row writes whole 16-byte chunks (conflict-free).
+// the canonical K-major SWIZZLE_NONE layout with rows = M/N and cols = K (SBO = 128 B
+// between 8-row groups, LBO = SC between the two 16-B K chunks of one K=8 tf32 MMA);
+// a thread owning a row writes whole 16-byte chunks (conflict-free).
+//
+// kind::tf32 reads MN-major operands only in the 128B-with-32B-atom swizzle (CUTLASS:
+// "SW128_32B is the only available smem layout" for MN-major tf32), whose physical
+// arrangement differs from every K-major one, so a matrix needed in both orientations
+// takes two copies.  The fused recon kernel instead keeps the transposed weights in
+// tensor memory and issues those products with the A operand from TMEM (mma_tf32_ts).
 #pragma once
 
 #include <stdint.h>
@@ -43,7 +44,8 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int R, int kk) {
   return smem_desc(base + uint32_t(kk) * 2u * uint32_t(R * 16), uint32_t(R * 16), 128u);
 }
-// Descriptor of a CM-layout buffer used MN-major (cols = M or N, rows = K) at K-step kk.
+// SWIZZLE_NONE MN-major descriptor of a CM-layout buffer (cols = M or N, rows = K) at K-step
+// kk.  Kept for the self-test only: kind::tf32 does not accept this layout (see above).
 __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int R, int kk) {
   return smem_desc(base + uint32_t(kk) * 128u, 128u, uint32_t(R * 16));
 }
@@ -77,6 +79,16 @@ __device__ __forceinline__ void mma_tf32_mask(uint32_t d_tmem, uint64_t a_desc, 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+
+// A operand from tensor memory (M=128: row m in lane m, K elements in consecutive columns).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void commit(uint64_t* mbar) {

@@ -5,6 +5,7 @@
 //   cfg 1: D[64][N]  = A[64][K]  . B[K][N]     (A K-major, B MN-major)  e.g. gF = dz1 W1
 //   cfg 2: D[128][N] = A[K][128]^T . B[K][N]   (A MN-major, B MN-major) e.g. dW1^T = F^T dz1
 //   cfg 3: D[128][N] = A[128][K] . B[N][K]^T   (M = 128, K-major both)
+//   cfg 4: D[128][N] = A[128][K] . B[N][K]^T   (A from tensor memory, cols 128.., B K-major)
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -19,7 +20,8 @@ __global__ void __launch_bounds__(128) k_umma_debug(int cfg_flags, int K, int N,
   const int M = (cfg >= 2) ? 128 : 64;
   // A rows x cols and B rows x cols as stored (row-major inputs)
   const int a_rows = (cfg == 2) ? K : M, a_cols = (cfg == 2) ? 128 : K;
-  const int b_rows = (cfg == 0 || cfg == 3) ? N : K, b_cols = (cfg == 0 || cfg == 3) ? K : N;
+  const bool bk = (cfg == 0 || cfg == 3 || cfg == 4);
+  const int b_rows = bk ? N : K, b_cols = bk ? K : N;
   float *Ah, *Al, *Bh, *Bl;
   if (cfg_flags & 256) {  // B first in smem
     Bh = reinterpret_cast<float*>(sm);
@@ -92,7 +94,38 @@ __global__ void __launch_bounds__(128) k_umma_debug(int cfg_flags, int K, int N,
     __syncthreads();
     umma::fence_after_sync();
   }
-  if (threadIdx.x == 0) {
+  if (cfg == 4) {  // A (hi at column 128, lo at 128 + K) into tensor memory, lane = row
+    const int w = threadIdx.x >> 5, t = threadIdx.x & 31, row = 32 * w + t;
+    for (int c0 = 0; c0 < K; c0 += 16) {
+      uint32_t rh[16], rl[16];
+      for (int i = 0; i < 16; ++i) {
+        const float x = (c0 + i < K) ? A[row * K + c0 + i] : 0.f;
+        float hi, lo;
+        umma::split_tf32(x, hi, lo);
+        rh[i] = __float_as_uint(split3 ? hi : x);
+        rl[i] = __float_as_uint(lo);
+      }
+      umma::tmem_st16(umma::taddr(tb, 32 * w, 128 + c0), rh);
+      umma::tmem_st16(umma::taddr(tb, 32 * w, 128 + K + c0), rl);
+    }
+    umma::tmem_st_wait();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+  }
+  if (threadIdx.x == 0 && cfg == 4) {
+    const uint32_t idesc = umma::idesc_tf32(128, N, false, false);
+    const uint32_t sBh = umma::smem_u32(Bh), sBl = umma::smem_u32(Bl);
+    for (int kk = 0; kk < K / 8; ++kk) {
+      const uint64_t bh = umma::desc_kmajor(sBh, b_rows, kk), bl = umma::desc_kmajor(sBl, b_rows, kk);
+      umma::mma_tf32_ts(tb, umma::taddr(tb, 0, 128 + 8 * kk), bh, idesc, kk > 0);
+      if (split3) {
+        umma::mma_tf32_ts(tb, umma::taddr(tb, 0, 128 + 8 * kk), bl, idesc, 1);
+        umma::mma_tf32_ts(tb, umma::taddr(tb, 0, 128 + K + 8 * kk), bh, idesc, 1);
+      }
+    }
+    umma::commit(&mbar);
+  } else if (threadIdx.x == 0) {
     const bool a_mn = (cfg == 2), b_mn = (cfg == 1 || cfg == 2);
     const uint32_t idesc = umma::idesc_tf32(M, N, a_mn, b_mn);
     const uint32_t sAh = umma::smem_u32(Ah), sAl = umma::smem_u32(Al), sBh = umma::smem_u32(Bh),
@@ -173,7 +206,8 @@ using namespace apmg;
 
 extern "C" int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
                                     float* D, void* stream) {
-  APMG_ARG_CHECK((cfg & 15) <= 3, "cfg 0..3 (+16: print descriptors)");
+  APMG_ARG_CHECK((cfg & 15) <= 4, "cfg 0..4 (+16: print descriptors)");
+  APMG_ARG_CHECK((cfg & 15) != 4 || (K <= 64 && N <= 128), "cfg 4: K <= 64, N <= 128");
   APMG_ARG_CHECK(K % 8 == 0 && K >= 8 && K <= 128, "K multiple of 8 in [8,128]");
   APMG_ARG_CHECK(N % 16 == 0 && N >= 16 && N <= 256, "N multiple of 16 in [16,256]");
   const int M = (cfg & 15) >= 2 ? 128 : 64;
