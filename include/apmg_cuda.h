@@ -194,6 +194,9 @@ int apmg_train_destroy(apmg_train_state* s);
 /* ---- tcgen05 self-test (one CTA, one GEMM; see csrc/umma_debug.cu) ---------- */
 int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
                          float* D, void* stream);
+/* clock64 stamps [16 tiles][12 phases] of CTA 0 of the last fused recon launch run with
+ * APMG_TC_SKIP & 64 (profiling aid, tools/tc_phases.py) */
+int apmg_debug_tc_phases(long long* out);
 
 /* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
 /* plateau_step (trainer.py:118-138) on the same code the device controller runs.

@@ -10,7 +10,7 @@
 //   head/loss     epilogue: out = h2 w3 * span + vmin, residual, sq error, g = dL/dout,
 //                 mask[p][j] = [z2 > 0] (exact 0/1 operand)
 //   dz1^T = V mask^T       tcgen05.mma with A = V = (w3 o W2)^T resident in TMEM (M=128,
-//                 rows 64..127 zero), B = mask; dz1[p][i] = g[p] dz1^T[i][p] [h1 > 0].
+//                 rows 64..127 repeat 0..63), B = mask; dz1[p][i] = g[p] dz1^T[i][p] [h1 > 0].
 //                 (g_z2 = g w3^T [z2>0] is rank one per row, optim.py:143-145, so its
 //                 product with W2 needs only the split of V: 2 products, exact mask.)
 //   gF^T = W1^T dz1^T      tcgen05.mma, A = W1^T resident in TMEM (M=128), B = dz1 hi/lo
@@ -68,6 +68,13 @@ static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t TC_ACC_A = 0, TC_ACC_B = 64, TC_CACHE = 128, TC_VH = 256, TC_VL = 320, TC_W1TH = 384,
                    TC_W1TL = 448;
+
+// per-phase clock stamps of CTA 0 / thread 0 for the first 16 tiles (APMG_TC_SKIP & 64)
+__device__ long long g_tc_stamp[16][12];
+#define TC_STAMP(k)                                                                 \
+  do {                                                                              \
+    if ((a.skip & 64) && blockIdx.x == 0 && tid == 0 && it < 16) g_tc_stamp[it][k] = clock64(); \
+  } while (0)
 
 __device__ __forceinline__ float* fptr(unsigned char* sm, uint32_t off) { return reinterpret_cast<float*>(sm + off); }
 
@@ -214,8 +221,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   // the WQ warps sharing a lane quarter use disjoint 8*GPW-column slices of the cache
   const uint32_t tmem_cache = tmem + TC_CACHE + 8 * GPW * wq + lane_base;
 
-  // ---- resident A operands in TMEM (row = lane): V[i][j] = w3[j] W2[j][i] (rows >= 64
-  // zero) and W1^T[k][i] = W1[i][k]; warps 0-3 write V, warps 4-7 write W1^T ----
+  // ---- resident A operands in TMEM (row = lane): V[i][j] = w3[j] W2[j][i] (rows 64-127
+  // repeat rows 0-63, so all four lane quarters receive dz1^T) and W1^T[k][i] = W1[i][k];
+  // warps 0-3 write V, warps 4-7 write W1^T ----
   if (warp < 8) {
     const int r = 32 * quarter + lane;
     const bool is_v = warp < 4;
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
       for (int c = 0; c < 16; ++c) {
         float x;
         if (is_v)
-          x = r < HID ? __fmul_rn(md.w3[c0 + c], md.w2[(c0 + c) * HID + r]) : 0.f;
+          x = __fmul_rn(md.w3[c0 + c], md.w2[(c0 + c) * HID + (r & (HID - 1))]);
         else
           x = md.w1[(c0 + c) * FE + r];
         float hi, lo;
@@ -278,6 +286,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     const int cnt = int(min64(P, a.n - tile * P));
     const float* cX = sX + (it & 1) * 3 * P;
     const float* cT = sT + (it & 1) * P;
+    TC_STAMP(0);
     // ---- encode: lane -> point, warp -> grid; cell terms cached in TMEM for the scatter ----
     {
       const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
@@ -315,6 +324,21 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
           *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
         }
         umma::tmem_st16(tmem_cache + 16 * jq, cache);
+        if (jq == 0) {
+          // features k < 64 (grids 0-31) are complete: start z1 on them while the rest encode
+          umma::fence_async_smem();
+          __syncthreads();
+          if (tid == 0) {
+            umma::fence_after_sync();
+            for (int kk = 0; kk < FE / 16; ++kk) {
+              const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
+              const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
+              umma::mma_tf32(TZ1, fh, wh, idesc64, kk > 0);
+              umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
+              umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
+            }
+          }
+        }
       }
       umma::tmem_st_wait();
     }
@@ -325,12 +349,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();  // F complete; every warp's scatter of the previous tile has read gF
     umma::fence_after_sync();
-    // ---- z1 = F W1^T (3xTF32) ----
+    TC_STAMP(1);
+    // ---- z1 = F W1^T (3xTF32), second half of K ----
     if (tid == 0) {
-      for (int kk = 0; kk < FE / 8; ++kk) {
+      for (int kk = FE / 16; kk < FE / 8; ++kk) {
         const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
         const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
-        umma::mma_tf32(TZ1, fh, wh, idesc64, kk > 0);
+        umma::mma_tf32(TZ1, fh, wh, idesc64, 1);
         umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
         umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
       }
@@ -339,6 +364,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
+    TC_STAMP(2);
     // ---- epilogue 1: h1 = relu(z1) -> h1 hi/lo; sign bitmap for the dz1 mask ----
     {
       float v[EPC];
@@ -364,6 +390,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC_STAMP(3);
     // ---- z2 = h1 W2^T (3xTF32) ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 8; ++kk) {
@@ -378,6 +405,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
+    TC_STAMP(4);
     // ---- epilogue 2: h2, head, loss, g, mask, dW3 ----
     float h2v[EPC];
     umma::tmem_ld16(TZ2 + lane_base + ep_col0, h2v);
@@ -416,6 +444,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC_STAMP(5);
     // ---- dz1^T[i][p] = sum_j V[i][j] mask[p][j]  (A = V from TMEM, 2 products) ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 8; ++kk) {
@@ -454,26 +483,46 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();  // dW2 has consumed h1 before dz1 overwrites it
     umma::fence_after_sync();
-    // ---- dz1 epilogue: rows i = lanes of quarters 0-1, 16 points per warp ----
-    if (quarter < 2) {
-      const int i = 32 * quarter + lane;
-      float v[16];
-      umma::tmem_ld16(TZ1 + lane_base + 16 * wq, v);
-      const uint32_t bits = sM1[i * 4 + wq];
+    TC_STAMP(6);
+    // ---- dz1 epilogue: row i = lane of quarter q (rows repeat every 64), 8 points per warp;
+    // an 8x8 register transpose within lane octets turns the column-per-lane values into
+    // row-per-lane float4 stores (CM rows are 16-byte chunks) ----
+    {
+      const int i = 32 * (quarter & 1) + lane, p0 = 8 * (wq + 4 * (quarter >> 1));
+      float v[8];
+      umma::tmem_ld8(TZ1 + lane_base + p0, v);
+      const uint32_t bits = uint32_t(sM1[i * 4 + (p0 >> 4)]) >> (p0 & 15);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int p = 16 * wq + c;
-        const float d = ((bits >> c) & 1u) ? __fmul_rn(sG[p], v[c]) : 0.f;
-        float hi, lo;
-        umma::split_tf32(d, hi, lo);
-        DZ1h[cm64(p, i)] = hi;
-        DZ1l[cm64(p, i)] = lo;
+      for (int c = 0; c < 8; ++c) v[c] = ((bits >> c) & 1u) ? __fmul_rn(sG[p0 + c], v[c]) : 0.f;
+      const int l = lane & 7;
+#pragma unroll
+      for (int st = 4; st >= 1; st >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c & st) continue;
+          const bool up = l & st;
+          const float r = __shfl_xor_sync(0xffffffffu, up ? v[c] : v[c ^ st], st);
+          if (up)
+            v[c] = r;
+          else
+            v[c ^ st] = r;
+        }
       }
+      // now v[c] = dz1[p0 + l][ib + c]
+      const int p = p0 + l, ib = 32 * (quarter & 1) + (lane & ~7);
+      float hi[8], lo[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) umma::split_tf32(v[c], hi[c], lo[c]);
+      *reinterpret_cast<float4*>(DZ1h + cm64(p, ib)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(DZ1h + cm64(p, ib + 4)) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      *reinterpret_cast<float4*>(DZ1l + cm64(p, ib)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<float4*>(DZ1l + cm64(p, ib + 4)) = make_float4(lo[4], lo[5], lo[6], lo[7]);
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC_STAMP(7);
     // ---- gF^T[k][p] = sum_i W1^T[k][i] dz1[p][i]  (A = W1^T from TMEM, 3xTF32) ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 8; ++kk) {
@@ -507,6 +556,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();  // dW1 and the gF^T product have consumed dz1 before gF overwrites it
     umma::fence_after_sync();
+    TC_STAMP(8);
     // ---- gF epilogue: row k = lane of each quarter, 16 points per warp -> gF[p][k] ----
     {
       const int k = 32 * quarter + lane;
@@ -517,8 +567,10 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     }
     umma::fence_before_sync();
     __syncthreads();
+    TC_STAMP(9);
     // ---- scatter (this thread's items; the next encode follows without a barrier) ----
     scatter_tile(md, a, GF, tmem_cache, cnt, warp, lane);
+    TC_STAMP(10);
   }
 
   // ---- flush per-CTA partials: [dW1 (64x128) | dW2 (64x64) | dW3 (64)] ----
@@ -555,6 +607,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
 }
 
 }  // namespace tc
+
+extern "C" int apmg_debug_tc_phases(long long* out) {
+  APMG_CUDA_TRY(cudaMemcpyFromSymbol(out, tc::g_tc_stamp, sizeof(tc::g_tc_stamp)));
+  return APMG_OK;
+}
 
 bool recon_tc_eligible(const ModelDev<float>& md) {
   const char* e = getenv("APMG_MLP");  // APMG_MLP=simt forces the SIMT kernel (A/B tests)
