@@ -236,12 +236,14 @@ __global__ void k_dens_finalize(T* __restrict__ tf, int M, int p, const double* 
                                 T* __restrict__ dtf, T* __restrict__ adam_m, T* __restrict__ adam_v,
                                 const TrainCtl* ctl) {
   if (ctl && (ctl->skip || !ctl->density_on)) return;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
+  __shared__ double red[32];
+  const int m = blockIdx.x;  // one block per grid: threads stride over the chunk partials
   double acc[13];
   for (int e = 0; e < 13; ++e) acc[e] = 0.0;
-  for (int c = 0; c < chunks; ++c)
+  for (int c = threadIdx.x; c < chunks; c += blockDim.x)
     for (int e = 0; e < 13; ++e) acc[e] += part[(int64_t(c) * M + m) * 13 + e];
+  for (int e = 0; e < 13; ++e) acc[e] = block_sum(acc[e], red);
+  if (threadIdx.x != 0) return;
   double a[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) a[3 * r + c] = double(tf[16 * m + 4 * r + c]);
@@ -409,8 +411,74 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_grad32(const float* __res
   }
 }
 
+// Chunked variant: a block stages kGradCH points (x, d_rho) in shared memory once and its
+// warps sweep them for every grid (the per-grid launch above re-reads x and d_rho M times);
+// per-(chunk, grid) lane sums are combined in f64 per block.
+constexpr int kGradCH = 4096;
+constexpr int kGradMaxM = 128;
+__global__ void __launch_bounds__(kDensThreads) k_dens_grad32c(const float* __restrict__ tf, int M, int p,
+                                                               const float* __restrict__ x, int64_t n,
+                                                               const float* __restrict__ drho, int ch,
+                                                               double* __restrict__ part, const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  extern __shared__ float4 sP[];                                   // [ch <= kGradCH] (x0, x1, x2, d_rho)
+  double* s_acc = reinterpret_cast<double*>(sP + kGradCH);         // [M][13]
+  float* s_tf = reinterpret_cast<float*>(s_acc + 13 * M);          // [M][13]
+  stage_transforms32(tf, M, s_tf);
+  for (int e = threadIdx.x; e < 13 * M; e += blockDim.x) s_acc[e] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int64_t c0 = int64_t(blockIdx.x) * ch; c0 < n; c0 += int64_t(gridDim.x) * ch) {
+    const int cnt = int(min64(ch, n - c0));
+    __syncthreads();  // previous chunk consumed, transforms / accumulators staged
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int64_t g = c0 + i;
+      sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], drho[g]);
+    }
+    __syncthreads();
+    for (int m = warp; m < M; m += nw) {
+      float a[13];
+#pragma unroll
+      for (int e = 0; e < 13; ++e) a[e] = s_tf[13 * m + e];
+      float acc[13];
+#pragma unroll
+      for (int e = 0; e < 13; ++e) acc[e] = 0.f;
+      for (int i = lane; i < cnt; i += 32) {
+        const float4 q = sP[i];
+        float b, l[3], lp[3];
+        bump32(a, q.x, q.y, q.z, p, b, l, lp);
+        if (!(b > 0.f)) continue;
+        const float w = q.w * b;
+        const float sc = a[12] * w;
+        acc[0] += w;
+        const float sl0 = sc * lp[0], sl1 = sc * lp[1], sl2 = sc * lp[2];
+        acc[1] = fmaf(sl0, q.x, acc[1]);
+        acc[2] = fmaf(sl0, q.y, acc[2]);
+        acc[3] = fmaf(sl0, q.z, acc[3]);
+        acc[4] = fmaf(sl1, q.x, acc[4]);
+        acc[5] = fmaf(sl1, q.y, acc[5]);
+        acc[6] = fmaf(sl1, q.z, acc[6]);
+        acc[7] = fmaf(sl2, q.x, acc[7]);
+        acc[8] = fmaf(sl2, q.y, acc[8]);
+        acc[9] = fmaf(sl2, q.z, acc[9]);
+        acc[10] += sl0;
+        acc[11] += sl1;
+        acc[12] += sl2;
+      }
+#pragma unroll
+      for (int e = 0; e < 13; ++e) {
+        const double v = warp_sum(double(acc[e]));
+        if (lane == 0) s_acc[13 * m + e] += v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 13 * M; e += blockDim.x) part[int64_t(blockIdx.x) * 13 * M + e] = s_acc[e];
+}
+
+static size_t grad32c_smem(int M) { return sizeof(float4) * kGradCH + size_t(13) * M * (sizeof(double) + sizeof(float)); }
+
 struct DensPlan {
-  int nb1, chunks;
+  int nb1, chunks, nbg;  // nbg: blocks of the chunked f32 gradient kernel
 };
 
 static DensPlan dens_plan(int M, int64_t n) {
@@ -418,6 +486,7 @@ static DensPlan dens_plan(int M, int64_t n) {
   d.nb1 = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kDensThreads), int64_t(num_sms()) * 8)));
   const int64_t want = std::max<int64_t>(1, (int64_t(num_sms()) * 8 + M - 1) / M);
   d.chunks = int(std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(n, kDensThreads))));
+  d.nbg = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 512), int64_t(num_sms()) * 2)));
   return d;
 }
 
@@ -428,8 +497,8 @@ size_t density_ws_bytes(int M, int64_t n) {
   c.take<double>(n);                          // d_s
   c.take<double>(2 * size_t(d.nb1));          // part1
   c.take<double>(2 * size_t(d.nb1));          // part2
-  c.take<double>(size_t(d.chunks) * M * 13);  // part3
-  c.take<double>(8);                          // stats
+  c.take<double>(size_t(std::max(d.chunks, d.nbg)) * M * 13);  // part3
+  c.take<double>(8);                                             // stats
   return c.used + 256;
 }
 
@@ -444,12 +513,13 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
   double* d_s = c.take<double>(n);
   double* part1 = c.take<double>(2 * size_t(d.nb1));
   double* part2 = c.take<double>(2 * size_t(d.nb1));
-  double* part3 = c.take<double>(size_t(d.chunks) * M * 13);
+  double* part3 = c.take<double>(size_t(std::max(d.chunks, d.nbg)) * M * 13);
   double* stats = c.take<double>(8);
   if (!c.ok()) {
     set_error("density workspace too small: need %zu, have %zu", c.used, wsb);
     return APMG_E_WORKSPACE;
   }
+  int parts = d.chunks;  // gradient partials per grid handed to the finalize kernel
   const char* e64 = getenv("APMG_DENSITY64");  // force the all-fp64 per-pair path (A/B tests)
   const bool fast32 = (sizeof(T) == 4) && !(e64 && e64[0] == '1');
   if constexpr (sizeof(T) == 4) {
@@ -475,15 +545,24 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
     if (fast32) {
       float* drho = reinterpret_cast<float*>(rho);  // rho is dead once the target pass has run
       APMG_LAUNCH("density_drho", k_dens_drho32, d.nb1, kDensThreads, 0, st, d_s, n, stats, drho, ctl);
-      APMG_LAUNCH("density_grad", k_dens_grad32, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, drho, part3,
-                  ctl);
+      if (M <= kGradMaxM) {
+        const size_t sm = grad32c_smem(M);
+        APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_grad32c, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        const int ch = int(std::min<int64_t>(kGradCH, ceil_div(n, d.nbg)));  // one balanced chunk per block
+        APMG_LAUNCH("density_grad", k_dens_grad32c, d.nbg, kDensThreads, sm, st, tf, M, p, x, n, drho, ch, part3,
+                    ctl);
+        parts = d.nbg;
+      } else {
+        APMG_LAUNCH("density_grad", k_dens_grad32, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, drho,
+                    part3, ctl);
+      }
     }
   }
   if (!fast32)
     APMG_LAUNCH("density_grad", k_dens_grad<T>, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, d_s, stats,
                 part3, ctl);
-  APMG_LAUNCH("density_finalize", k_dens_finalize<T>, int(ceil_div(M, 64)), 64, 0, st, tf, M, p, part3, d.chunks,
-              dtf, adam_m, adam_v, ctl);
+  APMG_LAUNCH("density_finalize", k_dens_finalize<T>, M, 128, 0, st, tf, M, p, part3, parts, dtf, adam_m, adam_v,
+              ctl);
   if (rho_total) APMG_CUDA_TRY(cudaMemcpyAsync(rho_total, stats, sizeof(double), cudaMemcpyDeviceToDevice, st));
   return APMG_OK;
 }

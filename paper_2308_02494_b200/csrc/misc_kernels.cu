@@ -128,66 +128,114 @@ __device__ __forceinline__ uint32_t bucket_of(float x, float y, float z) {
   return spread3(bx) | (spread3(by) << 1) | (spread3(bz) << 2);
 }
 
-template <typename T>
-__global__ void k_bucket_count(const T* __restrict__ coords, int64_t n, uint32_t* __restrict__ key,
-                               int32_t* __restrict__ counts, const TrainCtl* ctl) {
+// Batch generation for the sorted path, split so that the volume is sampled in bucket
+// order (coherent reads) instead of Philox order (one random DRAM sector per corner):
+//   k_batch_keys      Philox coords (f64, trainer.py:189) + bucket key + bucket counts
+//   k_bucket_scan     exclusive scan of the counts
+//   k_bucket_scatter  f64 coords to their bucket slot
+//   k_sample_sorted   fp64 trilinear targets (volume.py:147-199) + float32 coords, in place
+// Targets are sampled at the f64 coordinates exactly as in k_train_batch.
+__global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
+                             uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl) {
   if (ctl->skip) return;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t k = bucket_of(float(coords[3 * i]), float(coords[3 * i + 1]), float(coords[3 * i + 2]));
+  const uint64_t base = 3ull * uint64_t(batch) * uint64_t(ctl->it);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < batch; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t j = base + 3ull * uint64_t(i);
+    const uint64_t b0 = j >> 2, b1 = (j + 2) >> 2;
+    uint64_t wa[4], wb[4];
+    philox_block(b0 + 1, k0, k1, wa);
+    if (b1 != b0) philox_block(b1 + 1, k0, k1, wb);
+    double c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t jj = j + a;
+      const uint64_t word = ((jj >> 2) == b0) ? wa[jj & 3] : wb[jj & 3];
+      c[a] = add_rn(-1.0, mul_rn(2.0, word_to_double(word)));
+      c64[3 * i + a] = c[a];
+    }
+    const uint32_t k = bucket_of(__double2float_rn(c[0]), __double2float_rn(c[1]), __double2float_rn(c[2]));
     key[i] = k;
     atomicAdd(&counts[k], 1);
   }
 }
 
-// in-place exclusive scan of kBuckets counts (one block of 1024 threads)
+// in-place exclusive scan of kBuckets counts: one block of 1024 threads, 32 consecutive
+// counts per thread (vector loads), warp shuffles + one smem pass across warps
 constexpr int kBuckets = 32768;
-__global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl) {
+__global__ void __launch_bounds__(1024) k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl) {
   if (ctl->skip) return;
-  __shared__ int32_t part[1024];
-  const int t = threadIdx.x, per = kBuckets / 1024;
-  int32_t local[kBuckets / 1024];
+  __shared__ int32_t wsum[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int4* c4 = reinterpret_cast<int4*>(counts) + 8 * t;
+  int4 v[8];
   int32_t s = 0;
 #pragma unroll
-  for (int i = 0; i < per; ++i) {
-    local[i] = counts[t * per + i];
-    s += local[i];
+  for (int q = 0; q < 8; ++q) {
+    v[q] = c4[q];
+    s += v[q].x + v[q].y + v[q].z + v[q].w;
   }
-  part[t] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const int32_t v = t >= off ? part[t - off] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
-  }
-  int32_t run = part[t] - s;
+  int32_t inc = s;  // inclusive scan of the per-thread sums within the warp
 #pragma unroll
-  for (int i = 0; i < per; ++i) {
-    counts[t * per + i] = run;
-    run += local[i];
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = wsum[lane], wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += y;
+    }
+    wsum[lane] = wi - w;  // exclusive prefix of the warp totals
+  }
+  __syncthreads();
+  int32_t run = wsum[warp] + inc - s;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    int4 o;
+    o.x = run;
+    run += v[q].x;
+    o.y = run;
+    run += v[q].y;
+    o.z = run;
+    run += v[q].z;
+    o.w = run;
+    run += v[q].w;
+    c4[q] = o;
+  }
+}
+
+__global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
+                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pos = atomicAdd(&cursor[key[i]], 1);
+    c64_out[3 * pos] = c64[3 * i];
+    c64_out[3 * pos + 1] = c64[3 * i + 1];
+    c64_out[3 * pos + 2] = c64[3 * i + 2];
   }
 }
 
 template <typename T>
-__global__ void k_bucket_scatter(const T* __restrict__ coords, const T* __restrict__ targets,
-                                 const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cursor,
-                                 T* __restrict__ coords_out, T* __restrict__ targets_out, const TrainCtl* ctl) {
+__global__ void k_sample_sorted(const double* __restrict__ c64, int64_t n, const float* __restrict__ vol, int w,
+                                int h, int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl) {
   if (ctl->skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t pos = atomicAdd(&cursor[key[i]], 1);
-    coords_out[3 * pos] = coords[3 * i];
-    coords_out[3 * pos + 1] = coords[3 * i + 1];
-    coords_out[3 * pos + 2] = coords[3 * i + 2];
-    targets_out[pos] = targets[i];
+    const double c0 = c64[3 * i], c1 = c64[3 * i + 1], c2 = c64[3 * i + 2];
+    targets[i] = T(__double2float_rn(sample_trilinear(vol, w, h, d, c0, c1, c2)));
+    coords[3 * i] = T(__double2float_rn(c0));
+    coords[3 * i + 1] = T(__double2float_rn(c1));
+    coords[3 * i + 2] = T(__double2float_rn(c2));
   }
 }
 
-template __global__ void k_bucket_count<float>(const float*, int64_t, uint32_t*, int32_t*, const TrainCtl*);
-template __global__ void k_bucket_count<double>(const double*, int64_t, uint32_t*, int32_t*, const TrainCtl*);
-template __global__ void k_bucket_scatter<float>(const float*, const float*, const uint32_t*, int64_t, int32_t*, float*,
-                                                 float*, const TrainCtl*);
-template __global__ void k_bucket_scatter<double>(const double*, const double*, const uint32_t*, int64_t, int32_t*,
-                                                  double*, double*, const TrainCtl*);
+template __global__ void k_sample_sorted<float>(const double*, int64_t, const float*, int, int, int, float*, float*,
+                                                const TrainCtl*);
+template __global__ void k_sample_sorted<double>(const double*, int64_t, const float*, int, int, int, double*, double*,
+                                                 const TrainCtl*);
 
 // ---- synth_volume (volume.py:283-296)
 __global__ void k_synth(int w, int h, int d, int nb, const double* __restrict__ ex, const double* __restrict__ ey,

@@ -30,14 +30,14 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
                              const TrainCtl* ctl);
 int elementwise_grid(int64_t n, int per_sm);
 constexpr int kBuckets = 32768;
-template <typename T>
-__global__ void k_bucket_count(const T* __restrict__ coords, int64_t n, uint32_t* __restrict__ key,
-                               int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
+                             uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
 __global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
+                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out, const TrainCtl* ctl);
 template <typename T>
-__global__ void k_bucket_scatter(const T* __restrict__ coords, const T* __restrict__ targets,
-                                 const uint32_t* __restrict__ key, int64_t n, int32_t* __restrict__ cursor,
-                                 T* __restrict__ coords_out, T* __restrict__ targets_out, const TrainCtl* ctl);
+__global__ void k_sample_sorted(const double* __restrict__ c64, int64_t n, const float* __restrict__ vol, int w,
+                                int h, int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
 
 static bool sort_enabled() {
   const char* e = getenv("APMG_SORT");
@@ -122,7 +122,8 @@ struct apmg_train_state {
   TrainCtl* ctl;
   double *l_rec, *l_dens, *lr, *dens_hist, *plat_ring, *bias;
   int64_t* trig;
-  void *grad, *am, *av, *tm, *tv, *coords, *targets, *sq, *coords_raw, *targets_raw;
+  void *grad, *am, *av, *tm, *tv, *coords, *targets, *sq;
+  double *c64_raw, *c64_sorted;  // sorted path: f64 batch coordinates before / after bucketing
   uint32_t* key;
   int32_t* counts;
   bool sort;
@@ -169,8 +170,8 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   char* coords = cv.take<char>(es * 3 * B);
   char* targets = cv.take<char>(es * B);
   char* sq = cv.take<char>(es * B);
-  char* coords_raw = cv.take<char>(es * 3 * B);
-  char* targets_raw = cv.take<char>(es * B);
+  double* c64_raw = cv.take<double>(3 * B);
+  double* c64_sorted = cv.take<double>(3 * B);
   uint32_t* key = cv.take<uint32_t>(B);
   int32_t* counts = cv.take<int32_t>(kBuckets);
   const size_t rws = m->dtype == APMG_F32 ? recon_ws_bytes<float>(F, B) : recon_ws_bytes<double>(F, B);
@@ -194,8 +195,8 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
     s->coords = coords;
     s->targets = targets;
     s->sq = sq;
-    s->coords_raw = coords_raw;
-    s->targets_raw = targets_raw;
+    s->c64_raw = c64_raw;
+    s->c64_sorted = c64_sorted;
     s->key = key;
     s->counts = counts;
     s->recon_ws = recon_ws;
@@ -285,15 +286,14 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
   if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
-    APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
-                s->w, s->h, s->d, static_cast<T*>(s->coords_raw), static_cast<T*>(s->targets_raw), s->ctl);
     APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
-    APMG_LAUNCH("bucket_count", k_bucket_count<T>, elementwise_grid(B, 8), 256, 0, st,
-                static_cast<const T*>(s->coords_raw), B, s->key, s->counts, s->ctl);
+    APMG_LAUNCH("batch_keys", k_batch_keys, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->c64_raw, s->key,
+                s->counts, s->ctl);
     APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
-    APMG_LAUNCH("bucket_scatter", k_bucket_scatter<T>, elementwise_grid(B, 8), 256, 0, st,
-                static_cast<const T*>(s->coords_raw), static_cast<const T*>(s->targets_raw), s->key, B, s->counts,
-                static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+    APMG_LAUNCH("bucket_scatter", k_bucket_scatter, elementwise_grid(B, 8), 256, 0, st, s->c64_raw, s->key, B,
+                s->counts, s->c64_sorted, s->ctl);
+    APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B, s->volume,
+                s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
   } else {
     APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
                 s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
