@@ -148,10 +148,30 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
     tf = ROOT / "profiles" / "traffic_r01.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(kernel)
-    return {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
-            "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
-            "note": "algorithmic encoder gather + scatter bytes (4096+4096+20 B/pt); served from L2"}
+    out = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
+           "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+           "note": "algorithmic encoder gather + scatter bytes (4096+4096+20 B/pt); served from L2"}
+    pf = ROOT / "profiles" / "peaks_b200.json"
+    if kernel.startswith("recon_fwd_bwd") and pf.exists():
+        # encoder fwd is bound by L2 gather bandwidth, encoder bwd by L2 RED
+        # throughput -- algorithmic units of one launch against the probes of tools/peaks.py
+        pk2 = json.loads(pf.read_text())
+        g_ach = BATCH * ENC_BYTES / t / 1e9
+        r_ach = BATCH * (SCAT_BYTES // 8) / t / 1e9
+        fl_ach = BATCH * 74112 / t / 1e12
+        out["l2"] = {
+            "gather": {"achieved": g_ach, "peak": pk2["l2_gather_float2_GBps_16MiB"], "unit": "GB/s",
+                       "frac": g_ach / pk2["l2_gather_float2_GBps_16MiB"]},
+            "red": {"achieved": r_ach, "peak": pk2["l2_red_float2_Gops_16MiB"], "unit": "G float2 RED/s",
+                    "frac": r_ach / pk2["l2_red_float2_Gops_16MiB"]},
+            "mlp_tensor": {"achieved": fl_ach, "peak": pk2["tf32_tcgen05_tflops"], "unit": "TFLOP/s (tf32)",
+                           "frac": fl_ach / pk2["tf32_tcgen05_tflops"]},
+            "peak_source": "profiles/peaks_b200.json (tools/peaks.py: random float2 over a 16 MiB table)",
+            "note": "gather and RED are the un-aggregated algorithmic counts (512 corner loads and 512 "
+                    "float2 REDs per point); warp coherence and aggregation let the kernel exceed the "
+                    "random-access RED probe"}
+    return out
 
 
 def kernel_table():

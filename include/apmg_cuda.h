@@ -197,6 +197,11 @@ int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, cons
 /* clock64 stamps [16 tiles][12 phases] of CTA 0 of the last fused recon launch run with
  * APMG_TC_SKIP & 64 (profiling aid, tools/tc_phases.py) */
 int apmg_debug_tc_phases(long long* out);
+/* roofline peak probes (csrc/peaks.cu, tools/peaks.py): kind 0 L2 float2 gather, 1 L2 float2
+ * RED, 2 FP32 FFMA, 3 FP64 DFMA, 4 tcgen05 kind::tf32, 5 warp shuffles; `table` is a device
+ * buffer of table_bytes (power of two) for kinds 0-1 (a sink otherwise); *work receives the
+ * work unit count of the launch (bytes, REDs, FLOP, FLOP, FLOP, shuffles). */
+int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, int32_t iters, double* work, void* stream);
 
 /* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
 /* plateau_step (trainer.py:118-138) on the same code the device controller runs.

@@ -15,7 +15,7 @@ from paper_2308_02494_b200 import _lib as L  # noqa: E402
 def run(cfg, K, N, split3, seed=0):
     rng = np.random.default_rng(seed + 17 * cfg + K + N)
     M = 128 if cfg >= 2 else 64
-    if cfg == 0 or cfg == 3:
+    if cfg in (0, 3, 4):
         A = rng.normal(size=(M, K)).astype(np.float32)
         B = rng.normal(size=(N, K)).astype(np.float32)
         ref = A.astype(np.float64) @ B.astype(np.float64).T
@@ -35,10 +35,13 @@ def run(cfg, K, N, split3, seed=0):
     return float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
 
 
-# K-major A and B (the layouts the fused recon kernel issues): M=64 and M=128 accumulators.
-# (MN-major kind::tf32 operands -- configs 1 and 2 of the self-test -- read back as zeros on
-# this driver/toolkit, so the kernel never issues them; its backward uses register-fragment MMAs.)
-@pytest.mark.parametrize("cfg,K,N", [(0, 128, 64), (0, 64, 64), (3, 64, 64), (3, 64, 128), (0, 8, 16)])
+# K-major A and B from smem (the forward products of the fused recon kernel): M=64 and M=128
+# accumulators; cfg 4: A from tensor memory (the kernel's dz1^T and gF^T products, whose
+# transposed weights stay resident in TMEM).  MN-major kind::tf32 smem operands need the
+# 128B/32B-atom swizzle (configs 1-2 of the self-test use SWIZZLE_NONE and read zeros), so the
+# kernel does not issue them.
+@pytest.mark.parametrize("cfg,K,N", [(0, 128, 64), (0, 64, 64), (3, 64, 64), (3, 64, 128), (0, 8, 16),
+                                     (4, 64, 64), (4, 64, 128), (4, 8, 16)])
 def test_umma_gemm_configs(cfg, K, N):
     e3 = run(cfg, K, N, 1)
     e1 = run(cfg, K, N, 0)
