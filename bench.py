@@ -104,8 +104,15 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # APMG_BENCH_BACKEND=gloo: functional check of the N>1 path with several ranks on one
+        # GPU (the ranks never wait on each other's kernels; not a scaling measurement)
+        backend = os.environ.get("APMG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         return dist, rank, world, local
     return None, 0, 1, local
 
@@ -306,7 +313,7 @@ def main():
     ran, _ = sess.status()
     assert ran == W + K, f"expected {W + K} iterations, ran {ran}"
     if dist:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     log = sess.log()
@@ -334,7 +341,8 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if dist:
-            tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            tt = torch.tensor([dt], device="cuda" if dist.get_backend() == "nccl" else "cpu",
+                              dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         params_b = 4 * m2.parameter_count()

@@ -253,6 +253,26 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
   if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
     int rel = __popc(peers & ((1u << lane) - 1u));
     unsigned rem = peers & (0xfffffffeu << lane);
+    {
+      // round 1 pulls the partner's raw point (5 shuffles) and forms its 16 products here,
+      // instead of shuffling the 16 products (the shuffle crossbar is the scatter's bound)
+      const int next = __ffs(rem);
+      const int src = next ? next - 1 : lane;
+      const float pg0 = __shfl_sync(0xffffffffu, g0, src), pg1 = __shfl_sync(0xffffffffu, g1, src);
+      const float px = __shfl_sync(0xffffffffu, fx, src), py = __shfl_sync(0xffffffffu, fy, src),
+                  pz = __shfl_sync(0xffffffffu, fz, src);
+      if (next) {
+        const float wx[2] = {1.f - px, px}, wy[2] = {1.f - py, py}, wz[2] = {1.f - pz, pz};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float w = wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]);
+          v[2 * c] += pg0 * w;
+          v[2 * c + 1] += pg1 * w;
+        }
+      }
+      rem &= __ballot_sync(0xffffffffu, !(rel & 1));
+      rel >>= 1;
+    }
     while (__any_sync(0xffffffffu, rem != 0u)) {
       const int next = __ffs(rem);
       const int src = next ? next - 1 : lane;

@@ -10,6 +10,8 @@
 //   kind 4  tcgen05.mma kind::tf32, M=128 N=256 K=8, back to back from one thread per CTA
 //           (operands in smem, contents irrelevant); work = FLOP
 //   kind 5  warp shuffles (__shfl_sync, 32-bit); work = shuffle instructions (per warp)
+//   kind 6  shared-memory float atomic adds (red.shared.add.f32), 32 distinct banks per
+//           instruction; work = atomic instructions (per warp)
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -120,6 +122,19 @@ __global__ void __launch_bounds__(256) k_peak_shfl(int iters, float* __restrict_
   if (v[0] + v[1] + v[2] + v[3] == 12345.678f) sink[0] = v[0];
 }
 
+__global__ void __launch_bounds__(256) k_peak_atoms(int iters, float* __restrict__ sink) {
+  __shared__ float s[8][32 * 17];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = lane; e < 32 * 17; e += 32) s[warp][e] = 0.f;
+  __syncwarp();
+  float* base = s[warp];
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int u = 0; u < 16; ++u) atomicAdd(base + lane * 17 + ((u + it) & 15), 1.f);
+  __syncwarp();
+  if (base[lane] == 12345.f) sink[0] = base[lane];
+}
+
 }  // namespace apmg
 
 using namespace apmg;
@@ -163,6 +178,10 @@ extern "C" int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, i
     case 5:
       APMG_LAUNCH("peak_shfl", k_peak_shfl, sms * 8, 256, 0, st, iters, sink);
       *work = double(sms) * 8 * 8 * iters * 4;  // warp-level shuffle instructions
+      return APMG_OK;
+    case 6:
+      APMG_LAUNCH("peak_atoms", k_peak_atoms, sms * 8, 256, 0, st, iters, sink);
+      *work = double(sms) * 8 * 8 * iters * 16;  // warp-level atomic instructions
       return APMG_OK;
     default:
       set_error("unknown probe kind %d", kind);

@@ -49,6 +49,8 @@ def main():
     out["tf32_tcgen05_tflops"] = probe(4, sink, 64, 4096)[0] / 1e12
     out["shfl_Ginstr_per_s"] = probe(5, sink, 64, 4096)[0] / 1e9
     out["shfl_per_clk_per_sm"] = out["shfl_Ginstr_per_s"] * 1e9 / (out["sms"] * 1.965e9)
+    out["atoms_f32_Ginstr_per_s"] = probe(6, sink, 64, 1024)[0] / 1e9
+    out["atoms_per_clk_per_sm"] = out["atoms_f32_Ginstr_per_s"] * 1e9 / (out["sms"] * 1.965e9)
     out["how"] = ("csrc/peaks.cu via tools/peaks.py: best of 5 launches, CUDA events; gather/RED = random float2 "
                   "over a power-of-two table (16/64 MiB stay in the 126 MB L2), 8 independent accesses in flight "
                   "per thread, 148x8 CTAs of 256; FP32/FP64 = 8 independent FMA chains per thread; tf32 = "
