@@ -1,0 +1,281 @@
+// Tensor-core lattice sweep (trainer.py:226-247 psnr, decomposition.py:294-304 brick boxes)
+// for the flagship shape (float32, 64 grids x 2 channels -> 128 features, 64 hidden).
+//
+// One persistent CTA (16 warps) per SM, 64-voxel tiles, software-pipelined so that both
+// tensor-core products hide behind CUDA-core work:
+//     encode(t) | z1(t) issue | head(t-1) [z2(t-1) wait] | z1 wait, epilogue 1 -> h1 |
+//     z2(t) issue | encode(t+1) ...
+//   encode   lattice voxel -> f32 coordinate (the reference casts the f64 lattice
+//            coordinate to float32 before predicting) -> per-grid f32 cell math -> features
+//            split into TF32 hi/lo in the CM layout
+//   z1, z2   tcgen05.mma kind::tf32, M=64, N=64, 3 products (3xTF32)
+//   head     out = relu(z2) w3 * span + vmin; reconstruct-to-HBM and / or f64 SSE vs truth
+// Features use f32 lerps (<= 1 ulp from the bit-exact f64-lerp encoder of k_forward);
+// outputs agree with the reference forward to ~1e-6 relative (forward gate 1e-4).
+#include "fwd_args.cuh"
+#include "umma.cuh"
+
+namespace apmg {
+namespace itc {
+
+constexpr int P = 64;
+constexpr int NW = 16;
+constexpr int NT = 32 * NW;
+constexpr int WQ = NW / 4;
+constexpr int EPC = 64 / WQ;
+constexpr int GPW = 64 / NW;
+constexpr int FE = 128;
+constexpr int HID = 64;
+
+constexpr uint32_t OFF_W1H = 0;
+constexpr uint32_t OFF_W1L = OFF_W1H + 64 * 128 * 4;
+constexpr uint32_t OFF_W2H = OFF_W1L + 64 * 128 * 4;
+constexpr uint32_t OFF_W2L = OFF_W2H + 64 * 64 * 4;
+constexpr uint32_t OFF_FH = OFF_W2L + 64 * 64 * 4;
+constexpr uint32_t OFF_FL = OFF_FH + P * FE * 4;
+constexpr uint32_t OFF_H1H = OFF_FL + P * FE * 4;
+constexpr uint32_t OFF_H1L = OFF_H1H + P * HID * 4;
+constexpr uint32_t OFF_X = OFF_H1L + P * HID * 4;     // [P][3]
+constexpr uint32_t OFF_HEAD = OFF_X + P * 3 * 4;      // [WQ][P]
+constexpr uint32_t OFF_RED = OFF_HEAD + WQ * P * 4;   // [32] doubles
+constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // 2 mbarriers
+constexpr uint32_t OFF_TM = OFF_BAR + 16;
+constexpr uint32_t OFF_TF = OFF_TM + 16;              // [64][12]
+constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;     // [64]
+constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+constexpr uint32_t TMEM_COLS = 128;  // z1 | z2
+
+__device__ __forceinline__ float* fptr(unsigned char* sm, uint32_t off) { return reinterpret_cast<float*>(sm + off); }
+__device__ __forceinline__ uint32_t cm64(int r, int c) { return umma::cm_offset(r, c, 64) >> 2; }
+
+// lattice voxel index of point i of the box (x fastest)
+__device__ __forceinline__ int64_t voxel_of(const FwdArgs<float>& a, int64_t i) {
+  const int64_t plane = int64_t(a.bw) * a.bh;
+  const int z = int(i / plane);
+  const int64_t r = i - z * plane;
+  const int y = int(r / a.bw);
+  const int x = int(r - int64_t(y) * a.bw);
+  return (int64_t(a.bz0 + z) * a.LH + (a.by0 + y)) * a.LW + (a.bx0 + x);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const ModelDev<float>& md = a.md;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int quarter = warp & 3, wq = warp >> 2;
+  float* W1h = fptr(sm, OFF_W1H);
+  float* W1l = fptr(sm, OFF_W1L);
+  float* W2h = fptr(sm, OFF_W2H);
+  float* W2l = fptr(sm, OFF_W2L);
+  float* Fh = fptr(sm, OFF_FH);
+  float* Fl = fptr(sm, OFF_FL);
+  float* H1h = fptr(sm, OFF_H1H);
+  float* H1l = fptr(sm, OFF_H1L);
+  float* sX = fptr(sm, OFF_X);
+  float* sHead = fptr(sm, OFF_HEAD);
+  double* red = reinterpret_cast<double*>(sm + OFF_RED);
+  uint64_t* bar1 = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint64_t* bar2 = bar1 + 1;
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
+  float* sTF = fptr(sm, OFF_TF);
+  float* sW3 = fptr(sm, OFF_W3);
+
+  for (int e = tid; e < 64 * 128; e += NT) {
+    float hi, lo;
+    umma::split_tf32(md.w1[e], hi, lo);
+    const uint32_t o = cm64(e >> 7, e & 127);
+    W1h[o] = hi;
+    W1l[o] = lo;
+  }
+  for (int e = tid; e < 64 * 64; e += NT) {
+    float hi, lo;
+    umma::split_tf32(md.w2[e], hi, lo);
+    const uint32_t o = cm64(e >> 6, e & 63);
+    W2h[o] = hi;
+    W2l[o] = lo;
+  }
+  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  if (tid < HID) sW3[tid] = md.w3[tid];
+  if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
+  if (tid == 0) {
+    umma::mbar_init(bar1, 1);
+    umma::mbar_init(bar2, 1);
+    umma::fence_mbar_init();
+  }
+  umma::fence_async_smem();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_slot;
+  const uint32_t TZ1 = tmem, TZ2 = tmem + 64;
+  const uint32_t lane_base = uint32_t(32 * quarter) << 16;
+  const uint32_t sW1h = umma::smem_u32(W1h), sW1l = umma::smem_u32(W1l), sW2h = umma::smem_u32(W2h),
+                 sW2l = umma::smem_u32(W2l), sFh = umma::smem_u32(Fh), sFl = umma::smem_u32(Fl),
+                 sH1h = umma::smem_u32(H1h), sH1l = umma::smem_u32(H1l);
+  const uint32_t idesc64 = umma::idesc_tf32(64, 64, false, false);
+  const int ep_row = 16 * quarter + lane;
+  const int ep_col0 = EPC * wq;
+  uint32_t ph1 = 0, ph2 = 0;
+  double sse = 0.0;
+
+  // head of a finished tile: relu(z2) . w3 -> output / SSE (waits for its z2)
+  auto head = [&](int64_t tile) {
+    umma::mbar_wait(bar2, ph2);
+    ph2 ^= 1;
+    umma::fence_after_sync();
+    float v[EPC];
+    umma::tmem_ld16(TZ2 + lane_base + ep_col0, v);
+    if (lane < 16) {
+      float part = 0.f;
+#pragma unroll
+      for (int c = 0; c < EPC; ++c) part = fmaf(fmaxf(v[c], 0.f), sW3[ep_col0 + c], part);
+      sHead[wq * P + ep_row] = part;
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (tid < P) {
+      const int64_t i = tile * P + tid;
+      if (i < a.n) {
+        float raw = sHead[tid];
+#pragma unroll
+        for (int q = 1; q < WQ; ++q) raw += sHead[q * P + tid];
+        const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
+        const int64_t vx = voxel_of(a, i);
+        if (a.recon) a.recon[vx] = y;
+        if (a.truth) {
+          const double d = sub_rn(double(y), double(a.truth[vx]));
+          sse += d * d;
+        }
+      }
+    }
+  };
+
+  const int64_t tiles = ceil_div(a.n, P);
+  int64_t prev = -1;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    // coordinates of this tile (sX was last read by the previous encode, before its barrier)
+    if (tid < P) {
+      float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+      const int64_t i = tile * P + tid;
+      if (i < a.n) fwd_point(a, i, x0, x1, x2);
+      sX[3 * tid] = x0;
+      sX[3 * tid + 1] = x1;
+      sX[3 * tid + 2] = x2;
+    }
+    __syncthreads();
+    // ---- encode (overlaps the z2 product of the previous tile) ----
+    {
+      const float xa[2][3] = {{sX[3 * lane], sX[3 * lane + 1], sX[3 * lane + 2]},
+                              {sX[3 * (lane + 32)], sX[3 * (lane + 32) + 1], sX[3 * (lane + 32) + 2]}};
+#pragma unroll 1
+      for (int jq = 0; jq < GPW / 2; ++jq) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 2 * jq + (u >> 1), h = u & 1;
+          const int m = warp + NW * j, p = lane + 32 * h;
+          const float* tf = sTF + 12 * m;
+          const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
+          const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
+          const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
+          const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
+          int ix, iy, iz;
+          double fxd, fyd, fzd;
+          axis_term(l0, md.W, ix, fxd);
+          axis_term(l1, md.H, iy, fyd);
+          axis_term(l2, md.D, iz, fzd);
+          float f0 = 0.f, f1 = 0.f;
+          if (inside)
+            interp_pair_f32(md.grid, md.W, md.H * md.W, ((m * md.D + iz) * md.H + iy) * md.W + ix, float(fxd),
+                            float(fyd), float(fzd), f0, f1);
+          float hi0, lo0, hi1, lo1;
+          umma::split_tf32(f0, hi0, lo0);
+          umma::split_tf32(f1, hi1, lo1);
+          const uint32_t o = cm64(p, 2 * m);
+          *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
+          *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
+        }
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (tid == 0) {
+      for (int kk = 0; kk < FE / 8; ++kk) {
+        const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
+        const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
+        umma::mma_tf32(TZ1, fh, wh, idesc64, kk > 0);
+        umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
+        umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
+      }
+      umma::commit(bar1);
+    }
+    // ---- head of the previous tile (overlaps z1 of this one) ----
+    if (prev >= 0) head(prev);
+    // ---- epilogue 1 ----
+    umma::mbar_wait(bar1, ph1);
+    ph1 ^= 1;
+    umma::fence_after_sync();
+    {
+      float v[EPC];
+      umma::tmem_ld16(TZ1 + lane_base + ep_col0, v);
+      if (lane < 16) {
+#pragma unroll
+        for (int c4 = 0; c4 < EPC; c4 += 4) {
+          float hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) umma::split_tf32(fmaxf(v[c4 + e], 0.f), hi[e], lo[e]);
+          const uint32_t o = cm64(ep_row, ep_col0 + c4);
+          *reinterpret_cast<float4*>(H1h + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(H1l + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (tid == 0) {
+      for (int kk = 0; kk < HID / 8; ++kk) {
+        const uint64_t hh = umma::desc_kmajor(sH1h, 64, kk), hl = umma::desc_kmajor(sH1l, 64, kk);
+        const uint64_t wh = umma::desc_kmajor(sW2h, 64, kk), wl = umma::desc_kmajor(sW2l, 64, kk);
+        umma::mma_tf32(TZ2, hh, wh, idesc64, kk > 0);
+        umma::mma_tf32(TZ2, hh, wl, idesc64, 1);
+        umma::mma_tf32(TZ2, hl, wh, idesc64, 1);
+      }
+      umma::commit(bar2);
+    }
+    prev = tile;
+  }
+  if (prev >= 0) head(prev);
+  if (a.truth) {
+    const double s = block_sum(sse, red);
+    if (tid == 0) atomicAdd(a.sse, s);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+}  // namespace itc
+
+bool infer_tc_eligible(const FwdArgs<float>& a) {
+  const char* e = getenv("APMG_MLP");  // APMG_MLP=simt keeps the SIMT sweep (A/B tests)
+  return !(e && e[0] == 's') && a.mode == kFwdLattice && a.md.F == 128 && a.md.C == 2 && a.md.M == 64;
+}
+
+int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    APMG_CUDA_TRY(cudaFuncSetAttribute(itc::k_infer_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(itc::SMEM_BYTES)));
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(a.n, itc::P);
+  const int grid = int(min64(tiles, int64_t(num_sms())));
+  APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NT, itc::SMEM_BYTES, st, a);
+  return APMG_OK;
+}
+
+}  // namespace apmg

@@ -275,6 +275,45 @@ def test_decomposed_forward_and_psnr(golden):
     assert P.psnr(field, vol) == pytest.approx(float(g["dec_psnr"]), abs=1e-5)
 
 
+@pytest.mark.parametrize("box,affine", [(None, False), ((3, 40, 0, 36, 5, 30), False), ((0, 50, 2, 20, 1, 9), True)])
+def test_lattice_sweep_tensor_core_vs_reference(box, affine, monkeypatch):
+    """The flagship shape sweeps lattices on the tensor-core kernel (f32 lerps, 3xTF32 MLP);
+    its reconstruction matches the reference forward on the same f32 lattice coordinates
+    within the forward gate, and its f64 SSE matches the bit-exact SIMT sweep."""
+    rng = np.random.default_rng(11)
+    m = PM.init_model(PM.ModelConfig(64, 2, (32, 32, 32)), seed=3, vmin=-0.5, vmax=2.0)
+    m.grids[:] = (m.grids + rng.normal(scale=0.2, size=m.grids.shape)).astype(np.float32)
+    dims = (53, 41, 37)
+    truth = rng.uniform(-0.5, 2.0, size=dims[::-1]).astype(np.float32)
+    truth_d = L.to_device(truth)
+    sc, of = ((0.9, 1.1, 0.8), (0.05, -0.1, 0.02)) if affine else (None, None)
+    w, h, d = dims
+    bx = box if box is not None else (0, w - 1, 0, h - 1, 0, d - 1)
+    out = {}
+    for mode in ("tc", "simt"):
+        if mode == "simt":
+            monkeypatch.setenv("APMG_MLP", "simt")
+        recon = L.zeros(dims[::-1], np.float32)
+        sse = L.zeros((1,), np.float64)
+        PT.lattice_sse_model(m.device(), truth_d, dims, box=box, scale=sc, offset=of, sse=sse, recon=recon)
+        out[mode] = (L.to_host(recon), float(sse.item()))
+    monkeypatch.delenv("APMG_MLP", raising=False)
+    sl = (slice(bx[4], bx[5] + 1), slice(bx[2], bx[3] + 1), slice(bx[0], bx[1] + 1))
+    ax = [np.array([-1.0 + 2.0 * i / (n - 1) for i in range(n)]) for n in dims]
+    zz, yy, xx = np.meshgrid(ax[2][sl[0]], ax[1][sl[1]], ax[0][sl[2]], indexing="ij")
+    # psnr casts the lattice to float32 first; DecomposedField then applies its f64 affine
+    pts = np.stack([xx.ravel(), yy.ravel(), zz.ravel()], axis=1).astype(np.float32)
+    if affine:
+        pts = (pts.astype(np.float64) * np.array(sc) + np.array(of)).astype(np.float32)
+    ref = O.forward(oracle_from(m), pts)
+    assert forward_rel(out["tc"][0][sl].ravel(), ref, m.vmax - m.vmin) <= 1e-4
+    assert forward_rel(out["simt"][0][sl].ravel(), ref, m.vmax - m.vmin) <= 1e-4
+    assert out["tc"][1] == pytest.approx(out["simt"][1], rel=1e-5)
+    outside = np.ones(dims[::-1], bool)
+    outside[sl] = False
+    assert not out["tc"][0][outside].any()
+
+
 def test_psnr_matches_reference(golden):
     g = golden("psnr")
     m = model_from(g, "m_")
