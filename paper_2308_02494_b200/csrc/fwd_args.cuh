@@ -21,6 +21,7 @@ struct FwdArgs {
   // lattice sweep (kFwdLattice): voxel box of a (W,H,D) lattice
   int LW, LH, LD, bx0, by0, bz0, bw, bh;
   int affine;
+  int stamps;           // k_infer_tc phase stamps (profiling aid)
   double sc0, sc1, sc2, of0, of1, of2;
   const float* truth;   // [LD][LH][LW] or null
   float* recon;         // [LD][LH][LW] or null
