@@ -353,8 +353,9 @@ def main():
                        f"volume + parameter upload, device loop, parameter + log download"}
 
     infer = None
-    if not args.no_inference and world == 1:
-        infer = bench_inference(model_from_session=None)
+    if not args.no_inference:
+        infer = bench_inference(model_from_session=None) if world == 1 else \
+            bench_decomposed_inference(rank, world, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -404,6 +405,65 @@ def bench_inference(model_from_session=None, dims=(1024, 1024, 1024)):
     vox = dims[0] * dims[1] * dims[2]
     return {"metric": "inference voxels/sec", "value": vox / (ms * 1e-3), "ms_per_sweep": ms,
             "config": "C3: 1024^3 lattice, one 64x32^3x2 model, fused forward + fp64 SSE vs truth"}
+
+
+DIMS_C5 = (2048, 2048, 2048)
+
+
+def bench_decomposed_inference(rank, world, dist, dims=DIMS_C5, counts=(4, 4, 4)):
+    """C5: a 2048^3 lattice decomposed into 4x4x4 bricks (ghost 1); rank r sweeps bricks
+    flat % world == r (each through its own model and brick affine) in PSNR + reconstruct
+    mode against a synthetic truth it generates for its own boxes; SSE all-reduced.
+    value = all voxels / max-over-ranks sweep time (untrained brick models: throughput only)."""
+    import torch
+    from paper_2308_02494_b200 import _lib as L
+    from paper_2308_02494_b200 import model as PM
+    from paper_2308_02494_b200 import volume as PV
+    from paper_2308_02494_b200.decomposition import DecomposedField, DecompositionManifest, plan_partition
+    plan = plan_partition(dims, *counts, ghost=1)
+    nb = plan.brick_count
+    mine = [b for b in range(nb) if b % world == rank]
+    models = [PM.init_model(PM.ModelConfig(M, CH, RES), seed=(0 ^ b) & 0x7FFFFFFF) if b in mine else None
+              for b in range(nb)]
+    field = DecomposedField(DecompositionManifest(plan=plan, volume_header=PV.VolumeHeader(dims=dims), bricks=[]),
+                            models)
+    boxes = field.brick_boxes(dims)
+    blobs = [PV.BlobSpec(c, s, a) for c, s, a in BLOBS]
+    truth, recon = {}, {}
+    for b in mine:
+        x0, x1, y0, y1, z0, z1 = boxes[b]
+        ext = PV.Extent(lo=(x0, y0, z0), hi=(x1, y1, z1))
+        truth[b] = PV.synth_volume_device(dims, blobs, extent=ext)
+        recon[b] = torch.empty_like(truth[b])
+    field.device_models()
+    sse = L.zeros((1,), np.float64)
+    field.lattice_sse_local(mine, truth, recon, sse)  # warm-up
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sse.zero_()
+    e0.record()
+    field.lattice_sse_local(mine, truth, recon, sse)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        total = sse.to(dev)
+        dist.all_reduce(total)  # PSNR statistic over all bricks
+        sse_all = float(total.item())
+    else:
+        sse_all = float(sse.item())
+    vox = dims[0] * dims[1] * dims[2]
+    return {"metric": "inference voxels/sec", "value": vox / (ms * 1e-3), "ms_per_sweep": ms,
+            "config": f"C5: {dims[0]}^3 lattice, {counts[0]}x{counts[1]}x{counts[2]} bricks (ghost 1), "
+                      f"{len(mine)} bricks on rank {rank} of {world}, PSNR + reconstruct mode, "
+                      f"box-local truth/recon per rank, SSE all-reduced",
+            "sse": sse_all}
 
 
 if __name__ == "__main__":

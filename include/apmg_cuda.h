@@ -153,6 +153,12 @@ int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi
 int apmg_lattice_sweep(const apmg_model* m, int32_t w, int32_t h, int32_t d, const int32_t box[6],
                        const double* scale, const double* offset, const float* truth, double* sse,
                        float* recon, void* stream);
+/* Same sweep with box-local truth / recon: dense [bd][bh][bw] arrays of the box only
+ * (per-rank brick inference over a volume no single GPU holds; decomposition.py:294-304
+ * with trainer.py:226-247 per brick). */
+int apmg_brick_sweep(const apmg_model* m, int32_t w, int32_t h, int32_t d, const int32_t box[6],
+                     const double* scale, const double* offset, const float* truth_box, double* sse,
+                     float* recon_box, void* stream);
 
 /* ---- device-resident training loop (trainer.py:160-223) -------------------- */
 typedef struct apmg_train_config {

@@ -76,6 +76,8 @@ SIGNATURES = {
                                           _P, _P, _SZ, _P]),
     "apmg_lattice_sweep": (C.c_int, [_MP, _I32, _I32, _I32, C.POINTER(_I32), C.POINTER(_D), C.POINTER(_D), _P,
                                      _P, _P, _P]),
+    "apmg_brick_sweep": (C.c_int, [_MP, _I32, _I32, _I32, C.POINTER(_I32), C.POINTER(_D), C.POINTER(_D), _P,
+                                   _P, _P, _P]),
     "apmg_main_layout": (C.c_int, [_MP, C.POINTER(_I64)]),
     "apmg_train_workspace_bytes": (_SZ, [_MP, C.POINTER(ApmgTrainConfigC)]),
     "apmg_train_create": (C.c_int, [C.POINTER(_P), _MP, _P, _P, _P, _I32, _I32, _I32,

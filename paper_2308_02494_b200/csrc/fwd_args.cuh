@@ -22,6 +22,7 @@ struct FwdArgs {
   int LW, LH, LD, bx0, by0, bz0, bw, bh;
   int affine;
   int stamps;           // k_infer_tc phase stamps (profiling aid)
+  int box_local;        // truth / recon are dense [bd][bh][bw] arrays of the box (brick sweeps)
   double sc0, sc1, sc2, of0, of1, of2;
   const float* truth;   // [LD][LH][LW] or null
   float* recon;         // [LD][LH][LW] or null
@@ -31,6 +32,13 @@ struct FwdArgs {
   const int32_t* index; // [n] point ids of this brick
   float* gout;          // out[index[i]]
 };
+
+// truth / recon element of box voxel (x, y, z): global lattice index, or box-local
+template <typename T>
+__device__ __forceinline__ int64_t lattice_elem(const FwdArgs<T>& a, int x, int y, int z) {
+  if (a.box_local) return (int64_t(z) * a.bh + y) * a.bw + x;
+  return (int64_t(a.bz0 + z) * a.LH + (a.by0 + y)) * a.LW + (a.bx0 + x);
+}
 
 // f64 lattice coordinate of vertex i of n (axis_coords, volume.py:161-165)
 __device__ __forceinline__ double lattice_coord(int i, int n) {

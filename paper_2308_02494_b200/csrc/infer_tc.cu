@@ -83,14 +83,14 @@ __global__ void k_axis_tables(FwdArgs<float> a, float* __restrict__ tab) {
   }
 }
 
-// lattice voxel index of point i of the box (x fastest)
+// truth / recon element of point i of the box (x fastest)
 __device__ __forceinline__ int64_t voxel_of(const FwdArgs<float>& a, int64_t i) {
   const int64_t plane = int64_t(a.bw) * a.bh;
   const int z = int(i / plane);
   const int64_t r = i - z * plane;
   const int y = int(r / a.bw);
   const int x = int(r - int64_t(y) * a.bw);
-  return (int64_t(a.bz0 + z) * a.LH + (a.by0 + y)) * a.LW + (a.bx0 + x);
+  return lattice_elem(a, x, y, z);
 }
 
 __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const float* __restrict__ tab) {
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
       x0 = tx[x];
       x1 = ty[y];
       x2 = tz[z];
-      if (a.truth) tv = a.truth[(int64_t(a.bz0 + z) * a.LH + (a.by0 + y)) * a.LW + (a.bx0 + x)];
+      if (a.truth) tv = a.truth[lattice_elem(a, x, y, z)];
     }
     float* d = sX + (slot & 1) * 3 * P;
     d[3 * t] = x0;

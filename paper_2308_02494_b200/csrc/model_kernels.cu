@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kTileThreads) k_forward(FwdArgs<T> a) {
         const int64_t r = i - z * plane;
         const int yy = int(r / a.bw);
         const int x = int(r - int64_t(yy) * a.bw);
-        const int64_t v = (int64_t(a.bz0 + z) * a.LH + (a.by0 + yy)) * a.LW + (a.bx0 + x);
+        const int64_t v = lattice_elem(a, x, yy, z);
         if (a.recon) a.recon[v] = float(y);
         if (a.truth) {
           const double d = sub_rn(double(y), double(a.truth[v]));
@@ -522,8 +522,10 @@ extern "C" int apmg_recon_loss_grads(const apmg_model* m, const void* coords, co
 
 template <typename T>
 static int lattice_impl(const apmg_model* m, int32_t w, int32_t h, int32_t d, const int32_t* box, const double* sc,
-                        const double* of, const float* truth, double* sse, float* recon, void* stream) {
+                        const double* of, const float* truth, double* sse, float* recon, void* stream,
+                        int box_local = 0) {
   FwdArgs<T> a{};
+  a.box_local = box_local;
   a.md = make_model_dev<T>(*m);
   a.mode = kFwdLattice;
   a.LW = w;
@@ -563,6 +565,20 @@ extern "C" int apmg_lattice_sweep(const apmg_model* m, int32_t w, int32_t h, int
   APMG_ARG_CHECK(truth == nullptr || sse != nullptr, "truth given without sse accumulator");
   return m->dtype == APMG_F32 ? lattice_impl<float>(m, w, h, d, box, scale, offset, truth, sse, recon, stream)
                               : lattice_impl<double>(m, w, h, d, box, scale, offset, truth, sse, recon, stream);
+}
+
+extern "C" int apmg_brick_sweep(const apmg_model* m, int32_t w, int32_t h, int32_t d, const int32_t box[6],
+                                const double* scale, const double* offset, const float* truth_box, double* sse,
+                                float* recon_box, void* stream) {
+  int rc = check_model(m);
+  if (rc) return rc;
+  APMG_ARG_CHECK(w >= 1 && h >= 1 && d >= 1, "lattice dims must be positive");
+  APMG_ARG_CHECK(box[0] >= 0 && box[1] < w && box[2] >= 0 && box[3] < h && box[4] >= 0 && box[5] < d,
+                 "lattice box out of range");
+  APMG_ARG_CHECK(truth_box == nullptr || sse != nullptr, "truth given without sse accumulator");
+  return m->dtype == APMG_F32
+             ? lattice_impl<float>(m, w, h, d, box, scale, offset, truth_box, sse, recon_box, stream, 1)
+             : lattice_impl<double>(m, w, h, d, box, scale, offset, truth_box, sse, recon_box, stream, 1);
 }
 
 // Grouped forward over one brick's point list (used by apmg_decomposed_forward).

@@ -294,16 +294,20 @@ def _psnr_from_mse(mse: float, value_range: float) -> float:
     return float(min(10.0 * np.log10(value_range * value_range / mse), PSNR_CAP_DB))
 
 
-def lattice_sse_model(dm: DeviceModel, truth_dev, dims, box=None, scale=None, offset=None, sse=None, recon=None):
-    """Add the SSE of ``dm`` over a voxel box of the (W,H,D) lattice to the device scalar ``sse``."""
+def lattice_sse_model(dm: DeviceModel, truth_dev, dims, box=None, scale=None, offset=None, sse=None, recon=None,
+                      box_local: bool = False):
+    """Add the SSE of ``dm`` over a voxel box of the (W,H,D) lattice to the device scalar ``sse``
+    (and/or write its predictions to ``recon``).  ``box_local``: truth / recon are dense
+    arrays of the box only, as a rank holding one brick of a larger volume has them."""
     w, h, d = dims
     if box is None:
         box = (0, w - 1, 0, h - 1, 0, d - 1)
     b = (C.c_int32 * 6)(*box)
     sc = (C.c_double * 3)(*scale) if scale is not None else None
     of = (C.c_double * 3)(*offset) if offset is not None else None
-    L.check(L.lib().apmg_lattice_sweep(C.byref(dm.desc), w, h, d, b, sc, of, L.ptr(truth_dev), L.ptr(sse),
-                                       L.ptr(recon), L.stream_handle()), "lattice_sweep")
+    fn = L.lib().apmg_brick_sweep if box_local else L.lib().apmg_lattice_sweep
+    L.check(fn(C.byref(dm.desc), w, h, d, b, sc, of, L.ptr(truth_dev), L.ptr(sse), L.ptr(recon), L.stream_handle()),
+            "lattice_sweep")
 
 
 def psnr(field, volume: Volume, batch_size: int = 65536) -> float:

@@ -314,6 +314,40 @@ def test_lattice_sweep_tensor_core_vs_reference(box, affine, monkeypatch):
     assert not out["tc"][0][outside].any()
 
 
+@pytest.mark.parametrize("cfg", [(64, 2, (32, 32, 32)), (3, 2, (4, 5, 6))])
+def test_brick_local_sweep_matches_global(cfg):
+    """Per-rank brick sweeps with box-local truth / reconstruction (the C5 inference path)
+    reproduce the full-volume sweep of the decomposed field exactly, brick by brick."""
+    from paper_2308_02494_b200.decomposition import DecomposedField, DecompositionManifest, plan_partition
+    dims = (40, 33, 37)
+    plan = plan_partition(dims, 2, 2, 2, ghost=1)
+    rng = np.random.default_rng(5)
+    models = []
+    for b in range(plan.brick_count):
+        m = PM.init_model(PM.ModelConfig(cfg[0], cfg[1], cfg[2]), seed=b, vmin=-0.5, vmax=1.5)
+        m.grids[:] = (m.grids + rng.normal(scale=0.2, size=m.grids.shape)).astype(np.float32)
+        models.append(m)
+    field = DecomposedField(DecompositionManifest(plan=plan, volume_header=PV.VolumeHeader(dims=dims), bricks=[]),
+                            models)
+    truth = rng.uniform(-0.5, 1.5, size=dims[::-1]).astype(np.float32)
+    vol = P.Volume(dims=dims, data=truth)
+    recon_full = L.zeros(dims[::-1], np.float32)
+    sse_full = field.lattice_sse(vol, recon=recon_full)
+    boxes = field.brick_boxes(dims)
+    tb, rb = {}, {}
+    for b, (x0, x1, y0, y1, z0, z1) in enumerate(boxes):
+        tb[b] = L.to_device(np.ascontiguousarray(truth[z0:z1 + 1, y0:y1 + 1, x0:x1 + 1]))
+        rb[b] = L.zeros(tuple(tb[b].shape), np.float32)
+    half = [b for b in range(plan.brick_count) if b % 2 == 0]
+    rest = [b for b in range(plan.brick_count) if b % 2 == 1]
+    s0 = float(field.lattice_sse_local(half, tb, rb).item())
+    s1 = float(field.lattice_sse_local(rest, tb, rb).item())
+    assert s0 + s1 == pytest.approx(sse_full, rel=1e-12)
+    full = L.to_host(recon_full)
+    for b, (x0, x1, y0, y1, z0, z1) in enumerate(boxes):
+        assert np.array_equal(L.to_host(rb[b]), full[z0:z1 + 1, y0:y1 + 1, x0:x1 + 1])
+
+
 def test_psnr_matches_reference(golden):
     g = golden("psnr")
     m = model_from(g, "m_")
