@@ -15,6 +15,7 @@ namespace apmg {
 
 void set_error(const char* fmt, ...);
 std::atomic<uint64_t>& launch_counter();
+bool kernel_timing_on();  // per-launch CUDA events active (apmg_kernel_timing_enable)
 
 // Records a CUDA event pair around a launch when timing is enabled.
 struct LaunchScope {

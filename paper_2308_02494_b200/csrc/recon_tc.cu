@@ -115,30 +115,28 @@ struct Args {
   int skip;       // timing breakdown only (APMG_TC_SKIP): 1 scatter, 2 register MMAs, 4 gathers
 };
 
-// Grid-gradient scatter of one tile: thread (warp, lane) owns points lane, lane + 32 and
-// grids warp + NW*j, exactly the items it encoded; their cell terms come back from its TMEM
-// cache, their feature gradients from gF.
-__device__ __forceinline__ void scatter_tile(const ModelDev<float>& md, const Args& a, const float* GF,
-                                             uint32_t tmem_cache, int cnt, int warp, int lane) {
-#pragma unroll 1
-  for (int jq = 0; jq < (a.skip & 1 ? 0 : GPW / 2); ++jq) {
-    uint32_t cache[16];
-    umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
+// Grid-gradient scatter of one (2 grids x 2 points) group of a tile: thread (warp, lane)
+// owns points lane, lane + 32 and grids warp + NW*j, exactly the items it encoded; their
+// cell terms come back from its TMEM cache, their feature gradients from gF.
+__device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const Args& a, const float* GF,
+                                              uint32_t tmem_cache, int jq, int cnt, int warp, int lane) {
+  if (a.skip & 1) return;
+  uint32_t cache[16];
+  umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = 2 * jq + (u >> 1), h = u & 1;
-      const int m = warp + NW * j, p = lane + 32 * h;
-      const int vbase = int(cache[4 * u]);
-      const bool valid = vbase >= 0 && p < cnt;
-      float2 g = make_float2(0.f, 0.f);
-      if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
-      if (a.aggregate)
-        scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
-                                __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-      else if (valid)
-        scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
-                           __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-    }
+  for (int u = 0; u < 4; ++u) {
+    const int j = 2 * jq + (u >> 1), h = u & 1;
+    const int m = warp + NW * j, p = lane + 32 * h;
+    const int vbase = int(cache[4 * u]);
+    const bool valid = vbase >= 0 && p < cnt;
+    float2 g = make_float2(0.f, 0.f);
+    if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
+    if (a.aggregate)
+      scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+                              __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+    else if (valid)
+      scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
+                         __uint_as_float(cache[4 * u + 3]), g.x, g.y);
   }
 }
 
@@ -281,86 +279,87 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
   const int ep_row = 16 * quarter + lane;  // valid when lane < 16
   const int ep_col0 = EPC * wq;            // the WQ warps of a quarter split the 64 columns
 
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-    const int cnt = int(min64(P, a.n - tile * P));
-    const float* cX = sX + (it & 1) * 3 * P;
-    const float* cT = sT + (it & 1) * P;
-    TC_STAMP(0);
-    // ---- encode: lane -> point, warp -> grid; cell terms cached in TMEM for the scatter ----
-    {
-      const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
-                              {cX[3 * (lane + 32)], cX[3 * (lane + 32) + 1], cX[3 * (lane + 32) + 2]}};
-#pragma unroll 1
-      for (int jq = 0; jq < GPW / 2; ++jq) {  // groups of (2 grids x 2 points)
-        uint32_t cache[16];
+  // encode of one (2 grids x 2 points) group: lane -> point, warp -> grid; features split
+  // hi/lo into F, cell terms cached in TMEM for the scatter
+  auto encode_group = [&](const float* cX, int jq) {
+    const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
+                            {cX[3 * (lane + 32)], cX[3 * (lane + 32) + 1], cX[3 * (lane + 32) + 2]}};
+    uint32_t cache[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 2 * jq + (u >> 1), h = u & 1;
-          const int m = warp + NW * j, p = lane + 32 * h;
-          const float* tf = sTF + 12 * m;
-          const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
-          const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
-          const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
-          const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
-          int ix, iy, iz;
-          double fxd, fyd, fzd;
-          axis_term(l0, md.W, ix, fxd);
-          axis_term(l1, md.H, iy, fyd);
-          axis_term(l2, md.D, iz, fzd);
-          const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
-          const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
-          float f0 = 0.f, f1 = 0.f;
-          if (inside && !(a.skip & 4)) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
-          cache[4 * u] = uint32_t(vbase);
-          cache[4 * u + 1] = __float_as_uint(fx);
-          cache[4 * u + 2] = __float_as_uint(fy);
-          cache[4 * u + 3] = __float_as_uint(fz);
-          float hi0, lo0, hi1, lo1;
-          umma::split_tf32(f0, hi0, lo0);
-          umma::split_tf32(f1, hi1, lo1);
-          const uint32_t o = umma::cm_offset(p, 2 * m, 64) >> 2;
-          *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
-          *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
-        }
-        umma::tmem_st16(tmem_cache + 16 * jq, cache);
-        if (jq == 0) {
-          // features k < 64 (grids 0-31) are complete: start z1 on them while the rest encode
-          umma::fence_async_smem();
-          __syncthreads();
-          if (tid == 0) {
-            umma::fence_after_sync();
-            for (int kk = 0; kk < FE / 16; ++kk) {
-              const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
-              const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
-              umma::mma_tf32(TZ1, fh, wh, idesc64, kk > 0);
-              umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
-              umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
-            }
-          }
-        }
-      }
-      umma::tmem_st_wait();
+    for (int u = 0; u < 4; ++u) {
+      const int j = 2 * jq + (u >> 1), h = u & 1;
+      const int m = warp + NW * j, p = lane + 32 * h;
+      const float* tf = sTF + 12 * m;
+      const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
+      const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
+      const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
+      const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
+      int ix, iy, iz;
+      double fxd, fyd, fzd;
+      axis_term(l0, md.W, ix, fxd);
+      axis_term(l1, md.H, iy, fyd);
+      axis_term(l2, md.D, iz, fzd);
+      const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
+      const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
+      float f0 = 0.f, f1 = 0.f;
+      if (inside && !(a.skip & 4)) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+      cache[4 * u] = uint32_t(vbase);
+      cache[4 * u + 1] = __float_as_uint(fx);
+      cache[4 * u + 2] = __float_as_uint(fy);
+      cache[4 * u + 3] = __float_as_uint(fz);
+      float hi0, lo0, hi1, lo1;
+      umma::split_tf32(f0, hi0, lo0);
+      umma::split_tf32(f1, hi1, lo1);
+      const uint32_t o = umma::cm_offset(p, 2 * m, 64) >> 2;
+      *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
+      *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
     }
-    // prefetch the next tile's coordinates (that buffer was last read by tile it-1)
-    if (tile + gridDim.x < tiles)
-      load_tile(a, tile + gridDim.x, sX + ((it + 1) & 1) * 3 * P, sT + ((it + 1) & 1) * P, tid);
+    umma::tmem_st16(tmem_cache + 16 * jq, cache);
+  };
+  // z1 = F W1^T (3xTF32) over K-steps [k0, k1), committed when `last`
+  auto issue_z1 = [&](int k0, int k1, bool last) {
+    if (tid != 0) return;
+    umma::fence_after_sync();
+    for (int kk = k0; kk < k1; ++kk) {
+      const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
+      const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
+      umma::mma_tf32(TZ1, fh, wh, idesc64, kk > 0);
+      umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
+      umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
+    }
+    if (last) umma::commit(bar);
+  };
+  // Encode of tile t+1 is interleaved group by group with the scatter of tile t in every
+  // thread (scatter: shuffle-crossbar bound; encode: L2-latency bound), and the first half
+  // of z1 (features of grids 0-31) starts as soon as group 0 is written everywhere.
+  // `scatter_cnt` < 0: no scatter (first tile).
+  auto encode_tile = [&](const float* cX, int scatter_cnt, int64_t prefetch_tile, int prefetch_slot) {
+#pragma unroll 1
+    for (int jq = 0; jq < GPW / 2; ++jq) {
+      if (scatter_cnt >= 0) scatter_group(md, a, GF, tmem_cache, jq, scatter_cnt, warp, lane);
+      encode_group(cX, jq);
+      if (jq == 0) {
+        umma::fence_async_smem();
+        __syncthreads();
+        issue_z1(0, FE / 16, false);
+      }
+    }
+    umma::tmem_st_wait();
+    if (prefetch_tile < tiles)
+      load_tile(a, prefetch_tile, sX + (prefetch_slot & 1) * 3 * P, sT + (prefetch_slot & 1) * P, tid);
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();  // F complete; every warp's scatter of the previous tile has read gF
-    umma::fence_after_sync();
+    issue_z1(FE / 16, FE / 8, true);
+  };
+
+  int it = 0;
+  if (int64_t(blockIdx.x) < tiles) encode_tile(sX, -1, int64_t(blockIdx.x) + gridDim.x, 1);
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int cnt = int(min64(P, a.n - tile * P));
+    const float* cT = sT + (it & 1) * P;
+    TC_STAMP(0);
     TC_STAMP(1);
-    // ---- z1 = F W1^T (3xTF32), second half of K ----
-    if (tid == 0) {
-      for (int kk = FE / 16; kk < FE / 8; ++kk) {
-        const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
-        const uint64_t wh = umma::desc_kmajor(sW1h, 64, kk), wl = umma::desc_kmajor(sW1l, 64, kk);
-        umma::mma_tf32(TZ1, fh, wh, idesc64, 1);
-        umma::mma_tf32(TZ1, fh, wl, idesc64, 1);
-        umma::mma_tf32(TZ1, fl, wh, idesc64, 1);
-      }
-      umma::commit(bar);
-    }
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -568,8 +567,14 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     TC_STAMP(9);
-    // ---- scatter (this thread's items; the next encode follows without a barrier) ----
-    scatter_tile(md, a, GF, tmem_cache, cnt, warp, lane);
+    // ---- scatter of this tile, interleaved with the encode of the next one ----
+    const int64_t next = tile + gridDim.x;
+    if (next < tiles) {
+      encode_tile(sX + ((it + 1) & 1) * 3 * P, cnt, next + gridDim.x, it + 2);
+    } else {
+#pragma unroll 1
+      for (int jq = 0; jq < GPW / 2; ++jq) scatter_group(md, a, GF, tmem_cache, jq, cnt, warp, lane);
+    }
     TC_STAMP(10);
   }
 

@@ -88,6 +88,8 @@ extern "C" const char* apmg_version(void) { return "apmg-b200 0.1 sm_100a"; }
 extern "C" int apmg_device_sm_count(void) { return num_sms(); }
 extern "C" uint64_t apmg_launch_count(void) { return launch_counter().load(); }
 
+bool apmg::kernel_timing_on() { return g_timing; }
+
 extern "C" int apmg_kernel_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_tmu);
   if (!on) drain_pending();

@@ -131,7 +131,13 @@ struct apmg_train_state {
   size_t recon_wsb;
   void* dens_ws;
   size_t dens_wsb;
+  // CUDA graph of kGraphIters iterations, captured on first use and replayed (the
+  // iteration sequence is identical every time: all state lives in TrainCtl)
+  cudaGraphExec_t graph = nullptr;
+  uint64_t graph_launches = 0;
 };
+
+constexpr int64_t kGraphIters = 8;
 
 extern "C" int apmg_main_layout(const apmg_model* m, int64_t offsets[5]) {
   APMG_ARG_CHECK(m != nullptr, "null model");
@@ -315,11 +321,59 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   return APMG_OK;
 }
 
+static int run_direct(apmg_train_state* s, cudaStream_t st) {
+  return s->shape.dtype == APMG_F32 ? run_one<float>(s, st) : run_one<double>(s, st);
+}
+
+static bool graphs_enabled() {
+  const char* e = getenv("APMG_GRAPH");  // APMG_GRAPH=0: plain launches (A/B, debugging)
+  return !(e && e[0] == '0') && !kernel_timing_on();
+}
+
 extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
   APMG_ARG_CHECK(s != nullptr, "null state");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int64_t i = 0; i < n; ++i) {
-    const int rc = s->shape.dtype == APMG_F32 ? run_one<float>(s, st) : run_one<double>(s, st);
+  int64_t done = 0;
+  if (graphs_enabled() && n >= kGraphIters) {
+    if (!s->graph) {
+      int rc = run_direct(s, st);  // first iteration direct: one-time launch attributes set outside capture
+      if (rc) return rc;
+      ++done;
+      // capture on a private stream (the caller's may be the legacy default stream, which
+      // cannot capture); the graph is replayed on the caller's stream
+      cudaStream_t cs = nullptr;
+      APMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      APMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+      const uint64_t c0 = launch_counter().load();
+      for (int64_t i = 0; i < kGraphIters && rc == 0; ++i) rc = run_direct(s, cs);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      s->graph_launches = launch_counter().load() - c0;
+      launch_counter().fetch_sub(s->graph_launches);  // counted when replayed
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ec != cudaSuccess) {
+        set_error("train graph capture: %s", cudaGetErrorString(ec));
+        return APMG_E_CUDA;
+      }
+      const cudaError_t ei = cudaGraphInstantiate(&s->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) {
+        s->graph = nullptr;
+        set_error("train graph instantiate: %s", cudaGetErrorString(ei));
+        return APMG_E_CUDA;
+      }
+    }
+    for (; n - done >= kGraphIters; done += kGraphIters) {
+      APMG_CUDA_TRY(cudaGraphLaunch(s->graph, st));
+      launch_counter().fetch_add(s->graph_launches);
+    }
+  }
+  for (; done < n; ++done) {
+    const int rc = run_direct(s, st);
     if (rc) return rc;
   }
   return APMG_OK;
@@ -356,6 +410,7 @@ extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_dens
 }
 
 extern "C" int apmg_train_destroy(apmg_train_state* s) {
+  if (s && s->graph) cudaGraphExecDestroy(s->graph);
   delete s;
   return APMG_OK;
 }

@@ -29,8 +29,8 @@ torch.cuda.synchronize()
 buf = (C.c_longlong * (16 * 12))()
 L.check(L.lib().apmg_debug_tc_phases(buf))
 st = np.array(buf[:], dtype=np.int64).reshape(16, 12)[2:15]
-names = ["encode(+prev scatter tail)", "z1 mma wait", "epi1", "z2 mma wait", "epi2+head", "dz1 mma || dW2",
-         "dz1 epilogue", "gF mma || dW1", "gF epilogue", "scatter (thread 0)"]
+names = ["(unused)", "z1 mma wait", "epi1", "z2 mma wait", "epi2+head", "dz1 mma || dW2",
+         "dz1 epilogue", "gF mma || dW1", "gF epilogue", "scatter(t) + encode(t+1) (thread 0)"]
 d = np.diff(st[:, :11], axis=1)
 tile = np.diff(st[:, 0])
 print(f"cycles per tile (CTA 0): {tile.mean():.0f}")
