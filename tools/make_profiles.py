@@ -65,7 +65,7 @@ if __name__ == "__main__":
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
     res = {}
-    if len(sys.argv) > 2 and Path(sys.argv[2]).exists():
+    if len(sys.argv) > 2 and sys.argv[2] and Path(sys.argv[2]).exists():
         res["launches"] = launch_list(sys.argv[2])
     if len(sys.argv) > 3 and Path(sys.argv[3]).exists():
         res["full"] = full_capture(sys.argv[3])
