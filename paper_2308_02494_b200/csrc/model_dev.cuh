@@ -143,6 +143,16 @@ __device__ __forceinline__ void interp_pair(const ModelDev<float>& md, int m, co
   }
 }
 
+// packed fp32x2 (sm_100 FADD2 / FMUL2 / FFMA2): both channels of a corner in one
+// instruction, each half rounded exactly like the scalar operation
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2_lerp(float2 a, float2 b, float t) {  // a + t (b - a), per channel
+  return f2_fma(make_float2(t, t), f2_sub(b, a), a);
+}
+
 // Two channels in f32 arithmetic (training fast path: lerps rounded in f32 instead of
 // f64; features differ from the bit-exact encoder by <= 1 ulp).
 __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, int W, int HW, int vbase, float fx,
@@ -151,11 +161,10 @@ __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, 
   const float2 a000 = __ldg(g), a001 = __ldg(g + 1), a010 = __ldg(g + W), a011 = __ldg(g + W + 1);
   const float2 a100 = __ldg(g + HW), a101 = __ldg(g + HW + 1), a110 = __ldg(g + HW + W),
                a111 = __ldg(g + HW + W + 1);
-  auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
-  o0 = lerp(lerp(lerp(a000.x, a001.x, fx), lerp(a010.x, a011.x, fx), fy),
-            lerp(lerp(a100.x, a101.x, fx), lerp(a110.x, a111.x, fx), fy), fz);
-  o1 = lerp(lerp(lerp(a000.y, a001.y, fx), lerp(a010.y, a011.y, fx), fy),
-            lerp(lerp(a100.y, a101.y, fx), lerp(a110.y, a111.y, fx), fy), fz);
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(a000, a001, fx), f2_lerp(a010, a011, fx), fy),
+                           f2_lerp(f2_lerp(a100, a101, fx), f2_lerp(a110, a111, fx), fy), fz);
+  o0 = r.x;
+  o1 = r.y;
 }
 
 // Encode point (x0,x1,x2) in grid m into out[0..C) (zero outside the grid).
@@ -240,46 +249,26 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
   const int lane = threadIdx.x & 31;
   const int key = valid ? vbase : -1 - lane;
   const unsigned peers = __match_any_sync(0xffffffffu, key);
-  float v[16];
+  float2 v[8];  // corner c: (channel 0, channel 1)
   {
     const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+    const float2 g = make_float2(g0, g1);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float w = valid ? wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]) : 0.f;
-      v[2 * c] = g0 * w;
-      v[2 * c + 1] = g1 * w;
+      v[c] = f2_mul(g, make_float2(w, w));
     }
   }
   if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
     int rel = __popc(peers & ((1u << lane) - 1u));
     unsigned rem = peers & (0xfffffffeu << lane);
-    {
-      // round 1 pulls the partner's raw point (5 shuffles) and forms its 16 products here,
-      // instead of shuffling the 16 products (the shuffle crossbar is the scatter's bound)
-      const int next = __ffs(rem);
-      const int src = next ? next - 1 : lane;
-      const float pg0 = __shfl_sync(0xffffffffu, g0, src), pg1 = __shfl_sync(0xffffffffu, g1, src);
-      const float px = __shfl_sync(0xffffffffu, fx, src), py = __shfl_sync(0xffffffffu, fy, src),
-                  pz = __shfl_sync(0xffffffffu, fz, src);
-      if (next) {
-        const float wx[2] = {1.f - px, px}, wy[2] = {1.f - py, py}, wz[2] = {1.f - pz, pz};
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float w = wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]);
-          v[2 * c] += pg0 * w;
-          v[2 * c + 1] += pg1 * w;
-        }
-      }
-      rem &= __ballot_sync(0xffffffffu, !(rel & 1));
-      rel >>= 1;
-    }
     while (__any_sync(0xffffffffu, rem != 0u)) {
       const int next = __ffs(rem);
       const int src = next ? next - 1 : lane;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float t = __shfl_sync(0xffffffffu, v[k], src);
-        if (next) v[k] += t;
+      for (int c = 0; c < 8; ++c) {
+        const float2 t = make_float2(__shfl_sync(0xffffffffu, v[c].x, src), __shfl_sync(0xffffffffu, v[c].y, src));
+        if (next) v[c] = f2_add(v[c], t);
       }
       const unsigned keep = __ballot_sync(0xffffffffu, !(rel & 1));
       rem &= keep;
@@ -290,7 +279,7 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;
   float* base = dgrid + (size_t(vbase) << 1);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) atomic_add2(base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1), v[2 * c], v[2 * c + 1]);
+  for (int c = 0; c < 8; ++c) atomic_add2(base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1), v[c].x, v[c].y);
 }
 
 template <typename T>
