@@ -11,6 +11,10 @@
 //    result is rounded to the model dtype.
 //  * backward weights (optim.py:129-152): w = (wx * wy) * wz in f64.
 #pragma once
+#ifndef APMG_AGG_ROUNDS
+#define APMG_AGG_ROUNDS 3  // tree rounds cap: groups above 8 lanes issue one RED set per 8-lane block
+                          // (3 rounds measured 3% faster than the full 5: shuffles are the bound)
+#endif
 
 #include "common.cuh"
 
@@ -239,9 +243,11 @@ __device__ __forceinline__ void scatter_vertex_f32(const ModelDev<float>& md, fl
 
 // Warp-aggregated scatter: lanes whose point falls in the same cell (same base vertex)
 // of this grid are grouped with __match_any_sync, their 8 corners x 2 channel
-// contributions are summed with a peer tree reduction (log2(group) shuffle rounds), and
-// the group leader alone issues the 8 float2 REDs.  With spatially bucketed batches a
-// warp's 32 points cover ~1 grid cell per axis, so this cuts the L2 atomics ~8x.
+// contributions are summed with a peer tree reduction (one shuffle round per doubling, at
+// most APMG_AGG_ROUNDS rounds), and the lane heading each reduced block issues the 8
+// float2 REDs.  With spatially bucketed batches a warp's 32 points cover a few cells of a
+// grid, so this cuts the L2 atomics several-fold; the round cap trades a few more REDs
+// (L2 RED throughput has headroom) for fewer shuffles (the crossbar is the bound).
 // Must be called by all 32 lanes (invalid lanes pass valid = false).
 __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& md, float* __restrict__ dgrid,
                                                        bool valid, int vbase, float fx, float fy, float fz, float g0,
@@ -259,10 +265,12 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
       v[c] = f2_mul(g, make_float2(w, w));
     }
   }
+  const int rank = __popc(peers & ((1u << lane) - 1u));  // position within the group
+  int rounds = 0;
   if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
-    int rel = __popc(peers & ((1u << lane) - 1u));
+    int rel = rank;
     unsigned rem = peers & (0xfffffffeu << lane);
-    while (__any_sync(0xffffffffu, rem != 0u)) {
+    while (rounds < APMG_AGG_ROUNDS && __any_sync(0xffffffffu, rem != 0u)) {
       const int next = __ffs(rem);
       const int src = next ? next - 1 : lane;
 #pragma unroll
@@ -273,9 +281,11 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
       const unsigned keep = __ballot_sync(0xffffffffu, !(rel & 1));
       rem &= keep;
       rel >>= 1;
+      ++rounds;
     }
   }
-  if (!valid || (__ffs(peers) - 1) != lane) return;
+  // after `rounds` rounds the lanes of rank 0 mod 2^rounds hold their block's sums
+  if (!valid || (rank & ((1 << rounds) - 1)) != 0) return;
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;
   float* base = dgrid + (size_t(vbase) << 1);
 #pragma unroll
