@@ -200,6 +200,10 @@ int apmg_train_destroy(apmg_train_state* s);
 /* ---- tcgen05 self-test (one CTA, one GEMM; see csrc/umma_debug.cu) ---------- */
 int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
                          float* D, void* stream);
+/* 16-bit self-test (csrc/umma_bf16_debug.cu): D[M][N] = A[M][K] . B[K][N] (row-major f32 in),
+ * bf16x3 operands, mode bit 0 = B MN-major, bit 1 = A MN-major, split3: 6 products */
+int apmg_debug_umma_bf16(int32_t mode, int32_t M, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
+                         float* D, void* stream);
 /* clock64 stamps [16 tiles][12 phases] of CTA 0 of the last fused recon launch run with
  * APMG_TC_SKIP & 64 (profiling aid, tools/tc_phases.py) */
 int apmg_debug_tc_phases(long long* out);

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <cuda_bf16.h>
 
 namespace apmg {
 namespace umma {
@@ -89,6 +90,40 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// ---- 16-bit operands (kind::f16 with BF16 inputs, F32 accumulate) ----
+// CM layout for 2-byte elements: 8 rows x 16 B (8 elements) core matrices,
+//     byte offset(r, c) = (c/8)*R*16 + (r/8)*128 + (r%8)*16 + (c%8)*2,
+// K-major with rows = M/N (desc_kmajor: one K=16 MMA spans two 16-B chunks, like K=8 tf32)
+// and, for 16-bit types, also usable MN-major with rows = K (desc_mnmajor16).
+__host__ __device__ constexpr uint32_t cm16_offset(int r, int c, int R) {
+  return uint32_t((c >> 3) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (c & 7) * 2);
+}
+// MN-major descriptor at K-step kk (K=16 = two 8-row groups, 128 B apart)
+__device__ __forceinline__ uint64_t desc_mnmajor16(uint32_t base, int R, int kk) {
+  return smem_desc(base + uint32_t(kk) * 256u, 128u, uint32_t(R * 16));
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                      // c_format = F32
+         | (1u << 7)                    // a_format = BF16
+         | (1u << 10)                   // b_format = BF16
+         | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// x = h + m + l in bf16 (8+8+8 significant bits: the f32 significand, exponent permitting)
+__device__ __forceinline__ void split_bf16x3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
+  h = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(h);
+  m = __float2bfloat16_rn(r1);
+  l = __float2bfloat16_rn(r1 - __bfloat162float(m));
 }
 
 __device__ __forceinline__ void commit(uint64_t* mbar) {
