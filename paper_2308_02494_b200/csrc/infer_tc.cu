@@ -1,61 +1,62 @@
 // Tensor-core lattice sweep (trainer.py:226-247 psnr, decomposition.py:294-304 brick boxes)
 // for the flagship shape (float32, 64 grids x 2 channels -> 128 features, 64 hidden).
 //
-// One persistent CTA (16 warps) per SM, 64-voxel tiles, software-pipelined so that both
-// tensor-core products hide behind CUDA-core work:
+// One persistent CTA (16 warps) per SM, 128-voxel tiles (M=128 tcgen05 products: TMEM lane
+// = voxel), software-pipelined so that both tensor-core products hide behind CUDA-core work:
 //     encode(t) | z1(t) issue | head(t-1) [z2(t-1) wait] | z1 wait, epilogue 1 -> h1 |
 //     z2(t) issue | encode(t+1) ...
 //   encode   lattice voxel -> f32 coordinate (the reference casts the f64 lattice
 //            coordinate to float32 before predicting) -> per-grid f32 cell math -> features
-//            split into TF32 hi/lo in the CM layout
-//   z1, z2   tcgen05.mma kind::tf32, M=64, N=64, 3 products (3xTF32)
+//   z1, z2   tcgen05.mma kind::f16 on bf16x3 operands (x = h + m + l, 8+8+8 significant bits;
+//            6 products hh, hm, mh, hl, lh, mm: f32-level accuracy, each product exact in the
+//            f32 accumulator)
 //   head     out = relu(z2) w3 * span + vmin; reconstruct-to-HBM and / or f64 SSE vs truth
 // Features use f32 lerps (<= 1 ulp from the bit-exact f64-lerp encoder of k_forward);
 // outputs agree with the reference forward to ~1e-6 relative (forward gate 1e-4).
+//
+// Shared memory (221 KB): W1 (3 x 16 KB) | W2 (3 x 8 KB) | F [128][128] (3 x 32 KB) |
+// h1 [128][64] (3 x 16 KB) | small.  Operands in the 16-bit CM layout of umma.cuh.
 #include "fwd_args.cuh"
 #include "umma.cuh"
 
 namespace apmg {
 namespace itc {
 
-constexpr int P = 64;
+constexpr int P = 128;
 constexpr int NW = 16;
 constexpr int NT = 32 * NW;
-constexpr int WQ = NW / 4;
-constexpr int EPC = 64 / WQ;
-constexpr int GPW = 64 / NW;
+constexpr int WQ = NW / 4;     // warps per TMEM lane quarter
+constexpr int EPC = 64 / WQ;   // accumulator columns per warp in the epilogues (16)
 constexpr int FE = 128;
 constexpr int HID = 64;
 
-// weights as stacked [hi rows; lo rows] CM buffers (R = 128): one N=128 product gives
-// X.Whi and X.Wlo side by side, a second N=64 product adds Xlo.Whi onto the lo half
-constexpr uint32_t OFF_W1S = 0;                        // [128][128]
-constexpr uint32_t OFF_W2S = OFF_W1S + 128 * 128 * 4;  // [128][64]
-constexpr uint32_t OFF_FH = OFF_W2S + 128 * 64 * 4;
-constexpr uint32_t OFF_FL = OFF_FH + P * FE * 4;
-constexpr uint32_t OFF_H1H = OFF_FL + P * FE * 4;
-constexpr uint32_t OFF_H1L = OFF_H1H + P * HID * 4;
-constexpr uint32_t OFF_X = OFF_H1L + P * HID * 4;     // [2][P][3] (tile parity)
+constexpr uint32_t W1_PLANE = 64 * 128 * 2, W2_PLANE = 64 * 64 * 2, F_PLANE = P * FE * 2, H1_PLANE = P * HID * 2;
+constexpr uint32_t OFF_W1 = 0;
+constexpr uint32_t OFF_W2 = OFF_W1 + 3 * W1_PLANE;
+constexpr uint32_t OFF_F = OFF_W2 + 3 * W2_PLANE;
+constexpr uint32_t OFF_H1 = OFF_F + 3 * F_PLANE;
+constexpr uint32_t OFF_X = OFF_H1 + 3 * H1_PLANE;     // [2][P][3] (tile parity)
 constexpr uint32_t OFF_TRU = OFF_X + 2 * P * 3 * 4;   // [3][P] truth values (tile index mod 3)
 constexpr uint32_t OFF_HEAD = OFF_TRU + 3 * P * 4;    // [WQ][P]
 constexpr uint32_t OFF_RED = OFF_HEAD + WQ * P * 4;   // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // 2 mbarriers
 constexpr uint32_t OFF_TM = OFF_BAR + 16;
-constexpr uint32_t OFF_TF = OFF_TM + 16;              // [64][12]
-constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;     // [64]
-constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
+constexpr uint32_t OFF_W3 = OFF_TM + 16;              // [64]
+constexpr uint32_t OFF_TF = OFF_W3 + 64 * 4;          // [64][12] transforms (f32)
+constexpr uint32_t SMEM_BYTES = OFF_TF + 64 * 12 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-constexpr uint32_t TMEM_COLS = 256;  // z1 (hi | lo halves) | z2 (hi | lo halves)
+constexpr uint32_t TMEM_COLS = 128;  // z1 | z2
 
-// per-phase clock stamps of CTA 0 / thread 0 (APMG_INFER_STAMPS=1, tools/tc_phases.py --infer)
+// bf16x3 products q = 0..5: (A plane, B plane) = hh, hm, mh, hl, lh, mm (largest first)
+__host__ __device__ constexpr int kPA(int q) { return q == 2 ? 1 : (q == 4 ? 2 : (q == 5 ? 1 : 0)); }
+__host__ __device__ constexpr int kPB(int q) { return q == 1 ? 1 : (q == 3 ? 2 : (q == 5 ? 1 : 0)); }
+
+// per-phase clock stamps of CTA 0 / thread 0 (APMG_INFER_STAMPS=1, tools/infer_phases.py)
 __device__ long long g_itc_stamp[16][8];
 #define ITC_STAMP(k)                                                                 \
   do {                                                                               \
     if (a.stamps && blockIdx.x == 0 && tid == 0 && it < 16) g_itc_stamp[it][k] = clock64(); \
   } while (0)
-
-__device__ __forceinline__ float* fptr(unsigned char* sm, uint32_t off) { return reinterpret_cast<float*>(sm + off); }
-__device__ __forceinline__ uint32_t cm64(int r, int c) { return umma::cm_offset(r, c, 64) >> 2; }
 
 // per-axis coordinate tables: the lattice coordinate of a voxel is separable (f64 lattice
 // coordinate -> float32 -> optional f64 brick affine -> float32, fwd_point), so each axis
@@ -93,41 +94,59 @@ __device__ __forceinline__ int64_t voxel_of(const FwdArgs<float>& a, int64_t i) 
   return lattice_elem(a, x, y, z);
 }
 
+// bf16x3 split of a pair (packed cvt.rn.bf16x2.f32 and fp32x2 residuals), as 3 packed words
+__device__ __forceinline__ void split2_bf16x3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+  const __nv_bfloat162 bh = __float22bfloat162_rn(make_float2(x0, x1));
+  const float2 r1 = __fadd2_rn(make_float2(x0, x1), make_float2(-__low2float(bh), -__high2float(bh)));
+  const __nv_bfloat162 bm = __float22bfloat162_rn(r1);
+  const float2 r2 = __fadd2_rn(r1, make_float2(-__low2float(bm), -__high2float(bm)));
+  const __nv_bfloat162 bl = __float22bfloat162_rn(r2);
+  h = *reinterpret_cast<const uint32_t*>(&bh);
+  m = *reinterpret_cast<const uint32_t*>(&bm);
+  l = *reinterpret_cast<const uint32_t*>(&bl);
+}
+
+// write 8 consecutive columns (one 16-B chunk per plane) of row r of a bf16x3 CM buffer
+__device__ __forceinline__ void store_chunk3(unsigned char* buf, uint32_t plane, int r, int c0, int R, const float* v) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) split2_bf16x3(v[2 * e], v[2 * e + 1], h[e], m[e], l[e]);
+  const uint32_t o = umma::cm16_offset(r, c0, R);
+  *reinterpret_cast<uint4*>(buf + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(buf + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
+  *reinterpret_cast<uint4*>(buf + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const float* __restrict__ tab) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const ModelDev<float>& md = a.md;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int quarter = warp & 3, wq = warp >> 2;
-  float* W1s = fptr(sm, OFF_W1S);
-  float* W2s = fptr(sm, OFF_W2S);
-  float* Fh = fptr(sm, OFF_FH);
-  float* Fl = fptr(sm, OFF_FL);
-  float* H1h = fptr(sm, OFF_H1H);
-  float* H1l = fptr(sm, OFF_H1L);
-  float* sX = fptr(sm, OFF_X);
-  float* sHead = fptr(sm, OFF_HEAD);
-  float* sTru = fptr(sm, OFF_TRU);
+  unsigned char* W1 = sm + OFF_W1;
+  unsigned char* W2 = sm + OFF_W2;
+  unsigned char* F = sm + OFF_F;
+  unsigned char* H1 = sm + OFF_H1;
+  float* sX = reinterpret_cast<float*>(sm + OFF_X);
+  float* sTru = reinterpret_cast<float*>(sm + OFF_TRU);
+  float* sHead = reinterpret_cast<float*>(sm + OFF_HEAD);
   double* red = reinterpret_cast<double*>(sm + OFF_RED);
   uint64_t* bar1 = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
   uint64_t* bar2 = bar1 + 1;
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
-  float* sTF = fptr(sm, OFF_TF);
-  float* sW3 = fptr(sm, OFF_W3);
+  float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
 
-  for (int e = tid; e < 64 * 128; e += NT) {
-    float hi, lo;
-    umma::split_tf32(md.w1[e], hi, lo);
-    W1s[umma::cm_offset(e >> 7, e & 127, 128) >> 2] = hi;
-    W1s[umma::cm_offset(64 + (e >> 7), e & 127, 128) >> 2] = lo;
+  // weights: rows = output unit, 8-column chunks
+  for (int e = tid; e < 64 * 16; e += NT) {
+    const int r = e >> 4, c0 = (e & 15) * 8;
+    store_chunk3(W1, W1_PLANE, r, c0, 64, md.w1 + r * FE + c0);
   }
-  for (int e = tid; e < 64 * 64; e += NT) {
-    float hi, lo;
-    umma::split_tf32(md.w2[e], hi, lo);
-    W2s[umma::cm_offset(e >> 6, e & 63, 128) >> 2] = hi;
-    W2s[umma::cm_offset(64 + (e >> 6), e & 63, 128) >> 2] = lo;
+  for (int e = tid; e < 64 * 8; e += NT) {
+    const int r = e >> 3, c0 = (e & 7) * 8;
+    store_chunk3(W2, W2_PLANE, r, c0, 64, md.w2 + r * HID + c0);
   }
-  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (tid < HID) sW3[tid] = md.w3[tid];
+  float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
+  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar1, 1);
@@ -139,30 +158,27 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = *tm_slot;
-  const uint32_t TZ1 = tmem, TZ2 = tmem + 128;
+  const uint32_t TZ1 = tmem, TZ2 = tmem + 64;
   const uint32_t lane_base = uint32_t(32 * quarter) << 16;
-  const uint32_t sW1s = umma::smem_u32(W1s), sW2s = umma::smem_u32(W2s), sFh = umma::smem_u32(Fh),
-                 sFl = umma::smem_u32(Fl), sH1h = umma::smem_u32(H1h), sH1l = umma::smem_u32(H1l);
-  const uint32_t idesc64 = umma::idesc_tf32(64, 64, false, false), idesc128 = umma::idesc_tf32(64, 128, false, false);
-  const int ep_row = 16 * quarter + lane;
+  const uint32_t sW1 = umma::smem_u32(W1), sW2 = umma::smem_u32(W2), sF = umma::smem_u32(F), sH1 = umma::smem_u32(H1);
+  const uint32_t idesc = umma::idesc_bf16(128, 64, false, false);
+  const int ep_row = 32 * quarter + lane;  // M=128 accumulator: row = lane
   const int ep_col0 = EPC * wq;
   uint32_t ph1 = 0, ph2 = 0;
   double sse = 0.0;
+  int it = 0;
 
   // head of a finished tile: relu(z2) . w3 -> output / SSE (waits for its z2)
   auto head = [&](int64_t tile, int par) {
     umma::mbar_wait(bar2, ph2);
     ph2 ^= 1;
     umma::fence_after_sync();
-    float v[EPC], w[EPC];
+    float v[EPC];
     umma::tmem_ld16(TZ2 + lane_base + ep_col0, v);
-    umma::tmem_ld16(TZ2 + lane_base + 64 + ep_col0, w);
-    if (lane < 16) {
-      float part = 0.f;
+    float part = 0.f;
 #pragma unroll
-      for (int c = 0; c < EPC; ++c) part = fmaf(fmaxf(v[c] + w[c], 0.f), sW3[ep_col0 + c], part);
-      sHead[wq * P + ep_row] = part;
-    }
+    for (int c = 0; c < EPC; ++c) part = fmaf(fmaxf(v[c], 0.f), sW3[ep_col0 + c], part);
+    sHead[wq * P + ep_row] = part;
     umma::fence_before_sync();
     __syncthreads();
     if (tid < P) {
@@ -185,11 +201,10 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
   const float* tx = tab;
   const float* ty = tab + a.bw;
   const float* tz = tab + a.bw + a.bh;
-  int64_t prev = -1;
-  int it = 0;
-  // coordinates (axis-table lookups) and truth values of one tile into parity buffers
+  // coordinates (axis-table lookups) and truth values of one tile into parity buffers,
+  // by the last four warps (warp 0 issues the MMAs)
   auto load_coords = [&](int64_t tile, int slot) {
-    const int t = tid - (NT - P);  // the last two warps (warp 0 issues the MMAs)
+    const int t = tid - (NT - P);
     if (t < 0) return;
     float x0 = 0.f, x1 = 0.f, x2 = 0.f, tv = 0.f;
     const int64_t i = tile * P + t;
@@ -211,23 +226,26 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
   };
   load_coords(blockIdx.x, 0);
   __syncthreads();
+  int64_t prev = -1;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     ITC_STAMP(0);
     const float* cX = sX + (it & 1) * 3 * P;
-    // ---- encode (overlaps the z2 product of the previous tile) ----
+    // ---- encode (overlaps z2 of the previous tile): warp w owns grids 4w..4w+3, i.e.
+    // feature columns 8w..8w+7 (one 16-B chunk per plane); lane -> points lane + 32h ----
     {
-      const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
-                              {cX[3 * (lane + 32)], cX[3 * (lane + 32) + 1], cX[3 * (lane + 32) + 2]}};
-#pragma unroll 1
-      for (int jq = 0; jq < GPW / 2; ++jq) {
+      const float* tfw = sTF + 12 * (4 * warp);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 2 * jq + (u >> 1), h = u & 1;
-          const int m = warp + NW * j, p = lane + 32 * h;
-          const float* tf = sTF + 12 * m;
-          const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
-          const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
-          const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
+      for (int h = 0; h < P / 32; ++h) {
+        const int p = lane + 32 * h;
+        const float x0 = cX[3 * p], x1 = cX[3 * p + 1], x2 = cX[3 * p + 2];
+        float fv[8];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int m = 4 * warp + g;
+          const float* tf = tfw + 12 * g;
+          const float l0 = local_coord(x0, x1, x2, tf[0], tf[1], tf[2], tf[3]);
+          const float l1 = local_coord(x0, x1, x2, tf[4], tf[5], tf[6], tf[7]);
+          const float l2 = local_coord(x0, x1, x2, tf[8], tf[9], tf[10], tf[11]);
           const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
           int ix, iy, iz;
           double fxd, fyd, fzd;
@@ -238,13 +256,10 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
           if (inside)
             interp_pair_f32(md.grid, md.W, md.H * md.W, ((m * md.D + iz) * md.H + iy) * md.W + ix, float(fxd),
                             float(fyd), float(fzd), f0, f1);
-          float hi0, lo0, hi1, lo1;
-          umma::split_tf32(f0, hi0, lo0);
-          umma::split_tf32(f1, hi1, lo1);
-          const uint32_t o = cm64(p, 2 * m);
-          *reinterpret_cast<float2*>(Fh + o) = make_float2(hi0, hi1);
-          *reinterpret_cast<float2*>(Fl + o) = make_float2(lo0, lo1);
+          fv[2 * g] = f0;
+          fv[2 * g + 1] = f1;
         }
+        store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
       }
     }
     umma::fence_async_smem();
@@ -253,49 +268,39 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
     umma::fence_after_sync();
     ITC_STAMP(2);
     if (tid == 0) {
-      for (int kk = 0; kk < FE / 8; ++kk) {
-        const uint64_t fh = umma::desc_kmajor(sFh, 64, kk), fl = umma::desc_kmajor(sFl, 64, kk);
-        const uint64_t ws = umma::desc_kmajor(sW1s, 128, kk);
-        umma::mma_tf32(TZ1, fh, ws, idesc128, kk > 0);  // [Fh.Whi | Fh.Wlo]
-        umma::mma_tf32(TZ1 + 64, fl, ws, idesc64, 1);   // lo half += Flo.Whi
-      }
+      for (int kk = 0; kk < FE / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          umma::mma_bf16(TZ1, umma::desc_kmajor(sF + kPA(q) * F_PLANE, P, kk),
+                         umma::desc_kmajor(sW1 + kPB(q) * W1_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
       umma::commit(bar1);
     }
     load_coords(tile + gridDim.x, it + 1);  // next tile's inputs (slots not read until then)
     // ---- head of the previous tile (overlaps z1 of this one) ----
     if (prev >= 0) head(prev, (it + 2) % 3);
     ITC_STAMP(3);
-    // ---- epilogue 1 ----
+    // ---- epilogue 1: h1 = relu(z1) -> bf16x3 h1 rows ----
     umma::mbar_wait(bar1, ph1);
     ph1 ^= 1;
     umma::fence_after_sync();
     {
-      float v[EPC], w[EPC];
+      float v[EPC];
       umma::tmem_ld16(TZ1 + lane_base + ep_col0, v);
-      umma::tmem_ld16(TZ1 + lane_base + 64 + ep_col0, w);
-      if (lane < 16) {
 #pragma unroll
-        for (int c4 = 0; c4 < EPC; c4 += 4) {
-          float hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) umma::split_tf32(fmaxf(v[c4 + e] + w[c4 + e], 0.f), hi[e], lo[e]);
-          const uint32_t o = cm64(ep_row, ep_col0 + c4);
-          *reinterpret_cast<float4*>(H1h + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(H1l + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-        }
-      }
+      for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
+      store_chunk3(H1, H1_PLANE, ep_row, ep_col0, P, v);
+      store_chunk3(H1, H1_PLANE, ep_row, ep_col0 + 8, P, v + 8);
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
     if (tid == 0) {
-      for (int kk = 0; kk < HID / 8; ++kk) {
-        const uint64_t hh = umma::desc_kmajor(sH1h, 64, kk), hl = umma::desc_kmajor(sH1l, 64, kk);
-        const uint64_t ws = umma::desc_kmajor(sW2s, 128, kk);
-        umma::mma_tf32(TZ2, hh, ws, idesc128, kk > 0);
-        umma::mma_tf32(TZ2 + 64, hl, ws, idesc64, 1);
-      }
+      for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          umma::mma_bf16(TZ2, umma::desc_kmajor(sH1 + kPA(q) * H1_PLANE, P, kk),
+                         umma::desc_kmajor(sW2 + kPB(q) * W2_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
       umma::commit(bar2);
     }
     ITC_STAMP(4);
