@@ -23,8 +23,9 @@ namespace apmg {
 namespace itc {
 
 constexpr int P = 128;
-constexpr int NW = 16;
-constexpr int NT = 32 * NW;
+constexpr int NW = 16;          // worker warps (encode, epilogues, head)
+constexpr int NT = 32 * NW;     // worker threads (named barrier 1)
+constexpr int NTA = NT + 32;    // + one warp that only issues the tensor-core products
 constexpr int WQ = NW / 4;     // warps per TMEM lane quarter
 constexpr int EPC = 64 / WQ;   // accumulator columns per warp in the epilogues (16)
 constexpr int FE = 128;
@@ -39,8 +40,8 @@ constexpr uint32_t OFF_X = OFF_H1 + 3 * H1_PLANE;     // [2][P][3] (tile parity)
 constexpr uint32_t OFF_TRU = OFF_X + 2 * P * 3 * 4;   // [3][P] truth values (tile index mod 3)
 constexpr uint32_t OFF_HEAD = OFF_TRU + 3 * P * 4;    // [WQ][P]
 constexpr uint32_t OFF_RED = OFF_HEAD + WQ * P * 4;   // [32] doubles
-constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // 2 mbarriers
-constexpr uint32_t OFF_TM = OFF_BAR + 16;
+constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // 4 mbarriers: z1 done, z2 done, F ready, h1 ready
+constexpr uint32_t OFF_TM = OFF_BAR + 32;
 constexpr uint32_t OFF_W3 = OFF_TM + 16;              // [64]
 constexpr uint32_t OFF_TF = OFF_W3 + 64 * 4;          // [64][12] transforms (f32)
 constexpr uint32_t SMEM_BYTES = OFF_TF + 64 * 12 * 4;
@@ -117,7 +118,7 @@ __device__ __forceinline__ void store_chunk3(unsigned char* buf, uint32_t plane,
   *reinterpret_cast<uint4*>(buf + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-__global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const float* __restrict__ tab) {
+__global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const float* __restrict__ tab) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const ModelDev<float>& md = a.md;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -130,27 +131,31 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
   float* sTru = reinterpret_cast<float*>(sm + OFF_TRU);
   float* sHead = reinterpret_cast<float*>(sm + OFF_HEAD);
   double* red = reinterpret_cast<double*>(sm + OFF_RED);
-  uint64_t* bar1 = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint64_t* bar2 = bar1 + 1;
+  uint64_t* bar1 = reinterpret_cast<uint64_t*>(sm + OFF_BAR);  // z1 committed
+  uint64_t* bar2 = bar1 + 1;                                     // z2 committed
+  uint64_t* barF = bar1 + 2;                                     // F written by all worker warps
+  uint64_t* barH = bar1 + 3;                                     // h1 written by all worker warps
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
   float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
 
   // weights: rows = output unit, 8-column chunks
-  for (int e = tid; e < 64 * 16; e += NT) {
+  for (int e = tid; e < 64 * 16; e += NTA) {
     const int r = e >> 4, c0 = (e & 15) * 8;
     store_chunk3(W1, W1_PLANE, r, c0, 64, md.w1 + r * FE + c0);
   }
-  for (int e = tid; e < 64 * 8; e += NT) {
+  for (int e = tid; e < 64 * 8; e += NTA) {
     const int r = e >> 3, c0 = (e & 7) * 8;
     store_chunk3(W2, W2_PLANE, r, c0, 64, md.w2 + r * HID + c0);
   }
   if (tid < HID) sW3[tid] = md.w3[tid];
   float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
-  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  for (int e = tid; e < 64 * 12; e += NTA) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar1, 1);
     umma::mbar_init(bar2, 1);
+    umma::mbar_init(barF, NW);
+    umma::mbar_init(barH, NW);
     umma::fence_mbar_init();
   }
   umma::fence_async_smem();
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
     for (int c = 0; c < EPC; ++c) part = fmaf(fmaxf(v[c], 0.f), sW3[ep_col0 + c], part);
     sHead[wq * P + ep_row] = part;
     umma::fence_before_sync();
-    __syncthreads();
+    umma::named_sync(1, NT);  // worker warps only
     if (tid < P) {
       const int64_t i = tile * P + tid;
       if (i < a.n) {
@@ -198,115 +203,144 @@ __global__ void __launch_bounds__(NT, 1) k_infer_tc(FwdArgs<float> a, const floa
   };
 
   const int64_t tiles = ceil_div(a.n, P);
-  const float* tx = tab;
-  const float* ty = tab + a.bw;
-  const float* tz = tab + a.bw + a.bh;
-  // coordinates (axis-table lookups) and truth values of one tile into parity buffers,
-  // by the last four warps (warp 0 issues the MMAs)
-  auto load_coords = [&](int64_t tile, int slot) {
-    const int t = tid - (NT - P);
-    if (t < 0) return;
-    float x0 = 0.f, x1 = 0.f, x2 = 0.f, tv = 0.f;
-    const int64_t i = tile * P + t;
-    if (tile < tiles && i < a.n) {
-      const int64_t plane = int64_t(a.bw) * a.bh;
-      const int z = int(i / plane);
-      const int64_t r = i - z * plane;
-      const int y = int(r / a.bw), x = int(r - int64_t(y) * a.bw);
-      x0 = tx[x];
-      x1 = ty[y];
-      x2 = tz[z];
-      if (a.truth) tv = a.truth[lattice_elem(a, x, y, z)];
-    }
-    float* d = sX + (slot & 1) * 3 * P;
-    d[3 * t] = x0;
-    d[3 * t + 1] = x1;
-    d[3 * t + 2] = x2;
-    sTru[(slot % 3) * P + t] = tv;
-  };
-  load_coords(blockIdx.x, 0);
-  __syncthreads();
-  int64_t prev = -1;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-    ITC_STAMP(0);
-    const float* cX = sX + (it & 1) * 3 * P;
-    // ---- encode (overlaps z2 of the previous tile): warp w owns grids 4w..4w+3, i.e.
-    // feature columns 8w..8w+7 (one 16-B chunk per plane); lane -> points lane + 32h ----
-    {
-      const float* tfw = sTF + 12 * (4 * warp);
+  if (warp == NW) {
+    // ---- MMA warp: z1 when the workers' F is complete, z2 when their h1 is ----
+    uint32_t pf = 0, ph = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      umma::mbar_wait(barF, pf);
+      pf ^= 1;
+      umma::fence_after_sync();
+      if (lane == 0) {
+        for (int kk = 0; kk < FE / 16; ++kk)
 #pragma unroll
-      for (int h = 0; h < P / 32; ++h) {
-        const int p = lane + 32 * h;
-        const float x0 = cX[3 * p], x1 = cX[3 * p + 1], x2 = cX[3 * p + 2];
-        float fv[8];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int m = 4 * warp + g;
-          const float* tf = tfw + 12 * g;
-          const float l0 = local_coord(x0, x1, x2, tf[0], tf[1], tf[2], tf[3]);
-          const float l1 = local_coord(x0, x1, x2, tf[4], tf[5], tf[6], tf[7]);
-          const float l2 = local_coord(x0, x1, x2, tf[8], tf[9], tf[10], tf[11]);
-          const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
-          int ix, iy, iz;
-          double fxd, fyd, fzd;
-          axis_term(l0, md.W, ix, fxd);
-          axis_term(l1, md.H, iy, fyd);
-          axis_term(l2, md.D, iz, fzd);
-          float f0 = 0.f, f1 = 0.f;
-          if (inside)
-            interp_pair_f32(md.grid, md.W, md.H * md.W, ((m * md.D + iz) * md.H + iy) * md.W + ix, float(fxd),
-                            float(fyd), float(fzd), f0, f1);
-          fv[2 * g] = f0;
-          fv[2 * g + 1] = f1;
-        }
-        store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
+          for (int q = 0; q < 6; ++q)
+            umma::mma_bf16(TZ1, umma::desc_kmajor(sF + kPA(q) * F_PLANE, P, kk),
+                           umma::desc_kmajor(sW1 + kPB(q) * W1_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
+        umma::commit(bar1);
       }
-    }
-    umma::fence_async_smem();
-    umma::fence_before_sync();
-    __syncthreads();
-    umma::fence_after_sync();
-    ITC_STAMP(2);
-    if (tid == 0) {
-      for (int kk = 0; kk < FE / 16; ++kk)
+      __syncwarp();
+      umma::mbar_wait(barH, ph);
+      ph ^= 1;
+      umma::fence_after_sync();
+      if (lane == 0) {
+        for (int kk = 0; kk < HID / 16; ++kk)
 #pragma unroll
-        for (int q = 0; q < 6; ++q)
-          umma::mma_bf16(TZ1, umma::desc_kmajor(sF + kPA(q) * F_PLANE, P, kk),
-                         umma::desc_kmajor(sW1 + kPB(q) * W1_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
-      umma::commit(bar1);
+          for (int q = 0; q < 6; ++q)
+            umma::mma_bf16(TZ2, umma::desc_kmajor(sH1 + kPA(q) * H1_PLANE, P, kk),
+                           umma::desc_kmajor(sW2 + kPB(q) * W2_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
+        umma::commit(bar2);
+      }
+      __syncwarp();
     }
-    load_coords(tile + gridDim.x, it + 1);  // next tile's inputs (slots not read until then)
-    // ---- head of the previous tile (overlaps z1 of this one) ----
+  } else {
+    const float* tx = tab;
+    const float* ty = tab + a.bw;
+    const float* tz = tab + a.bw + a.bh;
+    // coordinates (axis-table lookups) and truth values of one tile into parity buffers,
+    // by the last four worker warps
+    // split in two: fetch (global loads into registers, issued at the top of an iteration so
+    // their latency hides behind the encode) and publish (smem stores after the encode)
+    struct Pre {
+      float x0, x1, x2, tv;
+    };
+    auto fetch_coords = [&](int64_t tile) {
+      Pre r{0.f, 0.f, 0.f, 0.f};
+      const int t = tid - (NT - P);
+      const int64_t i = tile * P + t;
+      if (t >= 0 && tile < tiles && i < a.n) {
+        const int64_t plane = int64_t(a.bw) * a.bh;
+        const int z = int(i / plane);
+        const int64_t rr = i - z * plane;
+        const int y = int(rr / a.bw), x = int(rr - int64_t(y) * a.bw);
+        r.x0 = tx[x];
+        r.x1 = ty[y];
+        r.x2 = tz[z];
+        if (a.truth) r.tv = a.truth[lattice_elem(a, x, y, z)];
+      }
+      return r;
+    };
+    auto publish_coords = [&](const Pre& r, int slot) {
+      const int t = tid - (NT - P);
+      if (t < 0) return;
+      float* d = sX + (slot & 1) * 3 * P;
+      d[3 * t] = r.x0;
+      d[3 * t + 1] = r.x1;
+      d[3 * t + 2] = r.x2;
+      sTru[(slot % 3) * P + t] = r.tv;
+    };
+    auto load_coords = [&](int64_t tile, int slot) { publish_coords(fetch_coords(tile), slot); };
+    load_coords(blockIdx.x, 0);
+    umma::named_sync(1, NT);
+    int64_t prev = -1;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      ITC_STAMP(0);
+      const float* cX = sX + (it & 1) * 3 * P;
+      const Pre nxt = fetch_coords(tile + gridDim.x);  // next tile's inputs, in flight during the encode
+      // ---- encode (overlaps z2 of the previous tile): warp w owns grids 4w..4w+3, i.e.
+      // feature columns 8w..8w+7 (one 16-B chunk per plane); lane -> points lane + 32h ----
+      {
+        const float* tfw = sTF + 12 * (4 * warp);
+  #pragma unroll
+        for (int h = 0; h < P / 32; ++h) {
+          const int p = lane + 32 * h;
+          const float x0 = cX[3 * p], x1 = cX[3 * p + 1], x2 = cX[3 * p + 2];
+          float fv[8];
+  #pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int m = 4 * warp + g;
+            const float* tf = tfw + 12 * g;
+            const float l0 = local_coord(x0, x1, x2, tf[0], tf[1], tf[2], tf[3]);
+            const float l1 = local_coord(x0, x1, x2, tf[4], tf[5], tf[6], tf[7]);
+            const float l2 = local_coord(x0, x1, x2, tf[8], tf[9], tf[10], tf[11]);
+            const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
+            int ix, iy, iz;
+            double fxd, fyd, fzd;
+            axis_term(l0, md.W, ix, fxd);
+            axis_term(l1, md.H, iy, fyd);
+            axis_term(l2, md.D, iz, fzd);
+            float f0 = 0.f, f1 = 0.f;
+            if (inside)
+              interp_pair_f32(md.grid, md.W, md.H * md.W, ((m * md.D + iz) * md.H + iy) * md.W + ix, float(fxd),
+                              float(fyd), float(fzd), f0, f1);
+            fv[2 * g] = f0;
+            fv[2 * g + 1] = f1;
+          }
+          store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
+        }
+      }
+      umma::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) umma::mbar_arrive(barF);  // this warp's F columns are in place
+      ITC_STAMP(2);
+      publish_coords(nxt, it + 1);  // next tile's inputs (slots not read until then)
+      // ---- head of the previous tile (overlaps z1 of this one); its worker barrier also
+      // publishes the coordinates just loaded (first tile: an explicit barrier) ----
+      if (prev >= 0)
+        head(prev, (it + 2) % 3);
+      else
+        umma::named_sync(1, NT);
+      ITC_STAMP(3);
+      // ---- epilogue 1: h1 = relu(z1) -> bf16x3 h1 rows ----
+      umma::mbar_wait(bar1, ph1);
+      ph1 ^= 1;
+      umma::fence_after_sync();
+      {
+        float v[EPC];
+        umma::tmem_ld16(TZ1 + lane_base + ep_col0, v);
+  #pragma unroll
+        for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
+        store_chunk3(H1, H1_PLANE, ep_row, ep_col0, P, v);
+        store_chunk3(H1, H1_PLANE, ep_row, ep_col0 + 8, P, v + 8);
+      }
+      umma::fence_async_smem();
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) umma::mbar_arrive(barH);  // this warp's h1 rows are in place
+      ITC_STAMP(4);
+      prev = tile;
+    }
     if (prev >= 0) head(prev, (it + 2) % 3);
-    ITC_STAMP(3);
-    // ---- epilogue 1: h1 = relu(z1) -> bf16x3 h1 rows ----
-    umma::mbar_wait(bar1, ph1);
-    ph1 ^= 1;
-    umma::fence_after_sync();
-    {
-      float v[EPC];
-      umma::tmem_ld16(TZ1 + lane_base + ep_col0, v);
-#pragma unroll
-      for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
-      store_chunk3(H1, H1_PLANE, ep_row, ep_col0, P, v);
-      store_chunk3(H1, H1_PLANE, ep_row, ep_col0 + 8, P, v + 8);
-    }
-    umma::fence_async_smem();
-    umma::fence_before_sync();
-    __syncthreads();
-    umma::fence_after_sync();
-    if (tid == 0) {
-      for (int kk = 0; kk < HID / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 6; ++q)
-          umma::mma_bf16(TZ2, umma::desc_kmajor(sH1 + kPA(q) * H1_PLANE, P, kk),
-                         umma::desc_kmajor(sW2 + kPB(q) * W2_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
-      umma::commit(bar2);
-    }
-    ITC_STAMP(4);
-    prev = tile;
   }
-  if (prev >= 0) head(prev, (it + 2) % 3);
   if (a.truth) {
     const double s = block_sum(sse, red);
     if (tid == 0) atomicAdd(a.sse, s);
@@ -349,7 +383,7 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const char* es = getenv("APMG_INFER_STAMPS");
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
-  APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NT, itc::SMEM_BYTES, st, b, tab);
+  APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   return APMG_OK;
 }
 
