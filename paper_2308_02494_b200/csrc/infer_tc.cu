@@ -95,29 +95,6 @@ __device__ __forceinline__ int64_t voxel_of(const FwdArgs<float>& a, int64_t i) 
   return lattice_elem(a, x, y, z);
 }
 
-// bf16x3 split of a pair (packed cvt.rn.bf16x2.f32 and fp32x2 residuals), as 3 packed words
-__device__ __forceinline__ void split2_bf16x3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
-  const __nv_bfloat162 bh = __float22bfloat162_rn(make_float2(x0, x1));
-  const float2 r1 = __fadd2_rn(make_float2(x0, x1), make_float2(-__low2float(bh), -__high2float(bh)));
-  const __nv_bfloat162 bm = __float22bfloat162_rn(r1);
-  const float2 r2 = __fadd2_rn(r1, make_float2(-__low2float(bm), -__high2float(bm)));
-  const __nv_bfloat162 bl = __float22bfloat162_rn(r2);
-  h = *reinterpret_cast<const uint32_t*>(&bh);
-  m = *reinterpret_cast<const uint32_t*>(&bm);
-  l = *reinterpret_cast<const uint32_t*>(&bl);
-}
-
-// write 8 consecutive columns (one 16-B chunk per plane) of row r of a bf16x3 CM buffer
-__device__ __forceinline__ void store_chunk3(unsigned char* buf, uint32_t plane, int r, int c0, int R, const float* v) {
-  uint32_t h[4], m[4], l[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) split2_bf16x3(v[2 * e], v[2 * e + 1], h[e], m[e], l[e]);
-  const uint32_t o = umma::cm16_offset(r, c0, R);
-  *reinterpret_cast<uint4*>(buf + o) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(buf + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
-  *reinterpret_cast<uint4*>(buf + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
 __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const float* __restrict__ tab) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const ModelDev<float>& md = a.md;
@@ -141,11 +118,11 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   // weights: rows = output unit, 8-column chunks
   for (int e = tid; e < 64 * 16; e += NTA) {
     const int r = e >> 4, c0 = (e & 15) * 8;
-    store_chunk3(W1, W1_PLANE, r, c0, 64, md.w1 + r * FE + c0);
+    umma::store_chunk3(W1, W1_PLANE, r, c0, 64, md.w1 + r * FE + c0);
   }
   for (int e = tid; e < 64 * 8; e += NTA) {
     const int r = e >> 3, c0 = (e & 7) * 8;
-    store_chunk3(W2, W2_PLANE, r, c0, 64, md.w2 + r * HID + c0);
+    umma::store_chunk3(W2, W2_PLANE, r, c0, 64, md.w2 + r * HID + c0);
   }
   if (tid < HID) sW3[tid] = md.w3[tid];
   float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
@@ -305,7 +282,7 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
             fv[2 * g] = f0;
             fv[2 * g + 1] = f1;
           }
-          store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
+          umma::store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
         }
       }
       umma::fence_async_smem();
@@ -329,8 +306,8 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
         umma::tmem_ld16(TZ1 + lane_base + ep_col0, v);
   #pragma unroll
         for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
-        store_chunk3(H1, H1_PLANE, ep_row, ep_col0, P, v);
-        store_chunk3(H1, H1_PLANE, ep_row, ep_col0 + 8, P, v + 8);
+        umma::store_chunk3(H1, H1_PLANE, ep_row, ep_col0, P, v);
+        umma::store_chunk3(H1, H1_PLANE, ep_row, ep_col0 + 8, P, v + 8);
       }
       umma::fence_async_smem();
       umma::fence_before_sync();

@@ -410,7 +410,12 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
   if constexpr (sizeof(T) == 4) {
     if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
       grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms())));
-      rc = launch_recon_tc(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
+      // default: bf16x3 all-tcgen05 kernel; APMG_RECON16=0 selects the tf32 / mma.sync one (A/B)
+      const char* e16 = getenv("APMG_RECON16");
+      if (!(e16 && e16[0] == '0'))
+        rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
+      else
+        rc = launch_recon_tc(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
       if (rc) return rc;
       done = true;
     }

@@ -1,0 +1,477 @@
+// Fused reconstruction step (optim.py:102-155) for the flagship shape (float32, 64 grids x
+// 2 channels -> 128 features, 64 hidden), every product on the 5th-gen tensor core with
+// bf16x3 operands (x = h + m + l, 8+8+8 significant bits; tcgen05.mma kind::f16, f32
+// accumulate).  16-bit operands are accepted K-major and MN-major from the same CM buffer,
+// so the transposed products of the backward read the forward's buffers directly.
+//
+// One persistent CTA (16 warps) per SM; a 64-point tile per loop iteration:
+//   encode      (point, grid) pairs -> features F (bf16x3), cell terms cached in TMEM
+//   z1 = F W1^T                         M=64 N=64  K=128, 6 products (f32-level accuracy)
+//   h1 = relu(z1) -> bf16x3, sign bitmap
+//   z2 = h1 W2^T                        M=64 N=64  K=64, 6 products
+//   head/loss, g = dL/dout, dz2 = [z2>0] g w3 -> bf16x3
+//   dz1 = dz2 W2      (B = W2 MN-major) M=64 N=64  K=64, 3 products (hh, hm, mh)
+//   dW2 += dz2^T h1   (A, B MN-major)   M=64 N=64  K=64, 3 products, TMEM-resident sum
+//   dz1 *= [h1 > 0] -> bf16x3
+//   gF = dz1 W1       (B = W1 MN-major) M=64 N=128 K=64, 3 products
+//   dW1 += dz1^T F    (A, B MN-major)   M=64 N=128 K=64, 3 products, TMEM-resident sum
+//   scatter     gF -> channel-last grid gradients (warp-aggregated float2 RED), interleaved
+//               with the encode of the next tile
+// The backward products keep ~2^-16 relative accuracy per term (gradient gate 1e-3); the
+// forward keeps the f32-level 6-product split (forward / loss gates).
+//
+// Shared memory (~199 KB): W1 | W2 | F | h1 | dz2 | dz1 (bf16x3, 16-bit CM layout) | small;
+// gF (f32, swizzled) reuses [h1 | dz2] once dW2 / dz1 have consumed them.  Tensor memory:
+// acc A (z1, then dz1) | acc B (z2) -- gF spans both -- | dW1 | dW2 | per-thread cell cache.
+#include "kernels.cuh"
+#include "umma.cuh"
+
+namespace apmg {
+namespace tc16 {
+
+constexpr int P = 64;
+constexpr int NW = 16;
+constexpr int NT = 32 * NW;
+constexpr int WQ = NW / 4;
+constexpr int EPC = 64 / WQ;  // 16
+constexpr int GPW = 64 / NW;  // 4
+constexpr int FE = 128;
+constexpr int HID = 64;
+
+constexpr uint32_t PL64x128 = 64 * 128 * 2, PL64x64 = 64 * 64 * 2;
+constexpr uint32_t OFF_W1 = 0;                          // [64 i][128 k] x3
+constexpr uint32_t OFF_W2 = OFF_W1 + 3 * PL64x128;      // [64 j][64 i] x3
+constexpr uint32_t OFF_F = OFF_W2 + 3 * PL64x64;        // [64 p][128 k] x3
+constexpr uint32_t OFF_H1 = OFF_F + 3 * PL64x128;       // [64 p][64 i] x3
+constexpr uint32_t OFF_DZ2 = OFF_H1 + 3 * PL64x64;      // [64 p][64 j] x3
+constexpr uint32_t OFF_DZ1 = OFF_DZ2 + 3 * PL64x64;     // [64 p][64 i] x3
+constexpr uint32_t OFF_GF = OFF_H1;                     // f32 [64][128] (32 KB) over h1 | dz2
+constexpr uint32_t OFF_X = OFF_DZ1 + 3 * PL64x64;       // [2][P][3]
+constexpr uint32_t OFF_T = OFF_X + 2 * P * 3 * 4;       // [2][P]
+constexpr uint32_t OFF_G = OFF_T + 2 * P * 4;           // [P]
+constexpr uint32_t OFF_HEAD = OFF_G + P * 4;            // [WQ][P]
+constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [64]
+constexpr uint32_t OFF_RED = OFF_DW3 + HID * 4;         // [32] doubles
+constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
+constexpr uint32_t OFF_TM = OFF_BAR + 8;
+constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
+constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
+constexpr uint32_t OFF_M1 = OFF_W3 + 64 * 4;            // [64 i][4] u16: bit p%16 of word p/16 = [h1 > 0]
+constexpr uint32_t SMEM_BYTES = OFF_M1 + 64 * 4 * 2;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+static_assert(P * FE * 4 <= 6 * PL64x64, "gF buffer fits over h1 | dz2");
+
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t TC_A = 0, TC_B = 64, TC_DW1 = 128, TC_DW2 = 256, TC_CACHE = 320;
+
+// bf16x3 product q: (A plane, B plane) = hh, hm, mh, hl, lh, mm
+__host__ __device__ constexpr int kPA(int q) { return q == 2 ? 1 : (q == 4 ? 2 : (q == 5 ? 1 : 0)); }
+__host__ __device__ constexpr int kPB(int q) { return q == 1 ? 1 : (q == 3 ? 2 : (q == 5 ? 1 : 0)); }
+
+__device__ __forceinline__ int gf_idx(int p, int k) { return p * 128 + (k ^ ((p & 15) << 1)); }
+
+struct Args {
+  ModelDev<float> md;
+  int64_t n;
+  const float* coords;
+  const float* targets;
+  float* sq;
+  float* dgrid;
+  float* part_dw;
+  double* part_loss;
+  const TrainCtl* ctl;
+  int aggregate;
+};
+
+__device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX, float* sT, int tid) {
+  if (tid < P) {
+    const int64_t i = tile * P + tid;
+    const bool ok = i < a.n;
+    sX[3 * tid] = ok ? a.coords[3 * i] : 0.f;
+    sX[3 * tid + 1] = ok ? a.coords[3 * i + 1] : 0.f;
+    sX[3 * tid + 2] = ok ? a.coords[3 * i + 2] : 0.f;
+    sT[tid] = ok ? a.targets[i] : 0.f;
+  }
+}
+
+// scatter of one (2 grids x 2 points) group (see recon_tc.cu)
+__device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const Args& a, const float* GF,
+                                              uint32_t tmem_cache, int jq, int cnt, int warp, int lane) {
+  uint32_t cache[16];
+  umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = 2 * jq + (u >> 1), h = u & 1;
+    const int m = warp + NW * j, p = lane + 32 * h;
+    const int vbase = int(cache[4 * u]);
+    const bool valid = vbase >= 0 && p < cnt;
+    float2 g = make_float2(0.f, 0.f);
+    if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
+    if (a.aggregate)
+      scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+                              __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+    else if (valid)
+      scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
+                         __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  if (a.ctl && a.ctl->skip) return;
+  const ModelDev<float>& md = a.md;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int quarter = warp & 3, wq = warp >> 2;
+  unsigned char* W1 = sm + OFF_W1;
+  unsigned char* W2 = sm + OFF_W2;
+  unsigned char* F = sm + OFF_F;
+  unsigned char* H1 = sm + OFF_H1;
+  unsigned char* DZ2 = sm + OFF_DZ2;
+  unsigned char* DZ1 = sm + OFF_DZ1;
+  float* GF = reinterpret_cast<float*>(sm + OFF_GF);
+  float* sX = reinterpret_cast<float*>(sm + OFF_X);
+  float* sT = reinterpret_cast<float*>(sm + OFF_T);
+  float* sG = reinterpret_cast<float*>(sm + OFF_G);
+  float* sHead = reinterpret_cast<float*>(sm + OFF_HEAD);
+  float* sDW3 = reinterpret_cast<float*>(sm + OFF_DW3);
+  double* red = reinterpret_cast<double*>(sm + OFF_RED);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
+  float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
+  float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
+  uint16_t* sM1 = reinterpret_cast<uint16_t*>(sm + OFF_M1);
+
+  // ---- stage weights (bf16x3, rows = output unit) ----
+  for (int e = tid; e < 64 * 16; e += NT) {
+    const int r = e >> 4, c0 = (e & 15) * 8;
+    umma::store_chunk3(W1, PL64x128, r, c0, 64, md.w1 + r * FE + c0);
+  }
+  for (int e = tid; e < 64 * 8; e += NT) {
+    const int r = e >> 3, c0 = (e & 7) * 8;
+    umma::store_chunk3(W2, PL64x64, r, c0, 64, md.w2 + r * HID + c0);
+  }
+  if (tid < HID) sDW3[tid] = 0.f;
+  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  if (tid < HID) sW3[tid] = md.w3[tid];
+  if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
+  if (tid == 0) {
+    umma::mbar_init(bar, 1);
+    umma::fence_mbar_init();
+  }
+  const int64_t tiles = ceil_div(a.n, P);
+  load_tile(a, blockIdx.x, sX, sT, tid);
+  umma::fence_async_smem();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_slot;
+  const uint32_t lane_base = uint32_t(32 * quarter) << 16;
+  const uint32_t TA = tmem + TC_A, TB = tmem + TC_B, TDW1 = tmem + TC_DW1, TDW2 = tmem + TC_DW2;
+  const uint32_t tmem_cache = tmem + TC_CACHE + 8 * GPW * wq + lane_base;
+  // zero the TMEM-resident weight-gradient sums (warps 0-3 cover the four lane quarters)
+  if (warp < 4) {
+    uint32_t z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll 1
+    for (int c = 0; c < 192; c += 16) umma::tmem_st16(tmem + lane_base + TC_DW1 + c, z);
+    umma::tmem_st_wait();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+
+  const uint32_t sW1 = umma::smem_u32(W1), sW2 = umma::smem_u32(W2), sF = umma::smem_u32(F),
+                 sH1 = umma::smem_u32(H1), sDZ2 = umma::smem_u32(DZ2), sDZ1 = umma::smem_u32(DZ1);
+  const uint32_t id_kk = umma::idesc_bf16(64, 64, false, false);      // A, B K-major
+  const uint32_t id_kmn = umma::idesc_bf16(64, 64, false, true);      // B MN-major
+  const uint32_t id_kmn128 = umma::idesc_bf16(64, 128, false, true);  // B MN-major, N=128
+  const uint32_t id_mm = umma::idesc_bf16(64, 64, true, true);        // A, B MN-major
+  const uint32_t id_mm128 = umma::idesc_bf16(64, 128, true, true);
+  const float coef = __fmul_rn(float(2.0 / double(a.n)), md.span);
+
+  float dw3_acc[EPC];
+#pragma unroll
+  for (int c = 0; c < EPC; ++c) dw3_acc[c] = 0.f;
+  double loss = 0.0;
+  uint32_t phase = 0;
+  const int ep_row = 16 * quarter + lane;  // M=64 accumulator rows (lane < 16)
+  const int ep_col0 = EPC * wq;
+
+  auto encode_group = [&](const float* cX, int jq) {
+    const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
+                            {cX[3 * (lane + 32)], cX[3 * (lane + 32) + 1], cX[3 * (lane + 32) + 2]}};
+    uint32_t cache[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 2 * jq + (u >> 1), h = u & 1;
+      const int m = warp + NW * j, p = lane + 32 * h;
+      const float* tf = sTF + 12 * m;
+      const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
+      const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
+      const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
+      const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
+      int ix, iy, iz;
+      double fxd, fyd, fzd;
+      axis_term(l0, md.W, ix, fxd);
+      axis_term(l1, md.H, iy, fyd);
+      axis_term(l2, md.D, iz, fzd);
+      const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
+      const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
+      float f0 = 0.f, f1 = 0.f;
+      if (inside) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+      cache[4 * u] = uint32_t(vbase);
+      cache[4 * u + 1] = __float_as_uint(fx);
+      cache[4 * u + 2] = __float_as_uint(fy);
+      cache[4 * u + 3] = __float_as_uint(fz);
+      uint32_t hw, mw, lw;
+      umma::split2_bf16x3(f0, f1, hw, mw, lw);
+      const uint32_t o = umma::cm16_offset(p, 2 * m, 64);
+      *reinterpret_cast<uint32_t*>(F + o) = hw;
+      *reinterpret_cast<uint32_t*>(F + PL64x128 + o) = mw;
+      *reinterpret_cast<uint32_t*>(F + 2 * PL64x128 + o) = lw;
+    }
+    umma::tmem_st16(tmem_cache + 16 * jq, cache);
+  };
+  // z1 = F W1^T over K-steps [k0, k1) (K = 16 each), committed when `last`
+  auto issue_z1 = [&](int k0, int k1, bool last) {
+    if (tid != 0) return;
+    umma::fence_after_sync();
+    for (int kk = k0; kk < k1; ++kk)
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        umma::mma_bf16(TA, umma::desc_kmajor(sF + kPA(q) * PL64x128, 64, kk),
+                       umma::desc_kmajor(sW1 + kPB(q) * PL64x128, 64, kk), id_kk, (kk | q) ? 1u : 0u);
+    if (last) umma::commit(bar);
+  };
+  auto encode_tile = [&](const float* cX, int scatter_cnt, int64_t prefetch_tile, int prefetch_slot) {
+#pragma unroll 1
+    for (int jq = 0; jq < GPW / 2; ++jq) {
+      if (scatter_cnt >= 0) scatter_group(md, a, GF, tmem_cache, jq, scatter_cnt, warp, lane);
+      encode_group(cX, jq);
+      if (jq == 0) {  // features k < 64 (grids 0-31) complete: first half of z1
+        umma::fence_async_smem();
+        __syncthreads();
+        issue_z1(0, FE / 32, false);
+      }
+    }
+    umma::tmem_st_wait();
+    if (prefetch_tile < tiles)
+      load_tile(a, prefetch_tile, sX + (prefetch_slot & 1) * 3 * P, sT + (prefetch_slot & 1) * P, tid);
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();  // F complete; every warp's scatter of the previous tile has read gF
+    issue_z1(FE / 32, FE / 16, true);
+  };
+
+  int it = 0;
+  if (int64_t(blockIdx.x) < tiles) encode_tile(sX, -1, int64_t(blockIdx.x) + gridDim.x, 1);
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int cnt = int(min64(P, a.n - tile * P));
+    const float* cT = sT + (it & 1) * P;
+    umma::mbar_wait(bar, phase);
+    phase ^= 1;
+    umma::fence_after_sync();
+    // ---- epilogue 1: h1 = relu(z1) -> bf16x3; sign bitmap ----
+    {
+      float v[EPC];
+      umma::tmem_ld16(TA + lane_base + ep_col0, v);
+#pragma unroll
+      for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
+      if (lane < 16) {
+        umma::store_chunk3(H1, PL64x64, ep_row, ep_col0, 64, v);
+        umma::store_chunk3(H1, PL64x64, ep_row, ep_col0 + 8, 64, v + 8);
+      }
+#pragma unroll
+      for (int c = 0; c < EPC; ++c) {
+        const unsigned b = __ballot_sync(0xffffffffu, lane < 16 && v[c] > 0.f);
+        if (lane == 0) sM1[(ep_col0 + c) * 4 + quarter] = uint16_t(b & 0xffffu);
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    // ---- z2 = h1 W2^T ----
+    if (tid == 0) {
+      for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          umma::mma_bf16(TB, umma::desc_kmajor(sH1 + kPA(q) * PL64x64, 64, kk),
+                         umma::desc_kmajor(sW2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
+      umma::commit(bar);
+    }
+    umma::mbar_wait(bar, phase);
+    phase ^= 1;
+    umma::fence_after_sync();
+    // ---- epilogue 2: h2, head, loss, g, dz2 = [z2 > 0] g w3, dW3 ----
+    float h2v[EPC];
+    umma::tmem_ld16(TB + lane_base + ep_col0, h2v);
+    if (lane < 16) {
+      float part = 0.f;
+#pragma unroll
+      for (int c = 0; c < EPC; ++c) {
+        h2v[c] = fmaxf(h2v[c], 0.f);
+        part = fmaf(h2v[c], sW3[ep_col0 + c], part);
+      }
+      sHead[wq * P + ep_row] = part;
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (tid < P) {
+      float g = 0.f;
+      if (tid < cnt) {
+        float raw = sHead[tid];
+#pragma unroll
+        for (int q = 1; q < WQ; ++q) raw += sHead[q * P + tid];
+        const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
+        const float r = __fsub_rn(y, cT[tid]);
+        const float s = __fmul_rn(r, r);
+        a.sq[tile * P + tid] = s;
+        loss += double(s);
+        g = __fmul_rn(r, coef);
+      }
+      sG[tid] = g;
+    }
+    __syncthreads();
+    if (lane < 16) {
+      const float g = sG[ep_row];
+      float d[EPC];
+#pragma unroll
+      for (int c = 0; c < EPC; ++c) {
+        dw3_acc[c] = fmaf(g, h2v[c], dw3_acc[c]);
+        d[c] = h2v[c] > 0.f ? __fmul_rn(g, sW3[ep_col0 + c]) : 0.f;  // g_z2 (optim.py:143-145)
+      }
+      umma::store_chunk3(DZ2, PL64x64, ep_row, ep_col0, 64, d);
+      umma::store_chunk3(DZ2, PL64x64, ep_row, ep_col0 + 8, 64, d + 8);
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    // ---- dz1 = dz2 W2 (-> acc A), dW2 += dz2^T h1 (-> TMEM sum) ----
+    if (tid == 0) {
+      for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          umma::mma_bf16(TA, umma::desc_kmajor(sDZ2 + kPA(q) * PL64x64, 64, kk),
+                         umma::desc_mnmajor16(sW2 + kPB(q) * PL64x64, 64, kk), id_kmn, (kk | q) ? 1u : 0u);
+      for (int kk = 0; kk < P / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          umma::mma_bf16(TDW2, umma::desc_mnmajor16(sDZ2 + kPA(q) * PL64x64, 64, kk),
+                         umma::desc_mnmajor16(sH1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
+      umma::commit(bar);
+    }
+    umma::mbar_wait(bar, phase);
+    phase ^= 1;
+    umma::fence_after_sync();
+    // ---- dz1 *= [h1 > 0] -> bf16x3 ----
+    {
+      float v[EPC];
+      umma::tmem_ld16(TA + lane_base + ep_col0, v);
+      if (lane < 16) {
+        const int p = ep_row;
+#pragma unroll
+        for (int c = 0; c < EPC; ++c) {
+          const int i = ep_col0 + c;
+          if (!((sM1[i * 4 + (p >> 4)] >> (p & 15)) & 1u)) v[c] = 0.f;
+        }
+        umma::store_chunk3(DZ1, PL64x64, p, ep_col0, 64, v);
+        umma::store_chunk3(DZ1, PL64x64, p, ep_col0 + 8, 64, v + 8);
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    // ---- gF = dz1 W1 (-> acc A|B, N=128), dW1 += dz1^T F (-> TMEM sum) ----
+    if (tid == 0) {
+      for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          umma::mma_bf16(TA, umma::desc_kmajor(sDZ1 + kPA(q) * PL64x64, 64, kk),
+                         umma::desc_mnmajor16(sW1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
+      for (int kk = 0; kk < P / 16; ++kk)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          umma::mma_bf16(TDW1, umma::desc_mnmajor16(sDZ1 + kPA(q) * PL64x64, 64, kk),
+                         umma::desc_mnmajor16(sF + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
+      umma::commit(bar);
+    }
+    umma::mbar_wait(bar, phase);
+    phase ^= 1;
+    umma::fence_after_sync();
+    umma::fence_before_sync();
+    __syncthreads();  // h1 / dz2 consumed (dW2, dz1 done) before gF overwrites them
+    umma::fence_after_sync();
+    // ---- gF epilogue: rows p (lanes < 16), 32 columns per warp -> gF[p][k] ----
+    {
+      float v[32];
+      umma::tmem_ld16(TA + lane_base + 2 * ep_col0, v);
+      umma::tmem_ld16(TA + lane_base + 2 * ep_col0 + 16, v + 16);
+      if (lane < 16) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 2)
+          *reinterpret_cast<float2*>(GF + gf_idx(ep_row, 2 * ep_col0 + c)) = make_float2(v[c], v[c + 1]);
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    // ---- scatter of this tile, interleaved with the encode of the next one ----
+    const int64_t next = tile + gridDim.x;
+    if (next < tiles) {
+      encode_tile(sX + ((it + 1) & 1) * 3 * P, cnt, next + gridDim.x, it + 2);
+    } else {
+#pragma unroll 1
+      for (int jq = 0; jq < GPW / 2; ++jq) scatter_group(md, a, GF, tmem_cache, jq, cnt, warp, lane);
+    }
+  }
+
+  // ---- flush per-CTA partials: [dW1 (64x128) | dW2 (64x64) | dW3 (64)] from TMEM ----
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  float* dst = a.part_dw + int64_t(blockIdx.x) * (HID * FE + HID * HID + HID);
+  {
+    // M=64 accumulators: row 16q + t in lane 32q + t (t < 16); each warp 32 dW1 columns,
+    // 16 dW2 columns
+    float v[32];
+    umma::tmem_ld16(TDW1 + lane_base + 2 * ep_col0, v);
+    umma::tmem_ld16(TDW1 + lane_base + 2 * ep_col0 + 16, v + 16);
+    if (lane < 16)
+      for (int c = 0; c < 32; ++c) dst[ep_row * FE + 2 * ep_col0 + c] = v[c];
+    umma::tmem_ld16(TDW2 + lane_base + ep_col0, v);
+    if (lane < 16)
+      for (int c = 0; c < 16; ++c) dst[HID * FE + ep_row * HID + ep_col0 + c] = v[c];
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int c = 0; c < EPC; ++c) atomicAdd(&sDW3[ep_col0 + c], dw3_acc[c]);
+  }
+  const double bl = block_sum(loss, red);  // contains __syncthreads
+  if (tid < HID) dst[HID * FE + HID * HID + tid] = sDW3[tid];
+  if (tid == 0) a.part_loss[blockIdx.x] = bl;
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+}  // namespace tc16
+
+int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
+                      float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl,
+                      cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    APMG_CUDA_TRY(cudaFuncSetAttribute(tc16::k_recon_tc16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(tc16::SMEM_BYTES)));
+    attr = true;
+  }
+  const char* ea = getenv("APMG_SCATTER_AGG");
+  tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1};
+  APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
+  return APMG_OK;
+}
+
+}  // namespace apmg

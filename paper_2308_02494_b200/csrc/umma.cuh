@@ -126,6 +126,29 @@ __device__ __forceinline__ void split_bf16x3(float x, __nv_bfloat16& h, __nv_bfl
   l = __float2bfloat16_rn(r1 - __bfloat162float(m));
 }
 
+// bf16x3 split of a pair (packed cvt.rn.bf16x2.f32 and fp32x2 residuals), as 3 packed words
+__device__ __forceinline__ void split2_bf16x3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+  const __nv_bfloat162 bh = __float22bfloat162_rn(make_float2(x0, x1));
+  const float2 r1 = __fadd2_rn(make_float2(x0, x1), make_float2(-__low2float(bh), -__high2float(bh)));
+  const __nv_bfloat162 bm = __float22bfloat162_rn(r1);
+  const float2 r2 = __fadd2_rn(r1, make_float2(-__low2float(bm), -__high2float(bm)));
+  const __nv_bfloat162 bl = __float22bfloat162_rn(r2);
+  h = *reinterpret_cast<const uint32_t*>(&bh);
+  m = *reinterpret_cast<const uint32_t*>(&bm);
+  l = *reinterpret_cast<const uint32_t*>(&bl);
+}
+
+// write 8 consecutive columns (one 16-B chunk per plane) of row r of a bf16x3 CM buffer
+__device__ __forceinline__ void store_chunk3(unsigned char* buf, uint32_t plane, int r, int c0, int R, const float* v) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) split2_bf16x3(v[2 * e], v[2 * e + 1], h[e], m[e], l[e]);
+  const uint32_t o = umma::cm16_offset(r, c0, R);
+  *reinterpret_cast<uint4*>(buf + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(buf + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
+  *reinterpret_cast<uint4*>(buf + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 __device__ __forceinline__ void commit(uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
                : "memory");
