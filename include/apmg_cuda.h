@@ -209,6 +209,8 @@ int apmg_debug_umma_bf16(int32_t mode, int32_t M, int32_t K, int32_t N, int32_t 
 int apmg_debug_tc_phases(long long* out);
 /* same for the tensor-core lattice sweep: [16 tiles][8 phases] (APMG_INFER_STAMPS=1) */
 int apmg_debug_infer_phases(long long* out);
+/* same for the bf16x3 recon kernel: [16 tiles][12 phases] (APMG_TC_STAMPS=1) */
+int apmg_debug_tc16_phases(long long* out);
 /* roofline peak probes (csrc/peaks.cu, tools/peaks.py): kind 0 L2 float2 gather, 1 L2 float2
  * RED, 2 FP32 FFMA, 3 FP64 DFMA, 4 tcgen05 kind::tf32, 5 warp shuffles; `table` is a device
  * buffer of table_bytes (power of two) for kinds 0-1 (a sink otherwise); *work receives the

@@ -94,6 +94,7 @@ SIGNATURES = {
     "apmg_debug_tc_phases": (C.c_int, [_P]),
     "apmg_debug_umma_bf16": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "apmg_debug_infer_phases": (C.c_int, [_P]),
+    "apmg_debug_tc16_phases": (C.c_int, [_P]),
     "apmg_peak_probe": (C.c_int, [_I32, _P, _I64, _I32, _P, _P]),
 }
 

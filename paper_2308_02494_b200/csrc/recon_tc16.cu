@@ -68,6 +68,13 @@ constexpr uint32_t TC_A = 0, TC_B = 64, TC_DW1 = 128, TC_DW2 = 256, TC_CACHE = 3
 __host__ __device__ constexpr int kPA(int q) { return q == 2 ? 1 : (q == 4 ? 2 : (q == 5 ? 1 : 0)); }
 __host__ __device__ constexpr int kPB(int q) { return q == 1 ? 1 : (q == 3 ? 2 : (q == 5 ? 1 : 0)); }
 
+// per-phase clock stamps of CTA 0 / thread 0 for the first 16 tiles (APMG_TC_STAMPS=1)
+__device__ long long g_tc16_stamp[16][12];
+#define TC16_STAMP(k)                                                                   \
+  do {                                                                                  \
+    if (a.stamps && blockIdx.x == 0 && tid == 0 && it < 16) g_tc16_stamp[it][k] = clock64(); \
+  } while (0)
+
 __device__ __forceinline__ int gf_idx(int p, int k) { return p * 128 + (k ^ ((p & 15) << 1)); }
 
 struct Args {
@@ -81,6 +88,7 @@ struct Args {
   double* part_loss;
   const TrainCtl* ctl;
   int aggregate;
+  int stamps;
 };
 
 __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX, float* sT, int tid) {
@@ -269,9 +277,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     const int cnt = int(min64(P, a.n - tile * P));
     const float* cT = sT + (it & 1) * P;
+    TC16_STAMP(0);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
+    TC16_STAMP(1);
     // ---- epilogue 1: h1 = relu(z1) -> bf16x3; sign bitmap ----
     {
       float v[EPC];
@@ -292,6 +302,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC16_STAMP(2);
     // ---- z2 = h1 W2^T ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 16; ++kk)
@@ -304,6 +315,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
+    TC16_STAMP(3);
     // ---- epilogue 2: h2, head, loss, g, dz2 = [z2 > 0] g w3, dW3 ----
     float h2v[EPC];
     umma::tmem_ld16(TB + lane_base + ep_col0, h2v);
@@ -349,6 +361,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC16_STAMP(4);
     // ---- dz1 = dz2 W2 (-> acc A), dW2 += dz2^T h1 (-> TMEM sum) ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 16; ++kk)
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
+    TC16_STAMP(5);
     // ---- dz1 *= [h1 > 0] -> bf16x3 ----
     {
       float v[EPC];
@@ -385,6 +399,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
+    TC16_STAMP(6);
     // ---- gF = dz1 W1 (-> acc A|B, N=128), dW1 += dz1^T F (-> TMEM sum) ----
     if (tid == 0) {
       for (int kk = 0; kk < HID / 16; ++kk)
@@ -405,6 +420,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_before_sync();
     __syncthreads();  // h1 / dz2 consumed (dW2, dz1 done) before gF overwrites them
     umma::fence_after_sync();
+    TC16_STAMP(7);
     // ---- gF epilogue: rows p (lanes < 16), 32 columns per warp -> gF[p][k] ----
     {
       float v[32];
@@ -418,6 +434,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     }
     umma::fence_before_sync();
     __syncthreads();
+    TC16_STAMP(8);
     // ---- scatter of this tile, interleaved with the encode of the next one ----
     const int64_t next = tile + gridDim.x;
     if (next < tiles) {
@@ -459,6 +476,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
 
 }  // namespace tc16
 
+extern "C" int apmg_debug_tc16_phases(long long* out) {
+  APMG_CUDA_TRY(cudaMemcpyFromSymbol(out, tc16::g_tc16_stamp, sizeof(tc16::g_tc16_stamp)));
+  return APMG_OK;
+}
+
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl,
                       cudaStream_t st) {
@@ -469,7 +491,9 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
     attr = true;
   }
   const char* ea = getenv("APMG_SCATTER_AGG");
-  tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1};
+  const char* es = getenv("APMG_TC_STAMPS");
+  tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1,
+               (es && es[0] == '1') ? 1 : 0};
   APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
   return APMG_OK;
 }
