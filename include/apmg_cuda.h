@@ -184,7 +184,9 @@ size_t apmg_train_workspace_bytes(const apmg_model* m, const apmg_train_config* 
 /* Parameters are updated in place: grad-free main group `main_params` laid out
  * [grids_cl | w1 | w2 | w3] and `transforms` [M][4][4] (both dtype, device).
  * bias_table: HOST f64 [iterations][2] = (1-0.9^t, 1-0.99^t) for t = 1..iterations
- * computed in Python so Adam's bias corrections match the reference bit for bit. */
+ * computed in Python so Adam's bias corrections match the reference bit for bit.
+ * The state keeps a private 8x8x8-bricked copy of `volume` (cudaMalloc, freed by
+ * apmg_train_destroy; APMG_BRICKED=0 samples the caller's [D][H][W] array instead). */
 int apmg_train_create(apmg_train_state** out, const apmg_model* shape, void* main_params, void* transforms,
                       const float* volume, int32_t w, int32_t h, int32_t d, const apmg_train_config* cfg,
                       const double* bias_table, void* workspace, size_t workspace_bytes, void* stream);

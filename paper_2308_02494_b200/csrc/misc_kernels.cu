@@ -232,6 +232,54 @@ __global__ void k_sample_sorted(const double* __restrict__ c64, int64_t n, const
   }
 }
 
+// ---- 8x8x8-bricked copy of the training volume: a trilinear footprint (2x2x2 voxels)
+// falls in one 2 KB brick for (7/8)^3 of the points, so the sorted sampler touches ~2 DRAM
+// granules per point instead of ~6 with [D][H][W] rows (values and arithmetic unchanged)
+__device__ __forceinline__ int64_t brick_off(int x, int y, int z, int nbx, int nby) {
+  return ((int64_t(z >> 3) * nby + (y >> 3)) * nbx + (x >> 3)) * 512 + ((z & 7) << 6) + ((y & 7) << 3) + (x & 7);
+}
+
+__global__ void k_brick_volume(const float* __restrict__ vol, int w, int h, int d, int nbx, int nby,
+                               float* __restrict__ out) {
+  const int64_t n = int64_t(w) * h * d;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int x = int(i % w);
+    const int64_t r = i / w;
+    const int y = int(r % h), z = int(r / h);
+    out[brick_off(x, y, z, nbx, nby)] = vol[i];
+  }
+}
+
+template <typename T>
+__global__ void k_sample_sorted_bricked(const double* __restrict__ c64, int64_t n, const float* __restrict__ bricks,
+                                        int w, int h, int d, int nbx, int nby, T* __restrict__ coords,
+                                        T* __restrict__ targets, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double c0 = c64[3 * i], c1 = c64[3 * i + 1], c2 = c64[3 * i + 2];
+    const VolAxis ax = vol_axis(c0, w), ay = vol_axis(c1, h), az = vol_axis(c2, d);
+    const int x0 = ax.i0, x1 = ax.i0 + ax.step, y0 = ay.i0, y1 = ay.i0 + ay.step, z0 = az.i0, z1 = az.i0 + az.step;
+    const double c000 = __ldg(bricks + brick_off(x0, y0, z0, nbx, nby));
+    const double c001 = __ldg(bricks + brick_off(x1, y0, z0, nbx, nby));
+    const double c010 = __ldg(bricks + brick_off(x0, y1, z0, nbx, nby));
+    const double c011 = __ldg(bricks + brick_off(x1, y1, z0, nbx, nby));
+    const double c100 = __ldg(bricks + brick_off(x0, y0, z1, nbx, nby));
+    const double c101 = __ldg(bricks + brick_off(x1, y0, z1, nbx, nby));
+    const double c110 = __ldg(bricks + brick_off(x0, y1, z1, nbx, nby));
+    const double c111 = __ldg(bricks + brick_off(x1, y1, z1, nbx, nby));
+    const double x00 = lerp_d(c000, c001, ax.f), x10 = lerp_d(c010, c011, ax.f);
+    const double x01 = lerp_d(c100, c101, ax.f), x11 = lerp_d(c110, c111, ax.f);
+    targets[i] = T(__double2float_rn(lerp_d(lerp_d(x00, x10, ay.f), lerp_d(x01, x11, ay.f), az.f)));
+    coords[3 * i] = T(__double2float_rn(c0));
+    coords[3 * i + 1] = T(__double2float_rn(c1));
+    coords[3 * i + 2] = T(__double2float_rn(c2));
+  }
+}
+
+template __global__ void k_sample_sorted_bricked<float>(const double*, int64_t, const float*, int, int, int, int, int,
+                                                        float*, float*, const TrainCtl*);
+template __global__ void k_sample_sorted_bricked<double>(const double*, int64_t, const float*, int, int, int, int,
+                                                         int, double*, double*, const TrainCtl*);
 template __global__ void k_sample_sorted<float>(const double*, int64_t, const float*, int, int, int, float*, float*,
                                                 const TrainCtl*);
 template __global__ void k_sample_sorted<double>(const double*, int64_t, const float*, int, int, int, double*, double*,

@@ -38,6 +38,12 @@ __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t*
 template <typename T>
 __global__ void k_sample_sorted(const double* __restrict__ c64, int64_t n, const float* __restrict__ vol, int w,
                                 int h, int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
+__global__ void k_brick_volume(const float* __restrict__ vol, int w, int h, int d, int nbx, int nby,
+                               float* __restrict__ out);
+template <typename T>
+__global__ void k_sample_sorted_bricked(const double* __restrict__ c64, int64_t n, const float* __restrict__ bricks,
+                                        int w, int h, int d, int nbx, int nby, T* __restrict__ coords,
+                                        T* __restrict__ targets, const TrainCtl* ctl);
 
 static bool sort_enabled() {
   const char* e = getenv("APMG_SORT");
@@ -135,6 +141,9 @@ struct apmg_train_state {
   // iteration sequence is identical every time: all state lives in TrainCtl)
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_launches = 0;
+  // 8x8x8-bricked copy of the volume for the sorted sampler (owned; APMG_BRICKED=0 disables)
+  float* vol_bricked = nullptr;
+  int nbx = 0, nby = 0;
 };
 
 constexpr int64_t kGraphIters = 8;
@@ -244,6 +253,23 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
     set_error("train workspace too small: need %zu have %zu", need, workspace_bytes);
     return APMG_E_WORKSPACE;
   }
+  {
+    const char* eb = getenv("APMG_BRICKED");
+    if (s->sort && !(eb && eb[0] == '0')) {
+      s->nbx = (w + 7) / 8;
+      s->nby = (h + 7) / 8;
+      const int nbz = (d + 7) / 8;
+      const size_t bytes = sizeof(float) * 512 * size_t(s->nbx) * s->nby * nbz;
+      if (cudaMalloc(&s->vol_bricked, bytes) != cudaSuccess) {
+        s->vol_bricked = nullptr;  // no room: sample the row-major volume
+        cudaGetLastError();
+      } else {
+        const int64_t nv = int64_t(w) * h * d;
+        const int g = int(std::min<int64_t>(ceil_div(nv, 256), int64_t(num_sms()) * 32));
+        APMG_LAUNCH("brick_volume", k_brick_volume, g, 256, 0, st, volume, w, h, d, s->nbx, s->nby, s->vol_bricked);
+      }
+    }
+  }
   CtlParams& P = s->P;
   P.iterations = cfg->iterations;
   P.delay_start = cfg->delay_start;
@@ -298,8 +324,13 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
     APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
     APMG_LAUNCH("bucket_scatter", k_bucket_scatter, elementwise_grid(B, 8), 256, 0, st, s->c64_raw, s->key, B,
                 s->counts, s->c64_sorted, s->ctl);
-    APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B, s->volume,
-                s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+    if (s->vol_bricked)
+      APMG_LAUNCH("train_batch", k_sample_sorted_bricked<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B,
+                  s->vol_bricked, s->w, s->h, s->d, s->nbx, s->nby, static_cast<T*>(s->coords),
+                  static_cast<T*>(s->targets), s->ctl);
+    else
+      APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B,
+                  s->volume, s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
   } else {
     APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
                 s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
@@ -411,6 +442,7 @@ extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_dens
 
 extern "C" int apmg_train_destroy(apmg_train_state* s) {
   if (s && s->graph) cudaGraphExecDestroy(s->graph);
+  if (s && s->vol_bricked) cudaFree(s->vol_bricked);
   delete s;
   return APMG_OK;
 }
