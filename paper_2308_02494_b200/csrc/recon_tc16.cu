@@ -56,7 +56,7 @@ constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
-constexpr uint32_t OFF_M1 = OFF_W3 + 64 * 4;            // [64 i][4] u16: bit p%16 of word p/16 = [h1 > 0]
+constexpr uint32_t OFF_M1 = OFF_W3 + 64 * 4;            // (spare)
 constexpr uint32_t SMEM_BYTES = OFF_M1 + 64 * 4 * 2;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 static_assert(P * FE * 4 <= 6 * PL64x64, "gF buffer fits over h1 | dz2");
@@ -75,7 +75,10 @@ __device__ long long g_tc16_stamp[16][12];
     if (a.stamps && blockIdx.x == 0 && tid == 0 && it < 16) g_tc16_stamp[it][k] = clock64(); \
   } while (0)
 
-__device__ __forceinline__ int gf_idx(int p, int k) { return p * 128 + (k ^ ((p & 15) << 1)); }
+// gF [P][128] f32, 8-byte granules XOR-swizzled by row: f(p) maps p & 15 onto the even
+// offsets 0..30 so both the row-per-lane float2 scatter reads (16 rows per half warp) and
+// the 16x256b epilogue writes (8 rows x 4 column pairs) spread over the banks
+__device__ __forceinline__ int gf_idx(int p, int k) { return p * 128 + (k ^ (8 * (p & 3) + 2 * ((p >> 2) & 3))); }
 
 struct Args {
   ModelDev<float> md;
@@ -147,7 +150,6 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
   float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
   float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
-  uint16_t* sM1 = reinterpret_cast<uint16_t*>(sm + OFF_M1);
 
   // ---- stage weights (bf16x3, rows = output unit) ----
   for (int e = tid; e < 64 * 16; e += NT) {
@@ -198,13 +200,16 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   const uint32_t id_mm128 = umma::idesc_bf16(64, 128, true, true);
   const float coef = __fmul_rn(float(2.0 / double(a.n)), md.span);
 
-  float dw3_acc[EPC];
+  // M=64 accumulators are read with the 16x256b shape: thread t owns rows p0 = 16q + t/4 and
+  // p1 = p0 + 8, columns ep_col0 + 8r + ec (+1) of each 8-column repetition r
+  const int ep_col0 = EPC * wq;
+  const int p0 = 16 * quarter + (lane >> 2), p1 = p0 + 8, ec = 2 * (lane & 3);
+  float dw3_acc[4];  // columns ep_col0 + 8r + ec + j, index 2r + j
 #pragma unroll
-  for (int c = 0; c < EPC; ++c) dw3_acc[c] = 0.f;
+  for (int c = 0; c < 4; ++c) dw3_acc[c] = 0.f;
   double loss = 0.0;
   uint32_t phase = 0;
-  const int ep_row = 16 * quarter + lane;  // M=64 accumulator rows (lane < 16)
-  const int ep_col0 = EPC * wq;
+  uint32_t h1pos = 0;  // [h1 > 0] bits of this thread's 8 elements (epilogue 1 -> dz1 epilogue)
 
   auto encode_group = [&](const float* cX, int jq) {
     const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
@@ -282,20 +287,20 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     phase ^= 1;
     umma::fence_after_sync();
     TC16_STAMP(1);
-    // ---- epilogue 1: h1 = relu(z1) -> bf16x3; sign bitmap ----
+    // ---- epilogue 1: h1 = relu(z1) -> bf16x3; sign bits kept in a register ----
     {
-      float v[EPC];
-      umma::tmem_ld16(TA + lane_base + ep_col0, v);
+      float v[8];
+      umma::tmem_ld_16x256b_x2(TA + lane_base + ep_col0, v);
+      h1pos = 0;
 #pragma unroll
-      for (int c = 0; c < EPC; ++c) v[c] = fmaxf(v[c], 0.f);
-      if (lane < 16) {
-        umma::store_chunk3(H1, PL64x64, ep_row, ep_col0, 64, v);
-        umma::store_chunk3(H1, PL64x64, ep_row, ep_col0 + 8, 64, v + 8);
+      for (int e = 0; e < 8; ++e) {
+        if (v[e] > 0.f) h1pos |= 1u << e;
+        v[e] = fmaxf(v[e], 0.f);
       }
 #pragma unroll
-      for (int c = 0; c < EPC; ++c) {
-        const unsigned b = __ballot_sync(0xffffffffu, lane < 16 && v[c] > 0.f);
-        if (lane == 0) sM1[(ep_col0 + c) * 4 + quarter] = uint16_t(b & 0xffffu);
+      for (int r = 0; r < 2; ++r) {
+        umma::store_pair3(H1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
+        umma::store_pair3(H1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
       }
     }
     umma::fence_async_smem();
@@ -317,16 +322,28 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_after_sync();
     TC16_STAMP(3);
     // ---- epilogue 2: h2, head, loss, g, dz2 = [z2 > 0] g w3, dW3 ----
-    float h2v[EPC];
-    umma::tmem_ld16(TB + lane_base + ep_col0, h2v);
-    if (lane < 16) {
-      float part = 0.f;
+    float h2v[8];
+    umma::tmem_ld_16x256b_x2(TB + lane_base + ep_col0, h2v);
+    {
+      float part0 = 0.f, part1 = 0.f;
 #pragma unroll
-      for (int c = 0; c < EPC; ++c) {
-        h2v[c] = fmaxf(h2v[c], 0.f);
-        part = fmaf(h2v[c], sW3[ep_col0 + c], part);
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float w = sW3[ep_col0 + 8 * r + ec + j];
+          h2v[4 * r + j] = fmaxf(h2v[4 * r + j], 0.f);
+          h2v[4 * r + 2 + j] = fmaxf(h2v[4 * r + 2 + j], 0.f);
+          part0 = fmaf(h2v[4 * r + j], w, part0);
+          part1 = fmaf(h2v[4 * r + 2 + j], w, part1);
+        }
+      part0 += __shfl_xor_sync(0xffffffffu, part0, 1);
+      part0 += __shfl_xor_sync(0xffffffffu, part0, 2);
+      part1 += __shfl_xor_sync(0xffffffffu, part1, 1);
+      part1 += __shfl_xor_sync(0xffffffffu, part1, 2);
+      if ((lane & 3) == 0) {
+        sHead[wq * P + p0] = part0;
+        sHead[wq * P + p1] = part1;
       }
-      sHead[wq * P + ep_row] = part;
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -346,16 +363,22 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       sG[tid] = g;
     }
     __syncthreads();
-    if (lane < 16) {
-      const float g = sG[ep_row];
-      float d[EPC];
+    {
+      const float g0 = sG[p0], g1 = sG[p1];
 #pragma unroll
-      for (int c = 0; c < EPC; ++c) {
-        dw3_acc[c] = fmaf(g, h2v[c], dw3_acc[c]);
-        d[c] = h2v[c] > 0.f ? __fmul_rn(g, sW3[ep_col0 + c]) : 0.f;  // g_z2 (optim.py:143-145)
+      for (int r = 0; r < 2; ++r) {
+        float d0[2], d1[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float w = sW3[ep_col0 + 8 * r + ec + j];
+          const float a0 = h2v[4 * r + j], a1 = h2v[4 * r + 2 + j];
+          dw3_acc[2 * r + j] = fmaf(g1, a1, fmaf(g0, a0, dw3_acc[2 * r + j]));
+          d0[j] = a0 > 0.f ? __fmul_rn(g0, w) : 0.f;  // g_z2 (optim.py:143-145)
+          d1[j] = a1 > 0.f ? __fmul_rn(g1, w) : 0.f;
+        }
+        umma::store_pair3(DZ2, PL64x64, p0, ep_col0 + 8 * r + ec, 64, d0[0], d0[1]);
+        umma::store_pair3(DZ2, PL64x64, p1, ep_col0 + 8 * r + ec, 64, d1[0], d1[1]);
       }
-      umma::store_chunk3(DZ2, PL64x64, ep_row, ep_col0, 64, d);
-      umma::store_chunk3(DZ2, PL64x64, ep_row, ep_col0 + 8, 64, d + 8);
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
@@ -380,19 +403,17 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     phase ^= 1;
     umma::fence_after_sync();
     TC16_STAMP(5);
-    // ---- dz1 *= [h1 > 0] -> bf16x3 ----
+    // ---- dz1 *= [h1 > 0] -> bf16x3 (same elements as this thread's epilogue 1) ----
     {
-      float v[EPC];
-      umma::tmem_ld16(TA + lane_base + ep_col0, v);
-      if (lane < 16) {
-        const int p = ep_row;
+      float v[8];
+      umma::tmem_ld_16x256b_x2(TA + lane_base + ep_col0, v);
 #pragma unroll
-        for (int c = 0; c < EPC; ++c) {
-          const int i = ep_col0 + c;
-          if (!((sM1[i * 4 + (p >> 4)] >> (p & 15)) & 1u)) v[c] = 0.f;
-        }
-        umma::store_chunk3(DZ1, PL64x64, p, ep_col0, 64, v);
-        umma::store_chunk3(DZ1, PL64x64, p, ep_col0 + 8, 64, v + 8);
+      for (int e = 0; e < 8; ++e)
+        if (!((h1pos >> e) & 1u)) v[e] = 0.f;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        umma::store_pair3(DZ1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
+        umma::store_pair3(DZ1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
       }
     }
     umma::fence_async_smem();
@@ -421,15 +442,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     __syncthreads();  // h1 / dz2 consumed (dW2, dz1 done) before gF overwrites them
     umma::fence_after_sync();
     TC16_STAMP(7);
-    // ---- gF epilogue: rows p (lanes < 16), 32 columns per warp -> gF[p][k] ----
+    // ---- gF epilogue: 32 columns per warp -> gF[p][k] ----
     {
-      float v[32];
-      umma::tmem_ld16(TA + lane_base + 2 * ep_col0, v);
-      umma::tmem_ld16(TA + lane_base + 2 * ep_col0 + 16, v + 16);
-      if (lane < 16) {
+      float v[16];
+      umma::tmem_ld_16x256b_x4(TA + lane_base + 2 * ep_col0, v);
 #pragma unroll
-        for (int c = 0; c < 32; c += 2)
-          *reinterpret_cast<float2*>(GF + gf_idx(ep_row, 2 * ep_col0 + c)) = make_float2(v[c], v[c + 1]);
+      for (int r = 0; r < 4; ++r) {
+        const int k = 2 * ep_col0 + 8 * r + ec;
+        *reinterpret_cast<float2*>(GF + gf_idx(p0, k)) = make_float2(v[4 * r], v[4 * r + 1]);
+        *reinterpret_cast<float2*>(GF + gf_idx(p1, k)) = make_float2(v[4 * r + 2], v[4 * r + 3]);
       }
     }
     umma::fence_before_sync();
@@ -451,20 +472,34 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   umma::fence_after_sync();
   float* dst = a.part_dw + int64_t(blockIdx.x) * (HID * FE + HID * HID + HID);
   {
-    // M=64 accumulators: row 16q + t in lane 32q + t (t < 16); each warp 32 dW1 columns,
-    // 16 dW2 columns
-    float v[32];
-    umma::tmem_ld16(TDW1 + lane_base + 2 * ep_col0, v);
-    umma::tmem_ld16(TDW1 + lane_base + 2 * ep_col0 + 16, v + 16);
-    if (lane < 16)
-      for (int c = 0; c < 32; ++c) dst[ep_row * FE + 2 * ep_col0 + c] = v[c];
-    umma::tmem_ld16(TDW2 + lane_base + ep_col0, v);
-    if (lane < 16)
-      for (int c = 0; c < 16; ++c) dst[HID * FE + ep_row * HID + ep_col0 + c] = v[c];
-  }
-  if (lane < 16) {
+    float v[16];
+    umma::tmem_ld_16x256b_x4(TDW1 + lane_base + 2 * ep_col0, v);  // dW1 rows i = p0 / p1
 #pragma unroll
-    for (int c = 0; c < EPC; ++c) atomicAdd(&sDW3[ep_col0 + c], dw3_acc[c]);
+    for (int r = 0; r < 4; ++r) {
+      const int k = 2 * ep_col0 + 8 * r + ec;
+      dst[p0 * FE + k] = v[4 * r];
+      dst[p0 * FE + k + 1] = v[4 * r + 1];
+      dst[p1 * FE + k] = v[4 * r + 2];
+      dst[p1 * FE + k + 1] = v[4 * r + 3];
+    }
+    umma::tmem_ld_16x256b_x2(TDW2 + lane_base + ep_col0, v);  // dW2 rows j = p0 / p1
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = ep_col0 + 8 * r + ec;
+      dst[HID * FE + p0 * HID + i] = v[4 * r];
+      dst[HID * FE + p0 * HID + i + 1] = v[4 * r + 1];
+      dst[HID * FE + p1 * HID + i] = v[4 * r + 2];
+      dst[HID * FE + p1 * HID + i + 1] = v[4 * r + 3];
+    }
+  }
+  // dW3: the 8 threads sharing lane & 3 hold the same columns
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float v = dw3_acc[c];
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (lane < 4) atomicAdd(&sDW3[ep_col0 + 8 * (c >> 1) + ec + (c & 1)], v);
   }
   const double bl = block_sum(loss, red);  // contains __syncthreads
   if (tid < HID) dst[HID * FE + HID * HID + tid] = sDW3[tid];

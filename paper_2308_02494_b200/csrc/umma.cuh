@@ -149,6 +149,17 @@ __device__ __forceinline__ void store_chunk3(unsigned char* buf, uint32_t plane,
   *reinterpret_cast<uint4*>(buf + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// two adjacent columns (c even) of row r of a bf16x3 CM buffer: one 4-byte word per plane
+__device__ __forceinline__ void store_pair3(unsigned char* buf, uint32_t plane, int r, int c, int R, float x0,
+                                           float x1) {
+  uint32_t h, m, l;
+  split2_bf16x3(x0, x1, h, m, l);
+  const uint32_t o = cm16_offset(r, c, R);
+  *reinterpret_cast<uint32_t*>(buf + o) = h;
+  *reinterpret_cast<uint32_t*>(buf + plane + o) = m;
+  *reinterpret_cast<uint32_t*>(buf + 2 * plane + o) = l;
+}
+
 __device__ __forceinline__ void commit(uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
                : "memory");
@@ -217,6 +228,31 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16 lanes x 256 bit shape (M=64 accumulators: all 32 threads carry data).  Thread t gets
+// rows t/4 and t/4 + 8 of the 16-lane block, columns 2(t%4) and 2(t%4)+1 of each 8-column
+// repetition: v[4r+0] = (t/4, 8r+2(t%4)), v[4r+1] = (t/4, +1), v[4r+2] = (t/4+8, ..), v[4r+3]
+// (the mma.sync accumulator fragment layout; probed on B200).
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
