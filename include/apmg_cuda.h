@@ -213,7 +213,7 @@ int apmg_debug_tc_phases(long long* out);
 int apmg_debug_infer_phases(long long* out);
 /* same for the bf16x3 recon kernel: [16 tiles][12 phases] (APMG_TC_STAMPS=1) */
 int apmg_debug_tc16_phases(long long* out);
-/* roofline peak probes (csrc/peaks.cu, tools/peaks.py): kind 0 L2 float2 gather, 1 L2 float2
+/* roofline peak probes (csrc/peaks.cu, tools/peaks.py): kind 0 L2 float2 gather (7: float4), 1 L2 float2
  * RED, 2 FP32 FFMA, 3 FP64 DFMA, 4 tcgen05 kind::tf32, 5 warp shuffles; `table` is a device
  * buffer of table_bytes (power of two) for kinds 0-1 (a sink otherwise); *work receives the
  * work unit count of the launch (bytes, REDs, FLOP, FLOP, FLOP, shuffles). */

@@ -10,6 +10,7 @@
 //   kind 4  tcgen05.mma kind::tf32, M=128 N=256 K=8, back to back from one thread per CTA
 //           (operands in smem, contents irrelevant); work = FLOP
 //   kind 5  warp shuffles (__shfl_sync, 32-bit); work = shuffle instructions (per warp)
+//   kind 7  L2 gather of random float4 (16-byte) elements; work = bytes loaded
 //   kind 6  shared-memory float atomic adds (red.shared.add.f32), 32 distinct banks per
 //           instruction; work = atomic instructions (per warp)
 #include "common.cuh"
@@ -39,6 +40,23 @@ __global__ void __launch_bounds__(256) k_peak_gather(const float2* __restrict__ 
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y;
+  }
+  if (acc == 12345.678f) sink[0] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_peak_gather4(const float4* __restrict__ t, uint32_t mask, int iters,
+                                                      float* __restrict__ sink) {
+  uint32_t s = mix32(blockIdx.x * blockDim.x + threadIdx.x);
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s = s * 1664525u + 1013904223u;
+      v[u] = __ldg(t + (mix32(s) & mask));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
   }
   if (acc == 12345.678f) sink[0] = acc;
 }
@@ -179,6 +197,15 @@ extern "C" int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, i
       APMG_LAUNCH("peak_shfl", k_peak_shfl, sms * 8, 256, 0, st, iters, sink);
       *work = double(sms) * 8 * 8 * iters * 4;  // warp-level shuffle instructions
       return APMG_OK;
+    case 7: {
+      APMG_ARG_CHECK(table && table_bytes >= 16 && (table_bytes & (table_bytes - 1)) == 0,
+                     "table_bytes must be a power of two");
+      const int grid = sms * 8, block = 256;
+      APMG_LAUNCH("peak_gather4", k_peak_gather4, grid, block, 0, st, static_cast<const float4*>(table),
+                  uint32_t(table_bytes / 16 - 1), iters, sink);
+      *work = double(grid) * block * iters * 8 * 16;
+      return APMG_OK;
+    }
     case 6:
       APMG_LAUNCH("peak_atoms", k_peak_atoms, sms * 8, 256, 0, st, iters, sink);
       *work = double(sms) * 8 * 8 * iters * 16;  // warp-level atomic instructions

@@ -37,6 +37,8 @@ def main():
         t = torch.zeros((mib << 20) // 4, dtype=torch.float32, device="cuda")
         g, dt = probe(0, t, mib << 20, 256)
         out[f"l2_gather_float2_GBps_{mib}MiB"] = g / 1e9
+        g4, dt = probe(7, t, mib << 20, 256)
+        out[f"l2_gather_float4_GBps_{mib}MiB"] = g4 / 1e9
         r, dt = probe(1, t, mib << 20, 64)
         out[f"l2_red_float2_Gops_{mib}MiB"] = r / 1e9
     big = torch.zeros((1 << 30) // 4, dtype=torch.float32, device="cuda")
