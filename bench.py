@@ -374,7 +374,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 (3xTF32 tensor-core MLP, f64 density statistics and loss)", "data": "synthetic",
+            "dtype": "f32 (bf16x3 tensor-core MLP: 6-product forward, 3-product backward; f64 density statistics and loss)", "data": "synthetic",
             "config": {"workload": desc, "global_batch": BATCH * world, "model": "APMGSRN 64 grids 32^3 x2, MLP 2x64",
                        "density_loss": "every timed iteration", "parallelism": f"brick-sharded x{world}",
                        "l2": "inputs larger than L2 (512 MiB+ volume per rank); 16 MiB grids L2-resident by design"},

@@ -60,6 +60,10 @@ int apmg_device_sm_count(void);
 /* number of kernels this library launched since load (evidence for bench.py) */
 uint64_t apmg_launch_count(void);
 /* per-kernel CUDA-event timing on the launching stream (bench roofline). */
+/* Release the device blocks the library caches between sessions (the bricked volume
+ * copy of apmg_train_create).  No reference counterpart (memory management of the CUDA
+ * path). */
+int apmg_release_cached(void);
 int apmg_kernel_timing_enable(int on);
 /* copies up to `cap` records (name, total_ms, launches); returns count.  Synchronises. */
 int apmg_kernel_timing_read(char* names /* cap*64 bytes */, double* total_ms, int64_t* launches, int cap);

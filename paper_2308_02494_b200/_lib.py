@@ -49,6 +49,7 @@ SIGNATURES = {
     "apmg_version": (C.c_char_p, []),
     "apmg_device_sm_count": (C.c_int, []),
     "apmg_launch_count": (C.c_uint64, []),
+    "apmg_release_cached": (C.c_int, []),
     "apmg_kernel_timing_enable": (C.c_int, [C.c_int]),
     "apmg_kernel_timing_read": (C.c_int, [C.c_char_p, C.POINTER(_D), C.POINTER(_I64), C.c_int]),
     "apmg_to_local": (C.c_int, [_I32, _P, _P, _I64, _P, _P]),
@@ -170,10 +171,66 @@ def ptr(t) -> C.c_void_p:
     return C.c_void_p(0 if t is None else t.data_ptr())
 
 
+_STAGE_BYTES = 16 << 20
+_STAGE_SLOTS = 8
+_stage = None
+
+
+def _staging():
+    """Process-level ring of pinned staging buffers (allocated once) for large uploads."""
+    global _stage
+    if _stage is None:
+        import concurrent.futures as cf
+        t = torch()
+        bufs = [t.empty(_STAGE_BYTES, dtype=t.uint8, pin_memory=True) for _ in range(_STAGE_SLOTS)]
+        _stage = (bufs, [None] * _STAGE_SLOTS, cf.ThreadPoolExecutor(max_workers=_STAGE_SLOTS))
+    return _stage
+
+
+def _upload_staged(a: np.ndarray, out) -> None:
+    """Pageable host array -> device tensor through the pinned ring: host threads fill the
+    slots (numpy copies release the GIL) while the copy engine drains the filled ones, so
+    the host memcpy and the PCIe / C2C transfer overlap instead of running back to back
+    as the driver's own pageable path does."""
+    t = torch()
+    bufs, events, pool = _staging()
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(t.uint8)
+    n = src.size
+    chunks = [(o, min(_STAGE_BYTES, n - o)) for o in range(0, n, _STAGE_BYTES)]
+    st = t.cuda.current_stream()
+
+    def fill(slot, o, m):
+        ev = events[slot]
+        if ev is not None:
+            ev.synchronize()
+        np.copyto(bufs[slot][:m].numpy(), src[o:o + m])
+
+    futs = [None] * _STAGE_SLOTS
+    for i, (o, m) in enumerate(chunks[:_STAGE_SLOTS]):
+        futs[i] = pool.submit(fill, i, o, m)
+    for i, (o, m) in enumerate(chunks):
+        slot = i % _STAGE_SLOTS
+        futs[slot].result()
+        dst[o:o + m].copy_(bufs[slot][:m], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(st)
+        events[slot] = ev
+        j = i + _STAGE_SLOTS
+        if j < len(chunks):
+            futs[slot] = pool.submit(fill, slot, *chunks[j])
+    st.synchronize()
+
+
 def to_device(arr: np.ndarray, dtype=None):
-    """Host numpy -> contiguous CUDA tensor (plumbing only)."""
+    """Host numpy -> contiguous CUDA tensor (plumbing only); arrays of 4 MiB and more go
+    through the pinned staging ring."""
     t = require_cuda()
     a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
+    if a.nbytes >= (4 << 20):
+        out = t.empty(a.shape, dtype=t.from_numpy(a[:0].reshape(-1)).dtype, device=device())
+        _upload_staged(a, out)
+        return out
     return t.from_numpy(a).to(device(), non_blocking=False)
 
 
@@ -192,8 +249,50 @@ def workspace(nbytes: int):
     return empty((max(int(nbytes), 1),), np.uint8)
 
 
+def download_into(dev, out: np.ndarray) -> None:
+    """Contiguous device tensor -> existing contiguous host array of the same byte size,
+    through the pinned ring: the copy engine fills slot i+1 while host threads drain slot i."""
+    t = torch()
+    src = dev.detach().contiguous().view(-1).view(t.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    n = dst.size
+    if src.numel() != n:
+        raise ValueError(f"download_into: {src.numel()} device bytes into a {n}-byte host array")
+    bufs, events, pool = _staging()
+    st = t.cuda.current_stream()
+    chunks = [(o, min(_STAGE_BYTES, n - o)) for o in range(0, n, _STAGE_BYTES)]
+    futs = [None] * _STAGE_SLOTS
+
+    def drain(slot, ev, o, m):
+        ev.synchronize()
+        np.copyto(dst[o:o + m], bufs[slot][:m].numpy())
+
+    for i, (o, m) in enumerate(chunks):
+        slot = i % _STAGE_SLOTS
+        if futs[slot] is not None:
+            futs[slot].result()
+        bufs[slot][:m].copy_(src[o:o + m], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(st)
+        events[slot] = ev
+        futs[slot] = pool.submit(drain, slot, ev, o, m)
+    for f in futs:
+        if f is not None:
+            f.result()
+
+
 def to_host(t) -> np.ndarray:
+    if t.numel() * t.element_size() >= (4 << 20):
+        out = np.empty(tuple(t.shape), dtype=torch_to_np(t.dtype))
+        download_into(t, out)
+        return out
     return t.detach().cpu().numpy()
+
+
+def torch_to_np(dt):
+    t = torch()
+    return {t.float32: np.float32, t.float64: np.float64, t.int64: np.int64, t.int32: np.int32,
+            t.uint8: np.uint8}[dt]
 
 
 def dtype_code(np_dtype) -> int:

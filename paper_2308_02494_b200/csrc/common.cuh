@@ -27,6 +27,10 @@ struct LaunchScope {
 };
 
 int num_sms();
+// large-buffer cache (runtime.cu): blocks keep their allocation size for pool_free
+void* pool_alloc(size_t bytes);
+void pool_free(void* p, size_t bytes);
+void release_pool();
 
 #define APMG_CUDA_TRY(expr)                                                                  \
   do {                                                                                       \

@@ -79,9 +79,54 @@ int num_sms() {
   return n;
 }
 
+// Block cache for the library's own large device buffers (the bricked volume copy of a
+// training session).  cudaMalloc / cudaFree of a 0.5 GiB block cost 10-200 ms each and
+// cudaFree synchronises the device; sessions are created back to back (train_single,
+// the decomposed trainer's per-brick sessions), so freed blocks are kept and handed to
+// the next request of a similar size.  Cached blocks are released when an allocation
+// fails and by apmg_release_cached().
+static std::mutex g_pmu;
+static std::multimap<size_t, void*> g_pool;  // size -> free block
+
+void* pool_alloc(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    auto it = g_pool.lower_bound(bytes);
+    if (it != g_pool.end() && it->first <= bytes + bytes / 4) {
+      void* p = it->second;
+      g_pool.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
+  cudaGetLastError();
+  release_pool();
+  if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+void pool_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pmu);
+  g_pool.emplace(bytes, p);
+}
+
+void release_pool() {
+  std::lock_guard<std::mutex> lk(g_pmu);
+  for (auto& kv : g_pool) cudaFree(kv.second);
+  g_pool.clear();
+}
+
 }  // namespace apmg
 
 using namespace apmg;
+
+extern "C" int apmg_release_cached(void) {
+  release_pool();
+  return APMG_OK;
+}
 
 extern "C" const char* apmg_last_error(void) { return g_err.c_str(); }
 extern "C" const char* apmg_version(void) { return "apmg-b200 0.1 sm_100a"; }

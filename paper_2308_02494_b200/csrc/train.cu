@@ -143,6 +143,7 @@ struct apmg_train_state {
   uint64_t graph_launches = 0;
   // 8x8x8-bricked copy of the volume for the sorted sampler (owned; APMG_BRICKED=0 disables)
   float* vol_bricked = nullptr;
+  size_t vol_bricked_bytes = 0;
   int nbx = 0, nby = 0;
 };
 
@@ -260,10 +261,9 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
       s->nby = (h + 7) / 8;
       const int nbz = (d + 7) / 8;
       const size_t bytes = sizeof(float) * 512 * size_t(s->nbx) * s->nby * nbz;
-      if (cudaMalloc(&s->vol_bricked, bytes) != cudaSuccess) {
-        s->vol_bricked = nullptr;  // no room: sample the row-major volume
-        cudaGetLastError();
-      } else {
+      s->vol_bricked = static_cast<float*>(pool_alloc(bytes));
+      s->vol_bricked_bytes = bytes;
+      if (s->vol_bricked) {  // else no room: sample the row-major volume
         const int64_t nv = int64_t(w) * h * d;
         const int g = int(std::min<int64_t>(ceil_div(nv, 256), int64_t(num_sms()) * 32));
         APMG_LAUNCH("brick_volume", k_brick_volume, g, 256, 0, st, volume, w, h, d, s->nbx, s->nby, s->vol_bricked);
@@ -442,7 +442,10 @@ extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_dens
 
 extern "C" int apmg_train_destroy(apmg_train_state* s) {
   if (s && s->graph) cudaGraphExecDestroy(s->graph);
-  if (s && s->vol_bricked) cudaFree(s->vol_bricked);
+  if (s && s->vol_bricked) {
+    cudaDeviceSynchronize();  // as cudaFree would: no launch may still read the block
+    pool_free(s->vol_bricked, s->vol_bricked_bytes);
+  }
   delete s;
   return APMG_OK;
 }

@@ -196,9 +196,15 @@ class TrainSession:
     def pull_params(self) -> None:
         """Copy the device parameters back into the model's host arrays, in place."""
         m, o = self.model, self.off
-        main = L.to_host(self.main)
-        g = main[o[0]:o[0] + m.grids.size].reshape(m.config.grids, *m.config.resolution, m.config.channels)
-        m.grids[...] = np.moveaxis(g, -1, 1)
+        c = m.config
+        gdev = self.main[o[0]:o[0] + m.grids.size].view(c.grids, *c.resolution, c.channels)
+        gdev = gdev.permute(0, 4, 1, 2, 3).contiguous()  # channel-last device -> (G, C, ...) host layout
+        if m.grids.flags.c_contiguous and m.grids.dtype == L.torch_to_np(gdev.dtype):
+            L.download_into(gdev, m.grids)
+        else:
+            m.grids[...] = L.to_host(gdev)
+        main = L.to_host(self.main[o[1]:])
+        o = [x - o[1] for x in o]
         m.w1[...] = main[o[1]:o[1] + m.w1.size].reshape(m.w1.shape)
         m.w2[...] = main[o[2]:o[2] + m.w2.size].reshape(m.w2.shape)
         m.w3[...] = main[o[3]:o[3] + m.w3.size].reshape(m.w3.shape)

@@ -25,7 +25,7 @@ def tic():
     return time.perf_counter()
 
 
-for rep in range(2):
+for rep in range(3):
     t0 = tic()
     vol = PV.Volume(dims=dims, data=host)
     t1 = tic()
@@ -46,17 +46,14 @@ for rep in range(2):
     print(f"rep {rep}: Volume() {1e3*(t1-t0):.1f} ms, upload {1e3*(t2-t1):.1f} ms, init_model {1e3*(t3-t2):.1f} ms, "
           f"session {1e3*(t4-t3):.1f} ms, run {1e3*(t5-t4):.1f} ms, pull+log+close {1e3*(t6-t5):.1f} ms")
 
-# session creation detail
-import cProfile, pstats
-vol = PV.Volume(dims=dims, data=host)
-vol.device_data()
-m = PM.init_model(PM.ModelConfig(64, 2, (32, 32, 32)), seed=0, vmin=vol.vmin, vmax=vol.vmax)
-cfg = PT.TrainConfig(iterations=50, batch_size=1 << 20, delay_start=0, transform_hard_stop_fraction=1.0,
-                     plateau_enabled=False, seed=0)
-pr = cProfile.Profile()
-torch.cuda.synchronize()
-pr.enable()
-s = PT.TrainSession(m, vol, cfg)
-torch.cuda.synchronize()
-pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(12)
+
+# the bench's e2e call itself
+for rep in range(3):
+    vol = PV.Volume(dims=dims, data=host)
+    m = PM.init_model(PM.ModelConfig(64, 2, (32, 32, 32)), seed=0, vmin=vol.vmin, vmax=vol.vmax)
+    cfg = PT.TrainConfig(iterations=50, batch_size=1 << 20, delay_start=0, transform_hard_stop_fraction=1.0,
+                         plateau_enabled=False, seed=0)
+    t0 = tic()
+    _, lg = PT.train_single(m, vol, cfg)
+    t1 = tic()
+    print(f"train_single e2e rep {rep}: {1e3*(t1-t0):.1f} ms -> {50 * (1 << 20) / (t1 - t0) / 1e6:.1f} M pts/s")
