@@ -389,25 +389,57 @@ __global__ void k_adam(T* __restrict__ p, const T* __restrict__ g, T* __restrict
 }
 
 // training variant: scalars from the controller; consumes and clears the gradient
+// training variant: also keeps the x-pair grid copy (ModelDev::gridx) current: element e
+// of the two-channel grid (cell e/2, channel e%2) is the low half of gridx[cell] and the
+// high half of gridx[cell - 1].  gx = nullptr: no copy.
+// dgx != nullptr: the grid part of the gradient is in the x-pair layout (ModelDev::grad_pairs);
+// element (cell c, channel ch) sums dgx[c].lo and dgx[c - 1].hi, and clears both.
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl) {
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx) {
   if (ctl->skip) return;
   const T lr_t = T(ctl->lr_main_t), c1 = T(ctl->bc1_main), c2 = T(ctl->bc2_main);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const T gi = g[i];
+    const bool pair = sizeof(T) == 4 && dgx && i < gx_elems;
+    T gi = pair ? T(0) : g[i];
+    if constexpr (sizeof(T) == 4) {
+      if (pair) {
+        const int64_t c = i >> 1, ch = i & 1;
+        const float lo = dgx[4 * c + ch], hi = c > 0 ? dgx[4 * (c - 1) + 2 + ch] : 0.f;
+        if (lo != 0.f) dgx[4 * c + ch] = 0.f;
+        if (hi != 0.f) dgx[4 * (c - 1) + 2 + ch] = 0.f;
+        gi = lo + hi;
+      }
+    }
     if (gi == T(0)) continue;
     T pi = p[i], mi = m[i], vi = v[i];
     adam_elem(pi, gi, mi, vi, lr_t, c1, c2);
     p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    g[i] = T(0);
+    if (!pair) g[i] = T(0);
+    if constexpr (sizeof(T) == 4) {
+      if (gx && i < gx_elems) {
+        const int64_t c = i >> 1, ch = i & 1;
+        gx[4 * c + ch] = pi;
+        if (c > 0) gx[4 * (c - 1) + 2 + ch] = pi;
+      }
+    }
   }
 }
 
-template __global__ void k_adam_train<float>(float*, float*, float*, float*, int64_t, const TrainCtl*);
-template __global__ void k_adam_train<double>(double*, double*, double*, double*, int64_t, const TrainCtl*);
+template __global__ void k_adam_train<float>(float*, float*, float*, float*, int64_t, const TrainCtl*, float*,
+                                             int64_t, float*);
+template __global__ void k_adam_train<double>(double*, double*, double*, double*, int64_t, const TrainCtl*, float*,
+                                              int64_t, float*);
+
+// gridx[c] = (grid[c], grid[c + 1]) for the flat two-channel cells c (zero past the end)
+__global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < cells; c += int64_t(gridDim.x) * blockDim.x) {
+    const float2 a = grid[c], b = c + 1 < cells ? grid[c + 1] : make_float2(0.f, 0.f);
+    gx[c] = make_float4(a.x, a.y, b.x, b.y);
+  }
+}
 
 int elementwise_grid(int64_t n, int per_sm) {
   return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), int64_t(num_sms()) * per_sm)));

@@ -29,6 +29,14 @@ struct ModelDev {
   const T* __restrict__ w2;    // [64][64]
   const T* __restrict__ w3;    // [64]
   T span, vmin;                // np.asarray(vmax - vmin, dtype), np.asarray(vmin, dtype)
+  // optional x-pair copy of a two-channel f32 grid (training sessions): gridx[c] =
+  // (grid[c], grid[c + 1]) over the flat cell index c, so the two x-corners of a cell edge
+  // are one 16-byte load -- the encoder's gathers are L2-request-bound, not byte-bound
+  const float4* __restrict__ gridx = nullptr;
+  // the grid gradient the recon kernel scatters into is in the same x-pair layout
+  // (dgridx[c] = d/d(grid[c]), d/d(grid[c + 1]) partial sums; float4 REDs, half the RED
+  // operations): grad(grid[v]) = dgridx[v].lo + dgridx[v - 1].hi.  tc16 kernel only.
+  bool grad_pairs = false;
 };
 
 template <typename T>
@@ -171,6 +179,21 @@ __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, 
   o1 = r.y;
 }
 
+// interp_pair_f32 over the x-pair copy: 4 float4 loads instead of 8 float2, same
+// arithmetic in the same order (bit-identical features)
+__device__ __forceinline__ void interp_pairx_f32(const float4* __restrict__ gx, int W, int HW, int vbase, float fx,
+                                                 float fy, float fz, float& o0, float& o1) {
+  const float4* g = gx + vbase;
+  const float4 b00 = __ldg(g), b01 = __ldg(g + W), b10 = __ldg(g + HW), b11 = __ldg(g + HW + W);
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(make_float2(b00.x, b00.y), make_float2(b00.z, b00.w), fx),
+                                   f2_lerp(make_float2(b01.x, b01.y), make_float2(b01.z, b01.w), fx), fy),
+                           f2_lerp(f2_lerp(make_float2(b10.x, b10.y), make_float2(b10.z, b10.w), fx),
+                                   f2_lerp(make_float2(b11.x, b11.y), make_float2(b11.z, b11.w), fx), fy),
+                           fz);
+  o0 = r.x;
+  o1 = r.y;
+}
+
 // Encode point (x0,x1,x2) in grid m into out[0..C) (zero outside the grid).
 template <typename T>
 __device__ __forceinline__ void encode_grid_point(const ModelDev<T>& md, int m, T x0, T x1, T x2, T* out,
@@ -225,6 +248,17 @@ __device__ __forceinline__ void scatter_pair_f32(const ModelDev<float>& md, floa
 __device__ __forceinline__ void scatter_vertex_f32(const ModelDev<float>& md, float* __restrict__ dgrid, int vbase,
                                                    float fx, float fy, float fz, float g0, float g1) {
   const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+  if (md.grad_pairs) {
+    float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
+#pragma unroll
+    for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy) {
+        const float wzy = wy[cy] * wz[cz], w0 = wx[0] * wzy, w1 = wx[1] * wzy;
+        atomicAdd(base + cz * md.H * md.W + cy * md.W, make_float4(g0 * w0, g1 * w0, g0 * w1, g1 * w1));
+      }
+    return;
+  }
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;
   float* base = dgrid + (size_t(vbase) << 1);
 #pragma unroll
@@ -286,6 +320,14 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
   }
   // after `rounds` rounds the lanes of rank 0 mod 2^rounds hold their block's sums
   if (!valid || (rank & ((1 << rounds) - 1)) != 0) return;
+  if (md.grad_pairs) {  // x-pair gradient: corners (0, cy, cz) and (1, cy, cz) in one float4 RED
+    float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
+#pragma unroll
+    for (int c = 0; c < 8; c += 2)
+      atomicAdd(base + (c >> 2) * md.H * md.W + ((c >> 1) & 1) * md.W,
+                make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y));
+    return;
+  }
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;
   float* base = dgrid + (size_t(vbase) << 1);
 #pragma unroll

@@ -389,6 +389,16 @@ size_t recon_ws_bytes(int F, int64_t n) {
   return c.used + 256;
 }
 
+static bool use_tc16() {
+  const char* e16 = getenv("APMG_RECON16");
+  return !(e16 && e16[0] == '0');
+}
+
+bool recon_uses_tc16(const apmg_model& m) {
+  if (m.dtype != APMG_F32) return false;
+  return use_tc16() && recon_tc_eligible(make_model_dev<float>(m));
+}
+
 template <typename T>
 int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* targets, T* sq, double* loss,
                  T* dgrid, T* dw1, T* dw2, T* dw3, void* ws, size_t wsb, const TrainCtl* ctl, double* l_rec_log,
@@ -408,11 +418,11 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
   }
   bool done = false;
   if constexpr (sizeof(T) == 4) {
+    if (md.grad_pairs) APMG_ARG_CHECK(recon_tc_eligible(md) && use_tc16(), "x-pair gradients need the tc16 kernel");
     if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
       grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms())));
       // default: bf16x3 all-tcgen05 kernel; APMG_RECON16=0 selects the tf32 / mma.sync one (A/B)
-      const char* e16 = getenv("APMG_RECON16");
-      if (!(e16 && e16[0] == '0'))
+      if (use_tc16())
         rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
       else
         rc = launch_recon_tc(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);

@@ -11,6 +11,7 @@
 //           (operands in smem, contents irrelevant); work = FLOP
 //   kind 5  warp shuffles (__shfl_sync, 32-bit); work = shuffle instructions (per warp)
 //   kind 7  L2 gather of random float4 (16-byte) elements; work = bytes loaded
+//   kind 8  L2 RED of random float4 (red.global.add.v4.f32); work = float4 REDs issued
 //   kind 6  shared-memory float atomic adds (red.shared.add.f32), 32 distinct banks per
 //           instruction; work = atomic instructions (per warp)
 #include "common.cuh"
@@ -68,6 +69,17 @@ __global__ void __launch_bounds__(256) k_peak_red(float* __restrict__ t, uint32_
     for (int u = 0; u < 8; ++u) {
       s = s * 1664525u + 1013904223u;
       atomicAdd(reinterpret_cast<float2*>(t) + (mix32(s) & mask), make_float2(1e-7f, 1e-7f));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_peak_red4(float* __restrict__ t, uint32_t mask, int iters) {
+  uint32_t s = mix32(blockIdx.x * blockDim.x + threadIdx.x + 777u);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s = s * 1664525u + 1013904223u;
+      atomicAdd(reinterpret_cast<float4*>(t) + (mix32(s) & mask), make_float4(1e-7f, 1e-7f, 1e-7f, 1e-7f));
     }
   }
 }
@@ -204,6 +216,15 @@ extern "C" int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, i
       APMG_LAUNCH("peak_gather4", k_peak_gather4, grid, block, 0, st, static_cast<const float4*>(table),
                   uint32_t(table_bytes / 16 - 1), iters, sink);
       *work = double(grid) * block * iters * 8 * 16;
+      return APMG_OK;
+    }
+    case 8: {
+      APMG_ARG_CHECK(table && table_bytes >= 16 && (table_bytes & (table_bytes - 1)) == 0,
+                     "table_bytes must be a power of two");
+      const int grid = sms * 8, block = 256;
+      APMG_LAUNCH("peak_red4", k_peak_red4, grid, block, 0, st, static_cast<float*>(table),
+                  uint32_t(table_bytes / 16 - 1), iters);
+      *work = double(grid) * block * iters * 8;
       return APMG_OK;
     }
     case 6:

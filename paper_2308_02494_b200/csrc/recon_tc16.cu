@@ -92,6 +92,7 @@ struct Args {
   const TrainCtl* ctl;
   int aggregate;
   int stamps;
+  int skip;  // APMG_TC_SKIP (timing experiments only, wrong results): 1 = no scatter, 2 = no gathers
 };
 
 __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX, float* sT, int tid) {
@@ -108,6 +109,7 @@ __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX
 // scatter of one (2 grids x 2 points) group (see recon_tc.cu)
 __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const Args& a, const float* GF,
                                               uint32_t tmem_cache, int jq, int cnt, int warp, int lane) {
+  if (a.skip & 1) return;
   uint32_t cache[16];
   umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
 #pragma unroll
@@ -232,7 +234,12 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
       const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
       float f0 = 0.f, f1 = 0.f;
-      if (inside) interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+      if (inside && !(a.skip & 2)) {
+        if (md.gridx)
+          interp_pairx_f32(md.gridx, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+        else
+          interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+      }
       cache[4 * u] = uint32_t(vbase);
       cache[4 * u + 1] = __float_as_uint(fx);
       cache[4 * u + 2] = __float_as_uint(fy);
@@ -528,7 +535,8 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
   const char* ea = getenv("APMG_SCATTER_AGG");
   const char* es = getenv("APMG_TC_STAMPS");
   tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1,
-               (es && es[0] == '1') ? 1 : 0};
+               (es && es[0] == '1') ? 1 : 0, 0};
+  if (const char* sk = getenv("APMG_TC_SKIP")) a.skip = atoi(sk);
   APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
   return APMG_OK;
 }

@@ -27,7 +27,8 @@ __global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const flo
                               int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl);
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx);
+__global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);
 int elementwise_grid(int64_t n, int per_sm);
 constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
@@ -142,6 +143,9 @@ struct apmg_train_state {
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_launches = 0;
   // 8x8x8-bricked copy of the volume for the sorted sampler (owned; APMG_BRICKED=0 disables)
+  float4* gridx = nullptr;  // x-pair grid copy (ModelDev::gridx), or null
+  float4* gradx = nullptr;  // x-pair grid gradient (ModelDev::grad_pairs), or null
+  int64_t gx_cells = 0;
   float* vol_bricked = nullptr;
   size_t vol_bricked_bytes = 0;
   int nbx = 0, nby = 0;
@@ -194,7 +198,19 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   char* recon_ws = cv.take<char>(rws);
   const size_t dws = density_ws_bytes(m->grids, B);
   char* dens_ws = cv.take<char>(dws);
+  // x-pair grid copy for the tensor-core encoder (two-channel f32 models; APMG_GRIDX=0 off)
+  const char* eg = getenv("APMG_GRIDX");
+  const bool use_gx = m->dtype == APMG_F32 && m->channels == 2 && !(eg && eg[0] == '0');
+  const int64_t cells = int64_t(m->grids) * m->depth * m->height * m->width;
+  float4* gridx = use_gx ? cv.take<float4>(cells) : nullptr;
+  // ... and the x-pair grid gradient when the bf16x3 recon kernel runs (APMG_GRADX=0 off)
+  const char* ed = getenv("APMG_GRADX");
+  const bool use_dgx = use_gx && recon_uses_tc16(*m) && !(ed && ed[0] == '0');
+  float4* gradx = use_dgx ? cv.take<float4>(cells) : nullptr;
   if (s) {
+    s->gridx = gridx;
+    s->gradx = gradx;
+    s->gx_cells = use_gx ? cells : 0;
     s->ctl = ctl;
     s->l_rec = l_rec;
     s->l_dens = l_dens;
@@ -291,6 +307,7 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   APMG_CUDA_TRY(cudaMemcpyAsync(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
   APMG_CUDA_TRY(cudaMemcpyAsync(s->bias, bias_table, sizeof(double) * 2 * cfg->iterations, cudaMemcpyHostToDevice, st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->grad, 0, es * s->off[4], st));
+  if (s->gradx) APMG_CUDA_TRY(cudaMemsetAsync(s->gradx, 0, sizeof(float4) * s->gx_cells, st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->am, 0, es * s->off[4], st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->av, 0, es * s->off[4], st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->tm, 0, es * 16 * shape->grids, st));
@@ -314,7 +331,9 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   live.w2 = params + s->off[2];
   live.w3 = params + s->off[3];
   live.transforms = s->transforms;
-  const ModelDev<T> md = make_model_dev<T>(live);
+  ModelDev<T> md = make_model_dev<T>(live);
+  md.gridx = s->gridx;
+  md.grad_pairs = s->gradx != nullptr;
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
   if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
@@ -336,11 +355,14 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                 s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
   }
   int rc = launch_recon<T>(md, B, static_cast<const T*>(s->coords), static_cast<const T*>(s->targets),
-                           static_cast<T*>(s->sq), nullptr, grad + s->off[0], grad + s->off[1], grad + s->off[2],
+                           static_cast<T*>(s->sq), nullptr,
+                           s->gradx ? reinterpret_cast<T*>(s->gradx) : grad + s->off[0], grad + s->off[1],
+                           grad + s->off[2],
                            grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);
   if (rc) return rc;
   APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
-              static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl);
+              static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
+              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx));
   if (c.train_transforms) {
     rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, static_cast<const T*>(s->coords),
                               static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),
@@ -365,6 +387,10 @@ extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
   APMG_ARG_CHECK(s != nullptr, "null state");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t done = 0;
+  if (s->gridx && n > 0)  // (re)build the x-pair copy: the caller may have rewritten the parameters
+    APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(s->gx_cells, 8), 256, 0, st,
+                reinterpret_cast<const float2*>(static_cast<float*>(s->main_params) + s->off[0]), s->gridx,
+                s->gx_cells);
   if (graphs_enabled() && n >= kGraphIters) {
     if (!s->graph) {
       int rc = run_direct(s, st);  // first iteration direct: one-time launch attributes set outside capture

@@ -74,6 +74,7 @@ class TrainLog:
     plateau_trigger_iterations: list = field(default_factory=list)
     iterations_run: int = 0
     wall_seconds: float = 0.0
+    setup_seconds: float = 0.0  # volume / parameter upload and session creation (train_single)
 
     def records(self):
         stop = self.transform_stop_iteration
@@ -266,6 +267,7 @@ def train_single(model: ApmgModel, volume: Volume, cfg: TrainConfig, on_iteratio
         return model, log
     t0 = time.perf_counter()
     sess = TrainSession(model, volume, cfg)
+    setup = time.perf_counter() - t0  # apmg_train_create returns synchronised
     try:
         if on_iteration is None:
             done = 0
@@ -291,6 +293,7 @@ def train_single(model: ApmgModel, volume: Volume, cfg: TrainConfig, on_iteratio
     finally:
         sess.close()
     log.wall_seconds = time.perf_counter() - t0
+    log.setup_seconds = setup
     return model, log
 
 

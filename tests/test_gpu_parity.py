@@ -543,3 +543,24 @@ def test_recon_tensor_core_path_vs_oracle(res, monkeypatch):
     assert loss_s == pytest.approx(loss, rel=1e-5)
     for k in ("grids", "w1", "w2", "w3"):
         assert tensor_rel(grads[k], grads_s[k]) <= 1e-3, k
+
+
+@pytest.mark.gpu
+def test_gridx_pair_copy_matches_plain_grid(monkeypatch):
+    """Training sessions gather grid corners from the x-pair copy (ModelDev::gridx, kept current
+    by the fused Adam step).  The features must be bit-identical to gathering from the grid
+    itself: the first iteration's loss is equal, and the trajectories agree to the run-to-run
+    noise of the atomic scatter."""
+    vol = PV.synth_volume((96, 96, 96), C1_BLOBS)
+
+    def run():
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=24, batch_size=1 << 14, delay_start=8, seed=0, plateau_enabled=False)
+        return P.train_single(m, vol, cfg)[1]
+
+    a = run()
+    monkeypatch.setenv("APMG_GRIDX", "0")
+    b = run()
+    assert a.l_rec[0] == b.l_rec[0]
+    np.testing.assert_allclose(a.l_rec, b.l_rec, rtol=1e-3)

@@ -40,11 +40,15 @@ for n in ("__init__", "run", "status", "pull_params", "log", "close"):
     traced(PT.TrainSession, n)
 traced(PV.Volume, "device_data")
 
+if "--after-bench" in sys.argv:  # first the bench's own device-resident run, as in bench.py
+    sys.argv = ["bench.py", "--no-cpu-baseline", "--no-inference", "--no-e2e"]
+    bench.main()
 cfg = PT.TrainConfig(iterations=50, batch_size=1 << 20, delay_start=0, transform_hard_stop_fraction=1.0,
                      plateau_enabled=False, seed=0)
-vol = PV.Volume(dims=dims, data=host)
-m = PM.init_model(PM.ModelConfig(64, 2, (32, 32, 32)), seed=0, vmin=vol.vmin, vmax=vol.vmax)
-PT.train_single(m, vol, cfg)
+if "--cold" not in sys.argv:
+    vol = PV.Volume(dims=dims, data=host)
+    m = PM.init_model(PM.ModelConfig(64, 2, (32, 32, 32)), seed=0, vmin=vol.vmin, vmax=vol.vmax)
+    PT.train_single(m, vol, cfg)
 events.clear()
 for rep in range(4):
     vol = PV.Volume(dims=dims, data=host)

@@ -41,6 +41,8 @@ def main():
         out[f"l2_gather_float4_GBps_{mib}MiB"] = g4 / 1e9
         r, dt = probe(1, t, mib << 20, 64)
         out[f"l2_red_float2_Gops_{mib}MiB"] = r / 1e9
+        r4, dt = probe(8, t, mib << 20, 64)
+        out[f"l2_red_float4_Gops_{mib}MiB"] = r4 / 1e9
     big = torch.zeros((1 << 30) // 4, dtype=torch.float32, device="cuda")
     g, _ = probe(0, big, 1 << 30, 64)
     out["hbm_gather_float2_GBps_1GiB"] = g / 1e9
