@@ -1,7 +1,7 @@
 # Builds the in-tree C-ABI library for B200 (sm_100a) and the oracle checker.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2308_02494_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
 OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))

@@ -12,7 +12,7 @@
 //  * backward weights (optim.py:129-152): w = (wx * wy) * wz in f64.
 #pragma once
 #ifndef APMG_AGG_ROUNDS
-#define APMG_AGG_ROUNDS 3  // tree rounds cap: groups above 8 lanes issue one RED set per 8-lane block
+#define APMG_AGG_ROUNDS 2  // tree rounds cap: groups above 4 lanes issue one RED set per 4-lane block
                           // (3 rounds measured 3% faster than the full 5: shuffles are the bound)
 #endif
 

@@ -160,6 +160,16 @@ __device__ __forceinline__ void store_pair3(unsigned char* buf, uint32_t plane, 
   *reinterpret_cast<uint32_t*>(buf + 2 * plane + o) = l;
 }
 
+// same, high and middle planes only (operands of the 3-product backward)
+__device__ __forceinline__ void store_pair2(unsigned char* buf, uint32_t plane, int r, int c, int R, float x0,
+                                           float x1) {
+  uint32_t h, m, l;
+  split2_bf16x3(x0, x1, h, m, l);
+  const uint32_t o = cm16_offset(r, c, R);
+  *reinterpret_cast<uint32_t*>(buf + o) = h;
+  *reinterpret_cast<uint32_t*>(buf + plane + o) = m;
+}
+
 __device__ __forceinline__ void commit(uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
                : "memory");
