@@ -334,6 +334,70 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
   for (int c = 0; c < 8; ++c) atomic_add2(base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1), v[c].x, v[c].y);
 }
 
+// Leader-gather variant of the aggregated scatter: instead of tree-reducing the 8 x 2 corner
+// contributions (16 shuffles per round), each block leader fetches its members' five inputs
+// (g0, g1, fx, fy, fz) one member per round and forms their corner contributions itself:
+// 5 shuffles per member, the weights recomputed in the FMA pipe, which has headroom (the
+// shuffles share the LSU data path with the shared-memory traffic and the gathers).  Lanes
+// of rank r = 0 mod (CAP + 1) in their cell group lead blocks of up to CAP + 1 lanes.
+#ifndef APMG_GATHER_CAP
+#define APMG_GATHER_CAP 1
+#endif
+__device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float fz, float2* v, bool add) {
+  const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float w = wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]);
+    v[c] = add ? f2_fma(g, make_float2(w, w), v[c]) : f2_mul(g, make_float2(w, w));
+  }
+}
+
+__device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,
+                                                          bool valid, int vbase, float fx, float fy, float fz,
+                                                          float g0, float g1) {
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? vbase : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  const bool leader = valid && (rank % (APMG_GATHER_CAP + 1)) == 0;
+  // this leader's members: the next CAP set bits of peers above this lane
+  unsigned rest = 0u;
+  if (leader) {
+    unsigned above = peers & (0xfffffffeu << lane);
+#pragma unroll
+    for (int k = 0; k < APMG_GATHER_CAP; ++k) {
+      rest |= above & (0u - above);  // lowest set bit
+      above &= above - 1u;
+    }
+  }
+  float2 v[8];
+  corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
+#pragma unroll 1
+  for (int k = 0; k < APMG_GATHER_CAP && __any_sync(0xffffffffu, rest != 0u); ++k) {
+    const int src = rest ? __ffs(rest) - 1 : lane;
+    const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
+    const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
+                ez = __shfl_sync(0xffffffffu, fz, src);
+    if (rest) {
+      corner_terms(make_float2(h0, h1), ex, ey, ez, v, true);
+      rest &= rest - 1u;
+    }
+  }
+  if (!leader) return;
+  if (md.grad_pairs) {
+    float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
+#pragma unroll
+    for (int c = 0; c < 8; c += 2)
+      atomicAdd(base + (c >> 2) * md.H * md.W + ((c >> 1) & 1) * md.W,
+                make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y));
+    return;
+  }
+  const int sy = 2 * md.W, sz = 2 * md.H * md.W;
+  float* base = dgrid + (size_t(vbase) << 1);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) atomic_add2(base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1), v[c].x, v[c].y);
+}
+
 template <typename T>
 __device__ __forceinline__ void scatter_grid_point(const ModelDev<T>& md, T* __restrict__ dgrid, int m, T x0, T x1,
                                                    T x2, const T* g, int g_stride) {

@@ -15,7 +15,7 @@
 //   dz1 *= [h1 > 0] -> bf16x3
 //   gF = dz1 W1       (B = W1 MN-major) M=64 N=128 K=64, 3 products
 //   dW1 += dz1^T F    (A, B MN-major)   M=64 N=128 K=64, 3 products, TMEM-resident sum
-//   scatter     gF -> channel-last grid gradients (warp-aggregated float2 RED), interleaved
+//   scatter     gF -> x-pair grid gradients (warp-aggregated float4 RED), interleaved
 //               with the encode of the next tile
 // The backward products keep ~2^-16 relative accuracy per term (gradient gate 1e-3); the
 // forward keeps the f32-level 6-product split (forward / loss gates).
@@ -120,7 +120,10 @@ __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const A
     const bool valid = vbase >= 0 && p < cnt;
     float2 g = make_float2(0.f, 0.f);
     if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
-    if (a.aggregate)
+    if (a.aggregate == 2)
+      scatter_vertex_warp_gather(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+                                 __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+    else if (a.aggregate)
       scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
                               __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
     else if (valid)
@@ -534,7 +537,8 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
   }
   const char* ea = getenv("APMG_SCATTER_AGG");
   const char* es = getenv("APMG_TC_STAMPS");
-  tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, (ea && ea[0] == '0') ? 0 : 1,
+  // APMG_SCATTER_AGG: 0 plain REDs, 1 tree-reduced, 2 (default) leader-gather aggregation
+  tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, ea ? atoi(ea) : 2,
                (es && es[0] == '1') ? 1 : 0, 0};
   if (const char* sk = getenv("APMG_TC_SKIP")) a.skip = atoi(sk);
   APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
