@@ -68,6 +68,17 @@ __device__ __forceinline__ double local_coord(double x0, double x1, double x2, d
   return add_rn(add_rn(add_rn(mul_rn(x0, a0), mul_rn(x2, a2)), mul_rn(x1, a1)), t);
 }
 
+// local_coord<float> for two points at once: scalar products, packed sums (FADD2, each half
+// rounded as the scalar add).  The products stay scalar on purpose: ptxas (CUDA 12.9)
+// contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite the explicit rounding modifiers,
+// which would change the rounding of the local coordinates (and flip inside/outside tests).
+__device__ __forceinline__ float2 mul_s2(float2 x, float a) { return make_float2(__fmul_rn(x.x, a), __fmul_rn(x.y, a)); }
+__device__ __forceinline__ float2 local_coord2(float2 x0, float2 x1, float2 x2, float a0, float a1, float a2,
+                                               float t) {
+  const float2 p = __fadd2_rn(__fadd2_rn(mul_s2(x0, a0), mul_s2(x1, a1)), mul_s2(x2, a2));
+  return __fadd2_rn(p, make_float2(t, t));
+}
+
 // Interpolation terms of one point in one grid.
 struct Cell {
   int ix, iy, iz;
@@ -84,6 +95,16 @@ __device__ __forceinline__ void axis_term(float l, int n, int& i0, double& f) {
   const int i = min(max(int(floorf(u)), 0), n - 2);
   i0 = i;
   f = static_cast<double>(__fsub_rn(u, float(i)));
+}
+// axis_term<float> for two points: (l + 1) * 0.5 packed, the rest scalar (see local_coord2:
+// a packed multiply feeding the fraction's subtraction would be contracted)
+__device__ __forceinline__ void axis_term2(float2 l, int n, int& i0, int& i1, float& f0, float& f1) {
+  const float2 h = __fmul2_rn(__fadd2_rn(l, make_float2(1.0f, 1.0f)), make_float2(0.5f, 0.5f));
+  const float u0 = __fmul_rn(h.x, float(n - 1)), u1 = __fmul_rn(h.y, float(n - 1));
+  i0 = min(max(int(floorf(u0)), 0), n - 2);
+  i1 = min(max(int(floorf(u1)), 0), n - 2);
+  f0 = __fsub_rn(u0, float(i0));
+  f1 = __fsub_rn(u1, float(i1));
 }
 __device__ __forceinline__ void axis_term(double l, int n, int& i0, double& f) {
   const double u = mul_rn(mul_rn(add_rn(l, 1.0), 0.5), double(n - 1));

@@ -216,43 +216,49 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   uint32_t phase = 0;
   uint32_t h1pos = 0;  // [h1 > 0] bits of this thread's 8 elements (epilogue 1 -> dz1 epilogue)
 
+  // encode of grids warp + NW (2 jq), warp + NW (2 jq + 1) for points lane, lane + 32: the two
+  // points of a grid share its transform and run in packed fp32x2 arithmetic
   auto encode_group = [&](const float* cX, int jq) {
-    const float xa[2][3] = {{cX[3 * lane], cX[3 * lane + 1], cX[3 * lane + 2]},
-                            {cX[3 * (lane + 32)], cX[3 * (lane + 32) + 1], cX[3 * (lane + 32) + 2]}};
+    const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
+    const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
+    const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
     uint32_t cache[16];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = 2 * jq + (u >> 1), h = u & 1;
-      const int m = warp + NW * j, p = lane + 32 * h;
+    for (int jj = 0; jj < 2; ++jj) {
+      const int m = warp + NW * (2 * jq + jj);
       const float* tf = sTF + 12 * m;
-      const float l0 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[0], tf[1], tf[2], tf[3]);
-      const float l1 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[4], tf[5], tf[6], tf[7]);
-      const float l2 = local_coord(xa[h][0], xa[h][1], xa[h][2], tf[8], tf[9], tf[10], tf[11]);
-      const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
-      int ix, iy, iz;
-      double fxd, fyd, fzd;
-      axis_term(l0, md.W, ix, fxd);
-      axis_term(l1, md.H, iy, fyd);
-      axis_term(l2, md.D, iz, fzd);
-      const float fx = float(fxd), fy = float(fyd), fz = float(fzd);
-      const int vbase = inside ? ((m * md.D + iz) * md.H + iy) * md.W + ix : -1;
-      float f0 = 0.f, f1 = 0.f;
-      if (inside && !(a.skip & 2)) {
-        if (md.gridx)
-          interp_pairx_f32(md.gridx, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
-        else
-          interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx, fy, fz, f0, f1);
+      const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
+      const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
+      const float2 l2 = local_coord2(X0, X1, X2, tf[8], tf[9], tf[10], tf[11]);
+      int ix[2], iy[2], iz[2];
+      float fx[2], fy[2], fz[2];
+      axis_term2(l0, md.W, ix[0], ix[1], fx[0], fx[1]);
+      axis_term2(l1, md.H, iy[0], iy[1], fy[0], fy[1]);
+      axis_term2(l2, md.D, iz[0], iz[1], fz[0], fz[1]);
+      const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 2 * jj + h, p = lane + 32 * h;
+        const bool inside = (fabsf(la[h][0]) <= 1.f) && (fabsf(la[h][1]) <= 1.f) && (fabsf(la[h][2]) <= 1.f);
+        const int vbase = inside ? ((m * md.D + iz[h]) * md.H + iy[h]) * md.W + ix[h] : -1;
+        float f0 = 0.f, f1 = 0.f;
+        if (inside && !(a.skip & 2)) {
+          if (md.gridx)
+            interp_pairx_f32(md.gridx, md.W, md.H * md.W, vbase, fx[h], fy[h], fz[h], f0, f1);
+          else
+            interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx[h], fy[h], fz[h], f0, f1);
+        }
+        cache[4 * u] = uint32_t(vbase);
+        cache[4 * u + 1] = __float_as_uint(fx[h]);
+        cache[4 * u + 2] = __float_as_uint(fy[h]);
+        cache[4 * u + 3] = __float_as_uint(fz[h]);
+        uint32_t hw, mw, lw;
+        umma::split2_bf16x3(f0, f1, hw, mw, lw);
+        const uint32_t o = umma::cm16_offset(p, 2 * m, 64);
+        *reinterpret_cast<uint32_t*>(F + o) = hw;
+        *reinterpret_cast<uint32_t*>(F + PL64x128 + o) = mw;
+        *reinterpret_cast<uint32_t*>(F + 2 * PL64x128 + o) = lw;
       }
-      cache[4 * u] = uint32_t(vbase);
-      cache[4 * u + 1] = __float_as_uint(fx);
-      cache[4 * u + 2] = __float_as_uint(fy);
-      cache[4 * u + 3] = __float_as_uint(fz);
-      uint32_t hw, mw, lw;
-      umma::split2_bf16x3(f0, f1, hw, mw, lw);
-      const uint32_t o = umma::cm16_offset(p, 2 * m, 64);
-      *reinterpret_cast<uint32_t*>(F + o) = hw;
-      *reinterpret_cast<uint32_t*>(F + PL64x128 + o) = mw;
-      *reinterpret_cast<uint32_t*>(F + 2 * PL64x128 + o) = lw;
     }
     umma::tmem_st16(tmem_cache + 16 * jq, cache);
   };
