@@ -114,8 +114,8 @@ __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const A
   umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int j = 2 * jq + (u >> 1), h = u & 1;
-    const int m = warp + NW * j, p = lane + 32 * h;
+    const int h = u & 1;
+    const int m = 2 * warp + 32 * jq + (u >> 1), p = lane + 32 * h;  // encode_group's pair order
     const int vbase = int(cache[4 * u]);
     const bool valid = vbase >= 0 && p < cnt;
     float2 g = make_float2(0.f, 0.f);
@@ -216,16 +216,18 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   uint32_t phase = 0;
   uint32_t h1pos = 0;  // [h1 > 0] bits of this thread's 8 elements (epilogue 1 -> dz1 epilogue)
 
-  // encode of grids warp + NW (2 jq), warp + NW (2 jq + 1) for points lane, lane + 32: the two
-  // points of a grid share its transform and run in packed fp32x2 arithmetic
+  // encode of grids 2 warp + 32 jq + {0, 1} for points lane, lane + 32: the two points of a grid
+  // share its transform and run in packed fp32x2 arithmetic; the two grids' four features of a
+  // point are adjacent in F (one 8-byte store per plane)
   auto encode_group = [&](const float* cX, int jq) {
     const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
     const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
     const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
     uint32_t cache[16];
+    uint32_t fw[2][2][3];  // [grid jj][point h][plane]
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
-      const int m = warp + NW * (2 * jq + jj);
+      const int m = 2 * warp + 32 * jq + jj;
       const float* tf = sTF + 12 * m;
       const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
       const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
@@ -252,13 +254,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
         cache[4 * u + 1] = __float_as_uint(fx[h]);
         cache[4 * u + 2] = __float_as_uint(fy[h]);
         cache[4 * u + 3] = __float_as_uint(fz[h]);
-        uint32_t hw, mw, lw;
-        umma::split2_bf16x3(f0, f1, hw, mw, lw);
-        const uint32_t o = umma::cm16_offset(p, 2 * m, 64);
-        *reinterpret_cast<uint32_t*>(F + o) = hw;
-        *reinterpret_cast<uint32_t*>(F + PL64x128 + o) = mw;
-        *reinterpret_cast<uint32_t*>(F + 2 * PL64x128 + o) = lw;
+        umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
       }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t o = umma::cm16_offset(lane + 32 * h, 4 * warp + 64 * jq, 64);
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl)
+        *reinterpret_cast<uint2*>(F + pl * PL64x128 + o) = make_uint2(fw[0][h][pl], fw[1][h][pl]);
     }
     umma::tmem_st16(tmem_cache + 16 * jq, cache);
   };
