@@ -312,6 +312,37 @@ __device__ __forceinline__ void bump32(const float* a, float x0, float x1, float
   bump = (q <= 700.f) ? __expf(-q) : 0.f;
 }
 
+// bump32 for two points at once in packed fp32x2 (FFMA2 per half = the scalar fmaf), p = 10
+// (the flat-top exponent of the APMG models; other p take the scalar kernels).  s = l^2 is
+// clamped at 4: a point that far outside has bump exactly 0 either way, and the clamp keeps
+// its local^(2p-1) term finite so the packed gradient needs no per-half branch.
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ void bump32x2(const float* a, float2 x0, float2 x1, float2 x2, float2& bump, float2* l,
+                                         float2* lp) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    l[d] = f2fma(bc2(a[4 * d]), x0, f2fma(bc2(a[4 * d + 1]), x1, f2fma(bc2(a[4 * d + 2]), x2, bc2(a[4 * d + 3]))));
+  float2 q = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    float2 s = f2mul(l[d], l[d]);
+    s = make_float2(fminf(s.x, 4.f), fminf(s.y, 4.f));
+    const float2 s2 = f2mul(s, s), s4 = f2mul(s2, s2), s8 = f2mul(s4, s4);
+    const float2 r = f2mul(s8, s);
+    lp[d] = f2mul(l[d], r);
+    q = f2fma(r, s, q);
+  }
+  const float2 e = f2mul(q, bc2(-1.4426950408889634f));
+  bump = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+}
+
 __device__ void stage_transforms32(const float* __restrict__ tf, int M, float* s_tf) {
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     double a[12];
@@ -347,6 +378,76 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_rho32(const float* __rest
     rho[i] = double(r);
     srho += double(r);
     if (err) serr += double(err[i]);
+  }
+  srho = block_sum(srho, red);
+  serr = block_sum(serr, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = srho;
+    part[2 * blockIdx.x + 1] = serr;
+  }
+}
+
+// k_dens_rho32 with two consecutive points per thread (p = 10)
+// stage_transforms32 with a 16-float stride (16-byte aligned rows)
+__device__ void stage_transforms32_16(const float* __restrict__ tf, int M, float* s_tf) {
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    double a[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) a[e] = double(tf[16 * m + e]);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) s_tf[16 * m + e] = float(a[e]);
+    const double c0 = a[5] * a[10] - a[6] * a[9], c1 = a[6] * a[8] - a[4] * a[10], c2 = a[4] * a[9] - a[5] * a[8];
+    s_tf[16 * m + 12] = float(fabs(a[0] * c0 + a[1] * c1 + a[2] * c2));
+    s_tf[16 * m + 13] = s_tf[16 * m + 14] = s_tf[16 * m + 15] = 0.f;
+  }
+}
+
+template <typename TE>
+__global__ void __launch_bounds__(kDensThreads) k_dens_rho32x2(const float* __restrict__ tf, int M,
+                                                               const float* __restrict__ x,
+                                                               const TE* __restrict__ err, int64_t n,
+                                                               double* __restrict__ rho, double* __restrict__ part,
+                                                               const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  extern __shared__ float4 s_tf4[];  // [M][4]: rows of A|t, then (det, -, -, -): 4 LDS.128 per grid
+  __shared__ double red[32];
+  stage_transforms32_16(tf, M, reinterpret_cast<float*>(s_tf4));
+  __syncthreads();
+  double srho = 0.0, serr = 0.0;
+  const int64_t npair = (n + 1) >> 1;
+  for (int64_t ip = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ip < npair;
+       ip += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = 2 * ip;
+    const bool two = i + 1 < n;
+    float2 X0, X1, X2;
+    if (two) {
+      const float2* xp = reinterpret_cast<const float2*>(x + 3 * i);
+      const float2 f0 = xp[0], f1 = xp[1], f2 = xp[2];
+      X0 = make_float2(f0.x, f1.y);
+      X1 = make_float2(f0.y, f2.x);
+      X2 = make_float2(f1.x, f2.y);
+    } else {
+      X0 = bc2(x[3 * i]);
+      X1 = bc2(x[3 * i + 1]);
+      X2 = bc2(x[3 * i + 2]);
+    }
+    float2 r = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int m = 0; m < M; ++m) {
+      const float4 t0 = s_tf4[4 * m], t1 = s_tf4[4 * m + 1], t2 = s_tf4[4 * m + 2], t3 = s_tf4[4 * m + 3];
+      const float a[13] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w, t2.x, t2.y, t2.z, t2.w, t3.x};
+      float2 b, l[3], lp[3];
+      bump32x2(a, X0, X1, X2, b, l, lp);
+      r = f2fma(bc2(a[12]), b, r);
+    }
+    rho[i] = double(r.x);
+    srho += double(r.x);
+    if (err) serr += double(err[i]);
+    if (two) {
+      rho[i + 1] = double(r.y);
+      srho += double(r.y);
+      if (err) serr += double(err[i + 1]);
+    }
   }
   srho = block_sum(srho, red);
   serr = block_sum(serr, red);
@@ -475,6 +576,63 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_grad32c(const float* __re
   for (int e = threadIdx.x; e < 13 * M; e += blockDim.x) part[int64_t(blockIdx.x) * 13 * M + e] = s_acc[e];
 }
 
+// k_dens_grad32c with two staged points per lane and step (p = 10): float2 accumulators
+__global__ void __launch_bounds__(kDensThreads) k_dens_grad32cx2(const float* __restrict__ tf, int M,
+                                                                 const float* __restrict__ x, int64_t n,
+                                                                 const float* __restrict__ drho, int ch,
+                                                                 double* __restrict__ part, const TrainCtl* ctl) {
+  if (ctl && (ctl->skip || !ctl->density_on)) return;
+  extern __shared__ float4 sP[];                                   // [ch <= kGradCH] (x0, x1, x2, d_rho)
+  double* s_acc = reinterpret_cast<double*>(sP + kGradCH);         // [M][13]
+  float* s_tf = reinterpret_cast<float*>(s_acc + 13 * M);          // [M][13]
+  stage_transforms32(tf, M, s_tf);
+  for (int e = threadIdx.x; e < 13 * M; e += blockDim.x) s_acc[e] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int64_t c0 = int64_t(blockIdx.x) * ch; c0 < n; c0 += int64_t(gridDim.x) * ch) {
+    const int cnt = int(min64(ch, n - c0));
+    __syncthreads();  // previous chunk consumed, transforms / accumulators staged
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int64_t g = c0 + i;
+      sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], drho[g]);
+    }
+    __syncthreads();
+    for (int m = warp; m < M; m += nw) {
+      float a[13];
+#pragma unroll
+      for (int e = 0; e < 13; ++e) a[e] = s_tf[13 * m + e];
+      float2 acc[13];
+#pragma unroll
+      for (int e = 0; e < 13; ++e) acc[e] = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int i = lane; i < cnt; i += 64) {
+        const float4 q0 = sP[i];
+        const float4 q1 = i + 32 < cnt ? sP[i + 32] : make_float4(0.f, 0.f, 0.f, 0.f);  // d_rho 0: no share
+        const float2 X0 = make_float2(q0.x, q1.x), X1 = make_float2(q0.y, q1.y), X2 = make_float2(q0.z, q1.z);
+        float2 b, l[3], lp[3];
+        bump32x2(a, X0, X1, X2, b, l, lp);
+        const float2 w = f2mul(make_float2(q0.w, q1.w), b);
+        const float2 sc = f2mul(bc2(a[12]), w);
+        acc[0] = __fadd2_rn(acc[0], w);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const float2 sl = f2mul(sc, lp[d]);
+          acc[1 + 3 * d] = f2fma(sl, X0, acc[1 + 3 * d]);
+          acc[2 + 3 * d] = f2fma(sl, X1, acc[2 + 3 * d]);
+          acc[3 + 3 * d] = f2fma(sl, X2, acc[3 + 3 * d]);
+          acc[10 + d] = __fadd2_rn(acc[10 + d], sl);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 13; ++e) {
+        const double v = warp_sum(double(acc[e].x) + double(acc[e].y));
+        if (lane == 0) s_acc[13 * m + e] += v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 13 * M; e += blockDim.x) part[int64_t(blockIdx.x) * 13 * M + e] = s_acc[e];
+}
+
 static size_t grad32c_smem(int M) { return sizeof(float4) * kGradCH + size_t(13) * M * (sizeof(double) + sizeof(float)); }
 
 struct DensPlan {
@@ -502,6 +660,11 @@ size_t density_ws_bytes(int M, int64_t n) {
   return c.used + 256;
 }
 
+static bool packed_density() {  // APMG_DENSITY_X2=0: the one-point-per-lane kernels (A/B)
+  const char* e = getenv("APMG_DENSITY_X2");
+  return !(e && e[0] == '0');
+}
+
 template <typename T, typename TE>
 int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, double* loss, T* dtf,
                    double* rho_total, T* adam_m, T* adam_v, void* ws, size_t wsb, const TrainCtl* ctl,
@@ -527,8 +690,16 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
       const size_t smem32 = size_t(13) * M * sizeof(float);
       APMG_CUDA_TRY(
           cudaFuncSetAttribute(k_dens_rho32<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem32)));
-      APMG_LAUNCH("density_rho", k_dens_rho32<TE>, d.nb1, kDensThreads, smem32, st, tf, M, p, x, err, n, rho, part1,
-                  ctl);
+      if (p == 10 && packed_density()) {
+        const size_t smem16 = size_t(16) * M * sizeof(float);
+        APMG_CUDA_TRY(
+            cudaFuncSetAttribute(k_dens_rho32x2<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem16)));
+        APMG_LAUNCH("density_rho", k_dens_rho32x2<TE>, d.nb1, kDensThreads, smem16, st, tf, M, x, err, n, rho, part1,
+                    ctl);
+      } else {
+        APMG_LAUNCH("density_rho", k_dens_rho32<TE>, d.nb1, kDensThreads, smem32, st, tf, M, p, x, err, n, rho,
+                    part1, ctl);
+      }
     }
   }
   if (!fast32) {
@@ -547,10 +718,17 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
       APMG_LAUNCH("density_drho", k_dens_drho32, d.nb1, kDensThreads, 0, st, d_s, n, stats, drho, ctl);
       if (M <= kGradMaxM) {
         const size_t sm = grad32c_smem(M);
-        APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_grad32c, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         const int ch = int(std::min<int64_t>(kGradCH, ceil_div(n, d.nbg)));  // one balanced chunk per block
-        APMG_LAUNCH("density_grad", k_dens_grad32c, d.nbg, kDensThreads, sm, st, tf, M, p, x, n, drho, ch, part3,
-                    ctl);
+        if (p == 10 && packed_density()) {
+          APMG_CUDA_TRY(
+              cudaFuncSetAttribute(k_dens_grad32cx2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+          APMG_LAUNCH("density_grad", k_dens_grad32cx2, d.nbg, kDensThreads, sm, st, tf, M, x, n, drho, ch, part3,
+                      ctl);
+        } else {
+          APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_grad32c, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+          APMG_LAUNCH("density_grad", k_dens_grad32c, d.nbg, kDensThreads, sm, st, tf, M, p, x, n, drho, ch, part3,
+                      ctl);
+        }
         parts = d.nbg;
       } else {
         APMG_LAUNCH("density_grad", k_dens_grad32, dim3(d.chunks, M), kDensThreads, 0, st, tf, M, p, x, n, drho,

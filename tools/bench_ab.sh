@@ -8,5 +8,6 @@ import json, sys
 d = json.loads(sys.stdin.read())
 e = d.get('e2e') or {}
 print('$var=$v', round(d['value'] / 1e6, 1), 'M/s', round(d['ms_per_step'], 4), 'ms', 'e2e', round((e.get('value') or 0) / 1e6, 1),
-      {k: v for k, v in list(d.get('kernel_share', {}).items())[:4]})"
+      {k: v for k, v in list(d.get('kernel_share', {}).items())[:4]}, 'sum', round(sum(d.get('kernel_share', {}).values()), 4))
+if '$AB_ALL' == '1': print('   ', d.get('kernel_share'))"
 done
