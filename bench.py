@@ -358,7 +358,8 @@ def main():
         e2e = {"value": world * K * BATCH / dt, "unit": METRIC,
                "h2d_bytes_per_step": int((host_vol.data.nbytes + params_b + 16 * K) / K),
                "d2h_bytes_per_step": int((params_b + 24 * K) / K),
-               "setup_ms": round(1e3 * log2.setup_seconds, 2), "wall_ms": round(1e3 * dt, 2),
+               "setup_ms": round(1e3 * log2.setup_seconds, 2), "setup_split_ms": log2.setup_ms,
+               "wall_ms": round(1e3 * dt, 2),
                "note": f"paper_2308_02494_b200.train_single(host model, host Volume, iterations={K}): "
                        f"volume + parameter upload, device loop, parameter + log download"}
 

@@ -196,8 +196,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   __syncthreads();
   umma::fence_after_sync();
 
-  const uint32_t sW1 = umma::smem_u32(W1), sW2 = umma::smem_u32(W2), sF = umma::smem_u32(F),
-                 sH1 = umma::smem_u32(H1), sDZ2 = umma::smem_u32(DZ2), sDZ1 = umma::smem_u32(DZ1);
+  const uint32_t base16 = umma::smem_u32(sm) >> 4;  // descriptors: base16 + compile-time fields
   const uint32_t id_kk = umma::idesc_bf16(64, 64, false, false);      // A, B K-major
   const uint32_t id_kmn = umma::idesc_bf16(64, 64, false, true);      // B MN-major
   const uint32_t id_kmn128 = umma::idesc_bf16(64, 128, false, true);  // B MN-major, N=128
@@ -273,8 +272,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     for (int kk = k0; kk < k1; ++kk)
 #pragma unroll
       for (int q = 0; q < 6; ++q)
-        umma::mma_bf16(TA, umma::desc_kmajor(sF + kPA(q) * PL64x128, 64, kk),
-                       umma::desc_kmajor(sW1 + kPB(q) * PL64x128, 64, kk), id_kk, (kk | q) ? 1u : 0u);
+        umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_F + kPA(q) * PL64x128, 64, kk),
+                         umma::kmajor_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kk, (kk | q) ? 1u : 0u);
     if (last) umma::commit(bar);
   };
   auto encode_tile = [&](const float* cX, int scatter_cnt, int64_t prefetch_tile, int prefetch_slot) {
@@ -333,8 +332,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       for (int kk = 0; kk < HID / 16; ++kk)
 #pragma unroll
         for (int q = 0; q < 6; ++q)
-          umma::mma_bf16(TB, umma::desc_kmajor(sH1 + kPA(q) * PL64x64, 64, kk),
-                         umma::desc_kmajor(sW2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
+          umma::mma_bf16_c(TB, base16, umma::kmajor_c(OFF_H1 + kPA(q) * PL64x64, 64, kk),
+                           umma::kmajor_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
       umma::commit(bar);
     }
     umma::mbar_wait(bar, phase);
@@ -410,13 +409,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       for (int kk = 0; kk < HID / 16; ++kk)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          umma::mma_bf16(TA, umma::desc_kmajor(sDZ2 + kPA(q) * PL64x64, 64, kk),
-                         umma::desc_mnmajor16(sW2 + kPB(q) * PL64x64, 64, kk), id_kmn, (kk | q) ? 1u : 0u);
+          umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
+                           umma::mnmajor16_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kmn, (kk | q) ? 1u : 0u);
       for (int kk = 0; kk < P / 16; ++kk)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          umma::mma_bf16(TDW2, umma::desc_mnmajor16(sDZ2 + kPA(q) * PL64x64, 64, kk),
-                         umma::desc_mnmajor16(sH1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
+          umma::mma_bf16_c(TDW2, base16, umma::mnmajor16_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
+                           umma::mnmajor16_c(OFF_H1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
       umma::commit(bar);
     }
     umma::mbar_wait(bar, phase);
@@ -446,13 +445,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       for (int kk = 0; kk < HID / 16; ++kk)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          umma::mma_bf16(TA, umma::desc_kmajor(sDZ1 + kPA(q) * PL64x64, 64, kk),
-                         umma::desc_mnmajor16(sW1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
+          umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
+                           umma::mnmajor16_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
       for (int kk = 0; kk < P / 16; ++kk)
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          umma::mma_bf16(TDW1, umma::desc_mnmajor16(sDZ1 + kPA(q) * PL64x64, 64, kk),
-                         umma::desc_mnmajor16(sF + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
+          umma::mma_bf16_c(TDW1, base16, umma::mnmajor16_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
+                           umma::mnmajor16_c(OFF_F + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
       umma::commit(bar);
     }
     umma::mbar_wait(bar, phase);

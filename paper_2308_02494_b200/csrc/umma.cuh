@@ -118,6 +118,32 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// Descriptors as (runtime base) + (compile-time fields): DescC holds the low word without
+// the base, (offset >> 4) | (LBO >> 4) << 16, and the high word (SBO >> 4) | version.  The
+// issuing thread adds base16 = (smem window address >> 4) per operand -- one integer add per
+// MMA operand instead of re-deriving and masking every field (the single issuing thread is
+// on the critical path of the small M=64 products).  Valid while offsets stay < 256 KB.
+struct DescC {
+  uint32_t lo, hi;
+};
+__host__ __device__ constexpr DescC kmajor_c(uint32_t off, int R, int kk) {
+  return DescC{((off + uint32_t(kk) * 2u * uint32_t(R * 16)) >> 4) | ((uint32_t(R * 16) >> 4) << 16),
+               (128u >> 4) | (1u << 14)};
+}
+__host__ __device__ constexpr DescC mnmajor16_c(uint32_t off, int R, int kk) {
+  return DescC{((off + uint32_t(kk) * 256u) >> 4) | ((128u >> 4) << 16), (uint32_t(R * 16) >> 4) | (1u << 14)};
+}
+__device__ __forceinline__ void mma_bf16_c(uint32_t d_tmem, uint32_t base16, DescC a, DescC b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(base16 + a.lo), "r"(a.hi), "r"(base16 + b.lo), "r"(b.hi), "r"(idesc), "r"(accumulate));
+}
+
 // x = h + m + l in bf16 (8+8+8 significant bits: the f32 significand, exponent permitting)
 __device__ __forceinline__ void split_bf16x3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
   h = __float2bfloat16_rn(x);

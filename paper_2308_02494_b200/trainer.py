@@ -75,6 +75,7 @@ class TrainLog:
     iterations_run: int = 0
     wall_seconds: float = 0.0
     setup_seconds: float = 0.0  # volume / parameter upload and session creation (train_single)
+    setup_ms: dict = field(default_factory=dict)  # its split (TrainSession.setup_ms)
 
     def records(self):
         stop = self.transform_stop_iteration
@@ -151,6 +152,7 @@ class TrainSession:
 
     def __init__(self, model: ApmgModel, volume: Volume, cfg: TrainConfig):
         t = L.require_cuda()
+        t0 = time.perf_counter()
         self.model, self.volume, self.cfg = model, volume, cfg
         dt = model.dtype
         if dt not in (np.float32, np.float64):
@@ -167,7 +169,10 @@ class TrainSession:
         self.main[o[2]:o[2] + self.dm.w2.numel()].copy_(self.dm.w2.reshape(-1))
         self.main[o[3]:o[3] + self.dm.w3.numel()].copy_(self.dm.w3.reshape(-1))
         self.tf = self.dm.transforms
+        t1 = time.perf_counter()
         self.vol = volume.device_data()
+        t.cuda.current_stream().synchronize()
+        t2 = time.perf_counter()
         key = np.random.Philox(cfg.seed).state["state"]["key"]
         self.ccfg = L.ApmgTrainConfigC(
             cfg.iterations, cfg.batch_size, cfg.lr_main, cfg.lr_transform, cfg.delay_start,
@@ -184,6 +189,9 @@ class TrainSession:
                                           L.stream_handle()), "train_create")
         self.state = st
         self._torch = t
+        # host-side setup split (ms): parameters, volume upload, workspace + create (synchronised)
+        self.setup_ms = {"params": 1e3 * (t1 - t0), "volume": 1e3 * (t2 - t1),
+                         "create": 1e3 * (time.perf_counter() - t2)}
 
     def run(self, n: int) -> None:
         L.check(L.lib().apmg_train_run(self.state, int(n), L.stream_handle()), "train_run")
@@ -294,6 +302,7 @@ def train_single(model: ApmgModel, volume: Volume, cfg: TrainConfig, on_iteratio
         sess.close()
     log.wall_seconds = time.perf_counter() - t0
     log.setup_seconds = setup
+    log.setup_ms = {k: round(v, 2) for k, v in sess.setup_ms.items()}
     return model, log
 
 
