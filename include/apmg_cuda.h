@@ -60,6 +60,28 @@ int apmg_device_sm_count(void);
 /* number of kernels this library launched since load (evidence for bench.py) */
 uint64_t apmg_launch_count(void);
 /* per-kernel CUDA-event timing on the launching stream (bench roofline). */
+/* ---- renderer field-query path (render.py) ---------------------
+ * ray_box_hits (render.py:206-226): slab test of rays (origin HOST f64[3], dirs [n][3] f64)
+ * against [-1,1]^3 -> enter / exit [n] f64, hit [n] u8. */
+int apmg_ray_box_hits(const double* origin, const double* dirs, int64_t n, double* enter, double* exit_t,
+                      uint8_t* hit, void* stream);
+/* _render_rays sample points (render.py:286-290) of the rays ray_ids [nr] (i64, hit rays):
+ * pts [nr][samples][3] f32 = clip(origin + ((s+0.5) dt + enter) dir, -1, 1), dt [nr] f64. */
+int apmg_ray_points(const double* origin, const double* dirs, const int64_t* ray_ids, int64_t nr, int32_t samples,
+                    float* pts, double* dt, void* stream);
+/* TransferFunction.apply (render.py:126-138): values [n] f32 -> rgba [n][4] f32 through the
+ * baked LUT [256][4] f32; tf = HOST f32[5] {vmin, vmax - vmin, lo, hi - lo, vmax > vmin}. */
+int apmg_tf_apply(const float* values, int64_t n, const float* lut, const float* tf, float* rgba, void* stream);
+/* _render_rays tail (render.py:292-295): field values [nr][samples] -> transfer function ->
+ * front-to-back composite (render.py:240-264) -> out[ray_ids[j]] (RGBA f32; ray_ids NULL:
+ * out[j]).  comp = HOST f32[7] {reference_step, background[4], early_exit_alpha, early_on}. */
+int apmg_composite_values(const float* values, const double* dt, const int64_t* ray_ids, int64_t nr,
+                          int32_t samples, const float* lut, const float* tf, const float* comp, float* out,
+                          void* stream);
+/* _composite of RGBA samples [nr][count][4] with per-ray steps [nr] f32 (composite_ray). */
+int apmg_composite_rgba(const float* samples, const float* steps, int64_t nr, int32_t count, const float* comp,
+                        float* out, void* stream);
+
 /* Release the device blocks the library caches between sessions (the bricked volume
  * copy of apmg_train_create).  No reference counterpart (memory management of the CUDA
  * path). */

@@ -40,6 +40,8 @@ size_t recon_ws_bytes(int F, int64_t n);
 bool recon_tc_eligible(const ModelDev<float>& md);
 // launch_recon<float> on this model shape runs the bf16x3 tcgen05 kernel (recon_tc16.cu)
 bool recon_uses_tc16(const apmg_model& m);
+// grid for grid-stride elementwise kernels: enough 256-thread blocks for n, at most per_sm per SM
+int elementwise_grid(int64_t n, int per_sm);
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
 int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,

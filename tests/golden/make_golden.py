@@ -319,6 +319,59 @@ def gen_psnr():
     np.savez_compressed(OUT / "psnr.npz", **out)
 
 
+def gen_render():
+    """Renderer field-query path (render.py): ray/box hits incl. parallel and inside rays,
+    transfer-function lookups, single-ray composites, and full frames of a volume field, a
+    small model field and a flagship-shaped model field (non-trivial TF, window, early exit)."""
+    from apmg import render as rr
+    out = {}
+    # ray / box
+    origin = np.array([0.3, -0.2, 2.5])
+    dirs = np.array([[0.0, 0.0, -1.0], [0.0, 1.0, 0.0], [0.6, 0.0, -0.8], [0.0, 0.0, 1.0],
+                     [1e-300, 0.0, -1.0], [-0.1, 0.05, -0.99]])
+    dirs[-1] /= np.linalg.norm(dirs[-1])
+    e, x, h = rr.ray_box_hits(origin, dirs)
+    out.update(rb_origin=origin, rb_dirs=dirs, rb_enter=e, rb_exit=x, rb_hit=h)
+    e, x, h = rr.ray_box_hits(np.zeros(3), np.array([[1.0, 0.0, 0.0], [0.0, 0.0, -1.0]]))
+    out.update(rb0_enter=e, rb0_exit=x, rb0_hit=h)
+    e, x, h = rr.ray_box_hits(np.array([0.0, 2.0, 5.0]), np.array([[0.0, 0.0, -1.0]]))
+    out.update(rb1_hit=h)
+    # transfer function
+    tf = rr.TransferFunction(
+        color_points=[(0.0, (0.0, 0.0, 0.1)), (0.4, (1.0, 0.2, 0.0)), (1.0, (1.0, 1.0, 1.0))],
+        opacity_points=[(0.0, 0.0), (0.3, 0.05), (0.7, 0.9), (1.0, 0.2)], window=(0.1, 0.8))
+    vals = np.random.default_rng(5).uniform(-0.7, 1.8, 4096).astype(np.float32)
+    vals[:4] = [-0.5, 1.5, 0.5, np.float32(-0.5 + 0.1 * 2.0)]
+    out.update(tf_values=vals, tf_lut=tf.lut, tf_rgba=tf.apply(vals, -0.5, 1.5))
+    # composites
+    rng = np.random.default_rng(6)
+    samples = rng.uniform(0, 1, (64, 4)).astype(np.float32)
+    out.update(comp_samples=samples,
+               comp_a=rr.composite_ray(samples, step=0.01, reference_step=0.02),
+               comp_b=rr.composite_ray(samples, step=0.013, reference_step=0.02, background=(0.2, 0.3, 0.4, 0.5),
+                                       early_exit_alpha=None),
+               comp_c=rr.composite_ray(samples[:7], step=0.05, early_exit_alpha=0.5))
+    # frames
+    vol = rvol.synth_volume((17, 13, 11), [rvol.BlobSpec(center=(0.2, 0.0, -0.1), sigma=(0.4, 0.5, 0.3))])
+    cam = rr.Camera(eye=(1.5, 1.0, 2.5), look_at=(0.0, 0.0, 0.0), width=12, height=10)
+    cfg = rr.RenderConfig(samples_per_ray=16)
+    out.update(vol_data=vol.data, vol_dims=np.array(vol.dims),
+               img_volume=rr.render_frame(rr.VolumeField(vol), cam, rr.TransferFunction(), cfg))
+    small = rmodel.init_model(rmodel.ModelConfig(grids=2, channels=1, resolution=(4, 4, 4)), seed=2, vmin=0.0,
+                              vmax=1.0)
+    small.grids[:] = np.random.default_rng(0).normal(size=small.grids.shape).astype(np.float32)
+    out.update(model_arrays("small_", small))
+    cam2 = rr.Camera(eye=(0.0, 0.5, 2.9), look_at=(0.0, 0.0, 0.0), width=9, height=9)
+    out["img_small"] = rr.render_frame(rr.ModelField(small), cam2, rr.TransferFunction(),
+                                       rr.RenderConfig(samples_per_ray=8))
+    big = perturbed_model(11, 64, 2, (8, 8, 8), np.float32)
+    out.update(model_arrays("big_", big))
+    cam3 = rr.Camera(eye=(-1.2, 0.9, 2.2), look_at=(0.1, 0.0, 0.0), fov_deg=50, width=16, height=12)
+    cfg3 = rr.RenderConfig(samples_per_ray=24, background=(0.05, 0.05, 0.1, 1.0), early_exit_alpha=0.95)
+    out["img_big"] = rr.render_frame(rr.ModelField(big), cam3, tf, cfg3)
+    np.savez_compressed(OUT / "render.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["encode_forward", "recon", "density", "adam", "philox", "volume",
                              "train_small", "hash_decomp", "psnr", "train_c1"]

@@ -1,0 +1,191 @@
+"""GPU renderer field-query path (paper_2308_02494_b200.render, csrc/render_kernels.cu) against
+the reference renderer's outputs (tests/golden/render.npz) and the oracle, plus the reference
+tests' invariants: determinism (batch size, progressive assembly), misses, closed forms."""
+import numpy as np
+import pytest
+
+from oracle import apmg_oracle as O
+from oracle import render_oracle as R
+
+pytestmark = pytest.mark.gpu
+
+import paper_2308_02494_b200 as P  # noqa: E402
+from paper_2308_02494_b200 import model as PM  # noqa: E402
+from paper_2308_02494_b200 import render as PR  # noqa: E402
+from paper_2308_02494_b200 import volume as PV  # noqa: E402
+
+TF_COLORS = [(0.0, (0.0, 0.0, 0.1)), (0.4, (1.0, 0.2, 0.0)), (1.0, (1.0, 1.0, 1.0))]
+TF_ALPHA = [(0.0, 0.0), (0.3, 0.05), (0.7, 0.9), (1.0, 0.2)]
+# powf (CUDA <= 2 ulp vs libm) in the opacity correction, and for model fields the forward's
+# own gate (<= 1e-4 of the value range), propagated through LUT slopes of up to ~4 / range
+ATOL_VOLUME, ATOL_MODEL = 2e-6, 1e-3
+
+
+def model_from(g, prefix):
+    meta, rng = g[prefix + "meta"], g[prefix + "range"]
+    cfg = PM.ModelConfig(grids=int(meta[0]), channels=int(meta[1]), resolution=tuple(int(v) for v in meta[2:5]),
+                         flat_top_p=int(meta[5]))
+    m = PM.init_model(cfg, seed=0, vmin=float(rng[0]), vmax=float(rng[1]))
+    for k in ("transforms", "grids", "w1", "w2", "w3"):
+        getattr(m, k)[...] = g[prefix + k]
+    return m
+
+
+def test_ray_box_hits_bit_exact(golden):
+    g = golden("render")
+    e, x, h = PR.ray_box_hits(g["rb_origin"], g["rb_dirs"])
+    assert np.array_equal(e, g["rb_enter"]) and np.array_equal(x, g["rb_exit"]) and np.array_equal(h, g["rb_hit"])
+    e, x, h = PR.ray_box_hits(np.zeros(3), np.array([[1.0, 0.0, 0.0], [0.0, 0.0, -1.0]]))
+    assert np.array_equal(e, g["rb0_enter"]) and np.array_equal(x, g["rb0_exit"]) and np.array_equal(h, g["rb0_hit"])
+    assert not PR.ray_box_hits(np.array([0.0, 2.0, 5.0]), np.array([[0.0, 0.0, -1.0]]))[2][0]
+
+
+def test_transfer_function_bit_exact(golden):
+    g = golden("render")
+    tf = PR.TransferFunction(TF_COLORS, TF_ALPHA, (0.1, 0.8))
+    assert np.array_equal(tf.apply(g["tf_values"], -0.5, 1.5), g["tf_rgba"])
+    flat = PR.TransferFunction()
+    assert np.array_equal(flat.apply(np.array([-2.0]), vmin=-2.0, vmax=3.0)[0], flat.lut[0])
+    assert np.array_equal(PR.TransferFunction(window=(0.5, 1.0)).apply(np.array([0.5]), 0.0, 1.0)[0], flat.lut[0])
+    assert np.array_equal(flat.apply(np.array([0.3, 7.0]), 1.0, 1.0), flat.lut[[0, 0]])  # degenerate range
+
+
+def test_composite_ray(golden):
+    g = golden("render")
+    s = g["comp_samples"]
+    np.testing.assert_allclose(PR.composite_ray(s, step=0.01, reference_step=0.02), g["comp_a"], atol=ATOL_VOLUME)
+    np.testing.assert_allclose(PR.composite_ray(s, step=0.013, reference_step=0.02, background=(0.2, 0.3, 0.4, 0.5),
+                                                early_exit_alpha=None), g["comp_b"], atol=ATOL_VOLUME)
+    np.testing.assert_allclose(PR.composite_ray(s[:7], step=0.05, early_exit_alpha=0.5), g["comp_c"],
+                               atol=ATOL_VOLUME)
+    assert np.allclose(PR.composite_ray(np.zeros((10, 4), np.float32), 0.01, background=(0.2, 0.3, 0.4, 1.0)),
+                       [0.2, 0.3, 0.4, 1.0])
+    two = np.array([[1.0, 1.0, 1.0, 0.5], [0.0, 0.0, 0.0, 0.5]], dtype=np.float32)
+    out = PR.composite_ray(two, step=0.02, reference_step=0.02, background=(0, 0, 0, 0), early_exit_alpha=None)
+    assert np.allclose(out[:3], 0.5) and out[3] == pytest.approx(0.75)
+
+
+def test_volume_frame_vs_reference(golden):
+    g = golden("render")
+    w, h, d = (int(v) for v in g["vol_dims"])
+    vol = PV.Volume(dims=(w, h, d), data=g["vol_data"])
+    cam = PR.Camera(eye=(1.5, 1.0, 2.5), look_at=(0.0, 0.0, 0.0), width=12, height=10)
+    img = PR.render_frame(PR.VolumeField(vol), cam, PR.TransferFunction(), PR.RenderConfig(samples_per_ray=16))
+    np.testing.assert_allclose(img, g["img_volume"], atol=ATOL_VOLUME, rtol=0)
+
+
+@pytest.mark.parametrize("prefix,cam,cfg,tfargs", [
+    ("small_", dict(eye=(0.0, 0.5, 2.9), look_at=(0.0, 0.0, 0.0), width=9, height=9),
+     dict(samples_per_ray=8), None),
+    ("big_", dict(eye=(-1.2, 0.9, 2.2), look_at=(0.1, 0.0, 0.0), fov_deg=50, width=16, height=12),
+     dict(samples_per_ray=24, background=(0.05, 0.05, 0.1, 1.0), early_exit_alpha=0.95),
+     (TF_COLORS, TF_ALPHA, (0.1, 0.8))),
+])
+def test_model_frame_vs_reference(golden, prefix, cam, cfg, tfargs):
+    g = golden("render")
+    m = model_from(g, prefix)
+    tf = PR.TransferFunction(*tfargs) if tfargs else PR.TransferFunction()
+    img = PR.render_frame(PR.ModelField(m), PR.Camera(**cam), tf, PR.RenderConfig(**cfg))
+    np.testing.assert_allclose(img, g["img" + prefix[:-1].join(["_", ""])], atol=ATOL_MODEL, rtol=0)
+    # a bare model and a generic host field (its own .forward through the protocol) agree
+    img2 = PR.render_frame(m, PR.Camera(**cam), tf, PR.RenderConfig(**cfg))
+    assert img2.tobytes() == img.tobytes()
+
+
+class HostField:
+    """A field the renderer only knows through the duck-typed protocol (host .forward)."""
+
+    def __init__(self, vol_np):
+        self.data = vol_np
+        self.vmin, self.vmax = float(vol_np.min()), float(vol_np.max())
+        self.voxel_diagonal = None
+
+    def forward(self, pts):
+        return O.sample_volume(self.data, np.asarray(pts, dtype=np.float64)).astype(np.float32)
+
+
+def test_generic_field_and_batch_size_invariance():
+    vol = PV.synth_volume((9, 9, 9), [PV.BlobSpec(center=(0.2, 0, 0), sigma=(0.4, 0.5, 0.3))])
+    cam = PR.Camera(eye=(1.5, 1.0, 2.5), look_at=(0, 0, 0), width=12, height=10)
+    tf = PR.TransferFunction()
+    imgs = [PR.render_frame(PR.VolumeField(vol), cam, tf, PR.RenderConfig(samples_per_ray=16, batch_size=bs))
+            for bs in (7, 64, 100_000)]
+    assert imgs[0].tobytes() == imgs[1].tobytes() == imgs[2].tobytes()
+    hf = [PR.render_frame(HostField(vol.host_data()), cam, tf,
+                          PR.RenderConfig(samples_per_ray=16, batch_size=bs, reference_step=vol.voxel_diagonal))
+          for bs in (7, 100_000)]
+    assert hf[0].tobytes() == hf[1].tobytes()
+    np.testing.assert_allclose(hf[0], imgs[0], atol=ATOL_VOLUME)
+
+
+def test_progressive_bit_identical():
+    vol = PV.synth_volume((9, 9, 9), [PV.BlobSpec(center=(-0.3, 0.1, 0), sigma=(0.3, 0.3, 0.5))])
+    cam = PR.Camera(eye=(0.5, 0.8, 2.8), look_at=(0, 0, 0), width=11, height=7)
+    cfg = PR.RenderConfig(samples_per_ray=12)
+    tf = PR.TransferFunction()
+    direct = PR.render_frame(PR.VolumeField(vol), cam, tf, cfg)
+    passes = list(PR.render_progressive(PR.VolumeField(vol), cam, tf, cfg))
+    assert passes[-1].final and passes[-1].preview.tobytes() == direct.tobytes()
+    assert sum(p.new_pixels for p in passes) == 11 * 7
+    m = PM.init_model(PM.ModelConfig(grids=2, channels=1, resolution=(4, 4, 4)), seed=2, vmin=0.0, vmax=1.0)
+    m.grids[:] = np.random.default_rng(0).normal(size=m.grids.shape).astype(np.float32)
+    cam2 = PR.Camera(eye=(0, 0.5, 2.9), look_at=(0, 0, 0), width=9, height=9)
+    direct = PR.render_frame(PR.ModelField(m), cam2, tf, PR.RenderConfig(samples_per_ray=8))
+    final = list(PR.render_progressive(PR.ModelField(m), cam2, tf, PR.RenderConfig(samples_per_ray=8)))[-1]
+    assert final.preview.tobytes() == direct.tobytes()
+
+
+def test_miss_closed_form_and_early_exit():
+    const = PV.Volume(dims=(9, 9, 9), data=np.full((9, 9, 9), 0.75, dtype=np.float32))
+    away = PR.Camera(eye=(0, 0, 10), look_at=(0, 0, 20), width=8, height=8)
+    flat = PR.TransferFunction(color_points=[(0.0, (0.2, 0.5, 0.8)), (1.0, (0.2, 0.5, 0.8))],
+                               opacity_points=[(0.0, 0.3), (1.0, 0.3)])
+    img = PR.render_frame(PR.VolumeField(const), away, flat, PR.RenderConfig(samples_per_ray=8))
+    assert np.array_equal(img, np.broadcast_to(np.array([0, 0, 0, 1], dtype=np.float32), (8, 8, 4)))
+    cam = PR.Camera(eye=(0, 0, 3.2), look_at=(0, 0, 0), fov_deg=40, width=17, height=13)
+    cfg = PR.RenderConfig(samples_per_ray=24, background=(0.05, 0.05, 0.1, 1.0))
+    img = PR.render_frame(PR.VolumeField(const), cam, flat, cfg).reshape(-1, 4)
+    origin, dirs = PR.generate_rays(cam)
+    enter, exit_t, hit = R.box_hits(origin, dirs)
+    lut = R.bake_lut(flat.color_points, flat.opacity_points)
+    rgba = np.broadcast_to(R.tf_lookup(lut, (0.0, 1.0), np.float32(0.75), 0.75, 0.75), (1, 24, 4))
+    for n in range(len(dirs)):
+        exp = np.array(cfg.background, np.float32) if not hit[n] else R.composite(
+            rgba, np.array([(exit_t[n] - enter[n]) / 24], np.float32), const.voxel_diagonal, cfg.background, 0.99)[0]
+        np.testing.assert_allclose(img[n], exp, atol=ATOL_VOLUME)
+    one = PV.Volume(dims=(9, 9, 9), data=np.full((9, 9, 9), 1.0, dtype=np.float32))
+    cam3 = PR.Camera(eye=(0, 0, 3), look_at=(0, 0, 0), width=9, height=9)
+    tf9 = PR.TransferFunction(color_points=[(0.0, (1.0, 0.6, 0.2)), (1.0, (1.0, 0.6, 0.2))],
+                              opacity_points=[(0.0, 0.9), (1.0, 0.9)])
+    on = PR.render_frame(PR.VolumeField(one), cam3, tf9, PR.RenderConfig(samples_per_ray=48, early_exit_alpha=0.99))
+    off = PR.render_frame(PR.VolumeField(one), cam3, tf9, PR.RenderConfig(samples_per_ray=48, early_exit_alpha=None))
+    assert np.abs(on - off).max() <= 0.01
+
+
+def test_decomposed_field_frame_matches_host_protocol():
+    """DecomposedField rendered through its device forward equals rendering it through the
+    host protocol (.forward on host batches) bit for bit."""
+    import tempfile
+    from pathlib import Path
+    vol = PV.synth_volume((17, 17, 17), [PV.BlobSpec(center=(0.1, -0.2, 0.3), sigma=(0.4, 0.3, 0.5))])
+    with tempfile.TemporaryDirectory() as td:
+        path = Path(td) / "v.raw"
+        header = PV.save_volume(vol, path)
+        plan = P.plan_partition(vol.dims, 2, 1, 1, ghost=1)
+        cfgm = PM.ModelConfig(grids=4, channels=2, resolution=(4, 4, 4))
+        man = P.train_decomposed(path, header, plan, cfgm, P.TrainConfig(iterations=3, batch_size=256, delay_start=1, seed=0),
+                                 Path(td) / "out")
+        field = P.DecomposedField.load(Path(td) / "out" / "manifest.json")
+
+        class Proto:
+            vmin, vmax, voxel_diagonal = field.vmin, field.vmax, field.voxel_diagonal
+
+            def forward(self, pts):
+                return field.forward(np.asarray(pts, dtype=np.float32))
+
+        cam = PR.Camera(eye=(0.4, 0.3, 2.7), look_at=(0, 0, 0), width=10, height=8)
+        cfg = PR.RenderConfig(samples_per_ray=12)
+        a = PR.render_frame(field, cam, PR.TransferFunction(), cfg)
+        b = PR.render_frame(Proto(), cam, PR.TransferFunction(), cfg)
+        assert a.tobytes() == b.tobytes()
+        assert man is not None
