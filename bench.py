@@ -267,6 +267,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-inference", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -368,6 +369,10 @@ def main():
         infer = bench_inference(model_from_session=None) if world == 1 else \
             bench_decomposed_inference(rank, world, dist)
 
+    render = None
+    if rank == 0 and world == 1 and not args.no_render:
+        render = bench_render()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(L.to_host(vdev))
@@ -381,12 +386,39 @@ def main():
                        "density_loss": "every timed iteration", "parallelism": f"brick-sharded x{world}",
                        "l2": "inputs larger than L2 (512 MiB+ volume per rank); 16 MiB grids L2-resident by design"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
-            "kernel_share": shares, "e2e": e2e, "cpu_baseline": cpu, "inference": infer,
+            "kernel_share": shares, "e2e": e2e, "cpu_baseline": cpu, "inference": infer, "render": render,
             "final_l_rec": log.l_rec[-1] if log.l_rec else None,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def bench_render(size=512, samples=128, reps=5):
+    """Renderer field-query path: one C2-shaped model, a size^2 frame, `samples`
+    per ray, reference defaults otherwise (early exit at alpha 0.99).  Wall time of
+    render_frame (device rays, sample points, tensor-core field queries, transfer function,
+    compositing, RGBA download), after one warm-up frame."""
+    import numpy as np
+    import torch
+    from paper_2308_02494_b200 import model as PM
+    from paper_2308_02494_b200 import render as PR
+    m = PM.init_model(PM.ModelConfig(M, CH, RES), seed=0, vmin=0.0, vmax=1.0)
+    m.grids[:] = np.random.default_rng(0).normal(scale=0.3, size=m.grids.shape).astype(np.float32)
+    cam = PR.Camera(eye=(1.6, 1.1, 2.4), look_at=(0.0, 0.0, 0.0), width=size, height=size)
+    tf = PR.TransferFunction(opacity_points=[(0.0, 0.0), (0.5, 0.05), (1.0, 0.6)])
+    cfg = PR.RenderConfig(samples_per_ray=samples)
+    PR.render_frame(PR.ModelField(m), cam, tf, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        img = PR.render_frame(PR.ModelField(m), cam, tf, cfg)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    return {"metric": "rendered frames/sec", "value": 1.0 / dt, "ms_per_frame": 1e3 * dt,
+            "field_queries_per_sec_upper_bound": size * size * samples / dt,
+            "config": f"{size}x{size} frame, {samples} samples/ray, 64x32^3x2 model, early exit 0.99, "
+                      f"mean alpha {float(img[..., 3].mean()):.3f}"}
 
 
 def bench_inference(model_from_session=None, dims=(1024, 1024, 1024)):

@@ -65,18 +65,29 @@ uint64_t apmg_launch_count(void);
  * against [-1,1]^3 -> enter / exit [n] f64, hit [n] u8. */
 int apmg_ray_box_hits(const double* origin, const double* dirs, int64_t n, double* enter, double* exit_t,
                       uint8_t* hit, void* stream);
-/* _render_rays sample points (render.py:286-290) of the rays ray_ids [nr] (i64, hit rays):
- * pts [nr][samples][3] f32 = clip(origin + ((s+0.5) dt + enter) dir, -1, 1), dt [nr] f64. */
+/* generate_rays (render.py:202-220) on the device: basis = HOST f64[11] {fwd[3], right[3],
+ * true_up[3], tan(fov/2), width/height} from the host's camera setup -> dirs [height*width][3]
+ * f64, row-major from the top-left pixel, bit-identical to the numpy chain. */
+int apmg_generate_rays(const double* basis, int32_t width, int32_t height, double* dirs, void* stream);
+/* _render_rays sample points (render.py:286-290): samples s0 .. s0+count-1 of `samples` per ray
+ * for the rays ray_ids [nr] (i64, hit rays; enter / exit [*] f64 from apmg_ray_box_hits):
+ * pts [nr][count][3] f32 = clip(origin + ((s+0.5) dt + enter) dir, -1, 1), dt = (exit-enter)/samples. */
 int apmg_ray_points(const double* origin, const double* dirs, const int64_t* ray_ids, int64_t nr, int32_t samples,
-                    float* pts, double* dt, void* stream);
+                    int32_t s0, int32_t count, const double* enter, const double* exit_t, float* pts,
+                    void* stream);
 /* TransferFunction.apply (render.py:126-138): values [n] f32 -> rgba [n][4] f32 through the
  * baked LUT [256][4] f32; tf = HOST f32[5] {vmin, vmax - vmin, lo, hi - lo, vmax > vmin}. */
 int apmg_tf_apply(const float* values, int64_t n, const float* lut, const float* tf, float* rgba, void* stream);
-/* _render_rays tail (render.py:292-295): field values [nr][samples] -> transfer function ->
- * front-to-back composite (render.py:240-264) -> out[ray_ids[j]] (RGBA f32; ray_ids NULL:
- * out[j]).  comp = HOST f32[7] {reference_step, background[4], early_exit_alpha, early_on}. */
-int apmg_composite_values(const float* values, const double* dt, const int64_t* ray_ids, int64_t nr,
-                          int32_t samples, const float* lut, const float* tf, const float* comp, float* out,
+/* _render_rays tail (render.py:292-295), one chunk of `count` samples per ray: field values
+ * [nr][count] -> transfer function -> front-to-back update (render.py:240-257) of the per-ray
+ * state [*][4] f32 (r, g, b, alpha; zero-initialised, indexed by ray id).  Rays whose alpha
+ * reached the early-exit threshold stop accumulating.  comp = HOST f32[7] {reference_step,
+ * background[4], early_exit_alpha, early_on}. */
+int apmg_composite_chunk(const float* values, const int64_t* ray_ids, int64_t nr, int32_t samples, int32_t count,
+                         const double* enter, const double* exit_t, const float* lut, const float* tf,
+                         const float* comp, float* state, void* stream);
+/* background blend of the final state (render.py:258-263) -> out[ray_ids[j]] RGBA f32. */
+int apmg_composite_finish(const int64_t* ray_ids, int64_t nr, const float* state, const float* comp, float* out,
                           void* stream);
 /* _composite of RGBA samples [nr][count][4] with per-ray steps [nr] f32 (composite_ray). */
 int apmg_composite_rgba(const float* samples, const float* steps, int64_t nr, int32_t count, const float* comp,
@@ -99,6 +110,11 @@ int apmg_encode(const apmg_model* m, const void* pts, int64_t n, void* feats, vo
 int apmg_decode(const apmg_model* m, const void* feats, int64_t n, void* out, void* stream);
 /* ApmgModel.forward (model.py:164-166): fused encode + decode, pts [n][3] -> out [n] */
 int apmg_forward(const apmg_model* m, const void* pts, int64_t n, void* out, void* stream);
+/* forward of a float32 point list through the tensor-core sweep kernel (the renderer's field
+ * queries): f32 lerps and bf16x3 MLP products -- within the forward gate (<= 1e-4 of the
+ * value range) of model.py:164-166 but not bit-equal to apmg_forward; other model shapes
+ * take apmg_forward's kernel. */
+int apmg_forward_tc(const apmg_model* m, const float* pts, int64_t n, float* out, void* stream);
 
 /* ---- reconstruction loss (optim.py:102-155) ------------------------------ */
 size_t apmg_recon_workspace_bytes(const apmg_model* m, int64_t n);

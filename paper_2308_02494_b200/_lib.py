@@ -50,11 +50,15 @@ SIGNATURES = {
     "apmg_device_sm_count": (C.c_int, []),
     "apmg_launch_count": (C.c_uint64, []),
     "apmg_release_cached": (C.c_int, []),
+    "apmg_forward_tc": (C.c_int, [_MP, _P, _I64, _P, _P]),
+    "apmg_generate_rays": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int32, _P, _P]),
     "apmg_ray_box_hits": (C.c_int, [C.POINTER(C.c_double), _P, _I64, _P, _P, _P, _P]),
-    "apmg_ray_points": (C.c_int, [C.POINTER(C.c_double), _P, _P, _I64, C.c_int32, _P, _P, _P]),
+    "apmg_ray_points": (C.c_int, [C.POINTER(C.c_double), _P, _P, _I64, C.c_int32, C.c_int32, C.c_int32, _P, _P,
+                                  _P, _P]),
     "apmg_tf_apply": (C.c_int, [_P, _I64, _P, C.POINTER(C.c_float), _P, _P]),
-    "apmg_composite_values": (C.c_int, [_P, _P, _P, _I64, C.c_int32, _P, C.POINTER(C.c_float),
-                                        C.POINTER(C.c_float), _P, _P]),
+    "apmg_composite_chunk": (C.c_int, [_P, _P, _I64, C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float), _P, _P]),
+    "apmg_composite_finish": (C.c_int, [_P, _I64, _P, C.POINTER(C.c_float), _P, _P]),
     "apmg_composite_rgba": (C.c_int, [_P, _P, _I64, C.c_int32, C.POINTER(C.c_float), _P, _P]),
     "apmg_kernel_timing_enable": (C.c_int, [C.c_int]),
     "apmg_kernel_timing_read": (C.c_int, [C.c_char_p, C.POINTER(_D), C.POINTER(_I64), C.c_int]),

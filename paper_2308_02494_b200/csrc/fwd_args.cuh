@@ -23,6 +23,7 @@ struct FwdArgs {
   int affine;
   int stamps;           // k_infer_tc phase stamps (profiling aid)
   int box_local;        // truth / recon are dense [bd][bh][bw] arrays of the box (brick sweeps)
+  int tc_points;        // kFwdPts through the tensor-core sweep kernel (f32 lerps, bf16x3 MLP)
   double sc0, sc1, sc2, of0, of1, of2;
   const float* truth;   // [LD][LH][LW] or null
   float* recon;         // [LD][LH][LW] or null

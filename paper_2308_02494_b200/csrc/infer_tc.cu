@@ -170,7 +170,11 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
 #pragma unroll
         for (int q = 1; q < WQ; ++q) raw += sHead[q * P + tid];
         const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
-        if (a.recon) a.recon[voxel_of(a, i)] = y;
+        if (a.mode == kFwdPts) {
+          a.out[i] = y;
+        } else if (a.recon) {
+          a.recon[voxel_of(a, i)] = y;
+        }
         if (a.truth) {
           const double d = sub_rn(double(y), double(sTru[par * P + tid]));  // par: tile index mod 3
           sse += d * d;
@@ -224,6 +228,14 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
       Pre r{0.f, 0.f, 0.f, 0.f};
       const int t = tid - (NT - P);
       const int64_t i = tile * P + t;
+      if (a.mode == kFwdPts) {  // point list (renderer samples): coordinates as given
+        if (t >= 0 && tile < tiles && i < a.n) {
+          r.x0 = __ldg(a.pts + 3 * i);
+          r.x1 = __ldg(a.pts + 3 * i + 1);
+          r.x2 = __ldg(a.pts + 3 * i + 2);
+        }
+        return r;
+      }
       if (t >= 0 && tile < tiles && i < a.n) {
         const int64_t plane = int64_t(a.bw) * a.bh;
         const int z = int(i / plane);
@@ -336,19 +348,22 @@ extern "C" int apmg_debug_infer_phases(long long* out) {
 
 bool infer_tc_eligible(const FwdArgs<float>& a) {
   const char* e = getenv("APMG_MLP");  // APMG_MLP=simt keeps the SIMT sweep (A/B tests)
-  return !(e && e[0] == 's') && a.mode == kFwdLattice && a.md.F == 128 && a.md.C == 2 && a.md.M == 64;
+  return !(e && e[0] == 's') && (a.mode == kFwdLattice || (a.mode == kFwdPts && a.tc_points)) &&
+         a.md.F == 128 && a.md.C == 2 && a.md.M == 64;
 }
 
 int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   static float* tab = nullptr;  // per-axis coordinate tables (grown on demand, never freed)
   static int64_t tab_cap = 0;
-  const int64_t need = int64_t(a.bw) + a.bh + ceil_div(a.n, int64_t(a.bw) * a.bh);
-  if (need > tab_cap) {
-    if (tab) APMG_CUDA_TRY(cudaFree(tab));
-    APMG_CUDA_TRY(cudaMalloc(&tab, sizeof(float) * need));
-    tab_cap = need;
+  if (a.mode == kFwdLattice) {
+    const int64_t need = int64_t(a.bw) + a.bh + ceil_div(a.n, int64_t(a.bw) * a.bh);
+    if (need > tab_cap) {
+      if (tab) APMG_CUDA_TRY(cudaFree(tab));
+      APMG_CUDA_TRY(cudaMalloc(&tab, sizeof(float) * need));
+      tab_cap = need;
+    }
+    APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   }
-  APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   static bool attr = false;
   if (!attr) {
     APMG_CUDA_TRY(cudaFuncSetAttribute(itc::k_infer_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -360,7 +375,10 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const char* es = getenv("APMG_INFER_STAMPS");
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
-  APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
+  if (a.mode == kFwdPts)
+    APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
+  else
+    APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   return APMG_OK;
 }
 

@@ -508,6 +508,20 @@ extern "C" int apmg_forward(const apmg_model* m, const void* pts, int64_t n, voi
                               : fwd_common<double>(m, kFwdPts, pts, n, out, stream);
 }
 
+extern "C" int apmg_forward_tc(const apmg_model* m, const float* pts, int64_t n, float* out, void* stream) {
+  int rc = check_model(m);
+  if (rc) return rc;
+  APMG_ARG_CHECK(m->dtype == APMG_F32, "apmg_forward_tc needs a float32 model");
+  FwdArgs<float> a{};
+  a.md = make_model_dev<float>(*m);
+  a.mode = kFwdPts;
+  a.n = n;
+  a.pts = pts;
+  a.out = out;
+  a.tc_points = 1;
+  return launch_forward<float>(a, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" size_t apmg_recon_workspace_bytes(const apmg_model* m, int64_t n) {
   if (!m) return 0;
   const int F = m->grids * m->channels;

@@ -59,20 +59,43 @@ __global__ void k_ray_box_hits(RayOrigin org, const double* __restrict__ dirs, i
   }
 }
 
-// render.py:286-290 for rays ray_ids[0..nr): dt = (exit - enter) / S, sample s at
-// t = (s + 0.5) dt + enter, p = clip(origin + t dir, -1, 1) -> float32
+// render.py:202-220 per pixel, from the host's camera basis (fwd, right, true_up, tan_half,
+// aspect): the same f64 chain numpy evaluates -- u = px tan_half aspect, v = py tan_half,
+// d = (fwd + u right) + v up, |d| = sqrt((d0^2 + d1^2) + d2^2), d / |d| -- so the directions are
+// bit-identical to generate_rays.
+struct CamBasis {
+  double f[3], r[3], u[3], tan_half, aspect;
+};
+__global__ void k_generate_rays(CamBasis cb, int W, int H, double* __restrict__ dirs) {
+  const int64_t n = int64_t(W) * H;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(q / W), i = int(q - int64_t(j) * W);
+    const double px = __dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn(double(i), 0.5), double(W)), 2.0), 1.0);
+    const double py = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn(double(j), 0.5), double(H)), 2.0));
+    const double u = __dmul_rn(__dmul_rn(px, cb.tan_half), cb.aspect), v = __dmul_rn(py, cb.tan_half);
+    double d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = __dadd_rn(__dadd_rn(cb.f[k], __dmul_rn(u, cb.r[k])), __dmul_rn(v, cb.u[k]));
+    const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                                            __dmul_rn(d[2], d[2])));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dirs[3 * q + k] = __ddiv_rn(d[k], nrm);
+  }
+}
+
+// render.py:286-290 for rays ray_ids[0..nr), samples s0 .. s0+cs-1 of S: dt = (exit - enter) / S,
+// sample s at t = (s + 0.5) dt + enter, p = clip(origin + t dir, -1, 1) -> float32
 __global__ void k_ray_points(RayOrigin org, const double* __restrict__ dirs, const int64_t* __restrict__ ray_ids,
-                             int64_t nr, int32_t S, float* __restrict__ pts, double* __restrict__ dt_out) {
-  const int64_t total = nr * S;
+                             int64_t nr, int32_t S, int32_t s0, int32_t cs, const double* __restrict__ enter,
+                             const double* __restrict__ exit_t, float* __restrict__ pts) {
+  const int64_t total = nr * cs;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = q / S;
-    const int s = int(q - j * S);
-    const double* d = dirs + 3 * ray_ids[j];
-    double e, x;
-    bool h;
-    box_hit(org, d, e, x, h);
-    const double dt = __ddiv_rn(__dsub_rn(x, e), double(S));
-    if (s == 0) dt_out[j] = dt;
+    const int64_t j = q / cs;
+    const int s = s0 + int(q - j * cs);
+    const int64_t r = ray_ids[j];
+    const double* d = dirs + 3 * r;
+    const double e = enter[r];
+    const double dt = __ddiv_rn(__dsub_rn(exit_t[r], e), double(S));
     const double t = __dadd_rn(__dmul_rn(__dadd_rn(double(s), 0.5), dt), e);
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
@@ -138,15 +161,44 @@ __device__ __forceinline__ float4 composite(Sample rgba, int S, float step, cons
                      __fadd_rn(b, __fmul_rn(rem, c.bg[2])), __fadd_rn(alpha, rem));
 }
 
-// field values [nr][S] of rays ray_ids -> transfer function -> composite -> out[ray_ids[j]]
-__global__ void k_composite_values(const float* __restrict__ values, const double* __restrict__ dt,
-                                   const int64_t* __restrict__ ray_ids, int64_t nr, int32_t S,
-                                   const float4* __restrict__ lut, TfParams tp, CompParams cp,
-                                   float4* __restrict__ out) {
+// One chunk of samples (s0 .. s0+cs-1 of S) of rays ray_ids: field values [nr][cs] ->
+// transfer function -> front-to-back update of the per-ray state (r, g, b, alpha), indexed by
+// ray id.  Chunked marching lets the host drop rays that reached the early-exit opacity before
+// their remaining samples are queried: the reference evaluates them and discards the result,
+// so the pixels are the same.
+__global__ void k_composite_chunk(const float* __restrict__ values, const int64_t* __restrict__ ray_ids, int64_t nr,
+                                  int32_t S, int32_t cs, const double* __restrict__ enter,
+                                  const double* __restrict__ exit_t, const float4* __restrict__ lut, TfParams tp,
+                                  CompParams cp, float4* __restrict__ state) {
   for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nr; j += int64_t(gridDim.x) * blockDim.x) {
-    const float* v = values + j * S;
-    const float4 o = composite([&](int s) { return tf_apply(lut, tp, v[s]); }, S, __double2float_rn(dt[j]), cp);
-    out[ray_ids ? ray_ids[j] : j] = o;
+    const int64_t r = ray_ids[j];
+    const float step = __double2float_rn(__ddiv_rn(__dsub_rn(exit_t[r], enter[r]), double(S)));
+    const float e = __fdiv_rn(step, cp.ref_step);
+    float4 st = state[r];
+    const float* v = values + j * cs;
+    for (int s = 0; s < cs; ++s) {
+      if (cp.early_on && !(st.w < cp.early)) break;
+      const float4 c = tf_apply(lut, tp, v[s]);
+      const float corr = __fsub_rn(1.f, powf(__fsub_rn(1.f, c.w), e));
+      const float contrib = __fmul_rn(__fsub_rn(1.f, st.w), corr);
+      st.x = __fadd_rn(st.x, __fmul_rn(contrib, c.x));
+      st.y = __fadd_rn(st.y, __fmul_rn(contrib, c.y));
+      st.z = __fadd_rn(st.z, __fmul_rn(contrib, c.z));
+      st.w = __fadd_rn(st.w, contrib);
+    }
+    state[r] = st;
+  }
+}
+
+// background blend of the final state of rays ray_ids (render.py:258-263)
+__global__ void k_composite_finish(const int64_t* __restrict__ ray_ids, int64_t nr, const float4* __restrict__ state,
+                                   CompParams cp, float4* __restrict__ out) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nr; j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = ray_ids[j];
+    const float4 st = state[r];
+    const float rem = __fmul_rn(__fsub_rn(1.f, st.w), cp.bg[3]);
+    out[r] = make_float4(__fadd_rn(st.x, __fmul_rn(rem, cp.bg[0])), __fadd_rn(st.y, __fmul_rn(rem, cp.bg[1])),
+                         __fadd_rn(st.z, __fmul_rn(rem, cp.bg[2])), __fadd_rn(st.w, rem));
   }
 }
 
@@ -180,13 +232,25 @@ extern "C" int apmg_ray_box_hits(const double* origin, const double* dirs, int64
   return APMG_OK;
 }
 
+extern "C" int apmg_generate_rays(const double* basis, int32_t width, int32_t height, double* dirs, void* stream) {
+  APMG_ARG_CHECK(basis && width >= 1 && height >= 1 && dirs, "bad camera arguments");
+  CamBasis cb{{basis[0], basis[1], basis[2]}, {basis[3], basis[4], basis[5]}, {basis[6], basis[7], basis[8]},
+              basis[9], basis[10]};
+  const int64_t n = int64_t(width) * height;
+  APMG_LAUNCH("generate_rays", k_generate_rays, elementwise_grid(n, 8), 256, 0, static_cast<cudaStream_t>(stream),
+              cb, width, height, dirs);
+  return APMG_OK;
+}
+
 extern "C" int apmg_ray_points(const double* origin, const double* dirs, const int64_t* ray_ids, int64_t nr,
-                               int32_t samples, float* pts, double* dt, void* stream) {
-  APMG_ARG_CHECK(origin && samples >= 1, "null origin or samples < 1");
-  if (nr == 0) return APMG_OK;
-  APMG_ARG_CHECK(dirs && ray_ids && pts && dt, "null argument");
-  APMG_LAUNCH("ray_points", k_ray_points, elementwise_grid(nr * samples, 8), 256, 0,
-              static_cast<cudaStream_t>(stream), origin_of(origin), dirs, ray_ids, nr, samples, pts, dt);
+                               int32_t samples, int32_t s0, int32_t count, const double* enter, const double* exit_t,
+                               float* pts, void* stream) {
+  APMG_ARG_CHECK(origin && samples >= 1 && s0 >= 0 && count >= 0 && s0 + count <= samples, "bad sample range");
+  if (nr == 0 || count == 0) return APMG_OK;
+  APMG_ARG_CHECK(dirs && ray_ids && enter && exit_t && pts, "null argument");
+  APMG_LAUNCH("ray_points", k_ray_points, elementwise_grid(nr * count, 8), 256, 0,
+              static_cast<cudaStream_t>(stream), origin_of(origin), dirs, ray_ids, nr, samples, s0, count, enter,
+              exit_t, pts);
   return APMG_OK;
 }
 
@@ -200,15 +264,26 @@ extern "C" int apmg_tf_apply(const float* values, int64_t n, const float* lut, c
   return APMG_OK;
 }
 
-extern "C" int apmg_composite_values(const float* values, const double* dt, const int64_t* ray_ids, int64_t nr,
-                                     int32_t samples, const float* lut, const float* tf, const float* comp, float* out,
-                                     void* stream) {
-  APMG_ARG_CHECK(tf && comp && samples >= 1, "null parameters or samples < 1");
+extern "C" int apmg_composite_chunk(const float* values, const int64_t* ray_ids, int64_t nr, int32_t samples,
+                                    int32_t count, const double* enter, const double* exit_t, const float* lut,
+                                    const float* tf, const float* comp, float* state, void* stream) {
+  APMG_ARG_CHECK(tf && comp && samples >= 1 && count >= 0, "null parameters or bad sample counts");
+  if (nr == 0 || count == 0) return APMG_OK;
+  APMG_ARG_CHECK(values && ray_ids && enter && exit_t && lut && state, "null argument");
+  APMG_LAUNCH("composite", k_composite_chunk, elementwise_grid(nr, 4), 128, 0, static_cast<cudaStream_t>(stream),
+              values, ray_ids, nr, samples, count, enter, exit_t, reinterpret_cast<const float4*>(lut),
+              tf_params(tf), comp_params(comp), reinterpret_cast<float4*>(state));
+  return APMG_OK;
+}
+
+extern "C" int apmg_composite_finish(const int64_t* ray_ids, int64_t nr, const float* state, const float* comp,
+                                     float* out, void* stream) {
+  APMG_ARG_CHECK(comp, "null parameters");
   if (nr == 0) return APMG_OK;
-  APMG_ARG_CHECK(values && dt && lut && out, "null argument");
-  APMG_LAUNCH("composite", k_composite_values, elementwise_grid(nr, 4), 128, 0, static_cast<cudaStream_t>(stream),
-              values, dt, ray_ids, nr, samples, reinterpret_cast<const float4*>(lut), tf_params(tf), comp_params(comp),
-              reinterpret_cast<float4*>(out));
+  APMG_ARG_CHECK(ray_ids && state && out, "null argument");
+  APMG_LAUNCH("composite_finish", k_composite_finish, elementwise_grid(nr, 4), 128, 0,
+              static_cast<cudaStream_t>(stream), ray_ids, nr, reinterpret_cast<const float4*>(state),
+              comp_params(comp), reinterpret_cast<float4*>(out));
   return APMG_OK;
 }
 

@@ -40,6 +40,19 @@ def test_ray_box_hits_bit_exact(golden):
     assert not PR.ray_box_hits(np.array([0.0, 2.0, 5.0]), np.array([[0.0, 0.0, -1.0]]))[2][0]
 
 
+@pytest.mark.parametrize("cam", [dict(eye=(1.5, 1.0, 2.5), look_at=(0.0, 0.0, 0.0), width=12, height=10),
+                                 dict(eye=(-1.2, 0.9, 2.2), look_at=(0.1, 0.0, 0.0), fov_deg=50, width=33, height=17),
+                                 dict(eye=(0.2, -3.0, 0.1), look_at=(0.0, 0.3, 0.0), up=(0.0, 0.0, 1.0), fov_deg=100,
+                                      width=1, height=7)])
+def test_device_rays_bit_exact(cam):
+    c = PR.Camera(**cam)
+    o1, d1 = PR.generate_rays(c)
+    o2, d2 = PR.generate_rays_device(c)
+    assert np.array_equal(o1, o2) and np.array_equal(d1, d2.cpu().numpy())
+    o3, d3 = R.rays(c.eye, c.look_at, c.up, c.fov_deg, c.width, c.height)
+    assert np.array_equal(d1, d3)
+
+
 def test_transfer_function_bit_exact(golden):
     g = golden("render")
     tf = PR.TransferFunction(TF_COLORS, TF_ALPHA, (0.1, 0.8))

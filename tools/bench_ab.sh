@@ -3,7 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 var=$1; vals=$2; shift 2
 for v in $vals; do
-  env "$var=$v" python bench.py --no-cpu-baseline --no-inference "$@" 2>/dev/null | python -c "
+  env "$var=$v" python bench.py --no-cpu-baseline --no-inference --no-render "$@" 2>/dev/null | python -c "
 import json, sys
 d = json.loads(sys.stdin.read())
 e = d.get('e2e') or {}
