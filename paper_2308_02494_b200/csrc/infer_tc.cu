@@ -270,31 +270,41 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
       {
         const float* tfw = sTF + 12 * (4 * warp);
   #pragma unroll
-        for (int h = 0; h < P / 32; ++h) {
-          const int p = lane + 32 * h;
-          const float x0 = cX[3 * p], x1 = cX[3 * p + 1], x2 = cX[3 * p + 2];
-          float fv[8];
+        for (int hp = 0; hp < P / 64; ++hp) {  // two points per pass: lane + 64 hp, lane + 64 hp + 32
+          const int pa = lane + 64 * hp, pb = pa + 32;
+          const float2 X0 = make_float2(cX[3 * pa], cX[3 * pb]), X1 = make_float2(cX[3 * pa + 1], cX[3 * pb + 1]),
+                       X2 = make_float2(cX[3 * pa + 2], cX[3 * pb + 2]);
+          float fv[2][8];
   #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const int m = 4 * warp + g;
             const float* tf = tfw + 12 * g;
-            const float l0 = local_coord(x0, x1, x2, tf[0], tf[1], tf[2], tf[3]);
-            const float l1 = local_coord(x0, x1, x2, tf[4], tf[5], tf[6], tf[7]);
-            const float l2 = local_coord(x0, x1, x2, tf[8], tf[9], tf[10], tf[11]);
-            const bool inside = (fabsf(l0) <= 1.f) && (fabsf(l1) <= 1.f) && (fabsf(l2) <= 1.f);
-            int ix, iy, iz;
-            double fxd, fyd, fzd;
-            axis_term(l0, md.W, ix, fxd);
-            axis_term(l1, md.H, iy, fyd);
-            axis_term(l2, md.D, iz, fzd);
-            float f0 = 0.f, f1 = 0.f;
-            if (inside)
-              interp_pair_f32(md.grid, md.W, md.H * md.W, ((m * md.D + iz) * md.H + iy) * md.W + ix, float(fxd),
-                              float(fyd), float(fzd), f0, f1);
-            fv[2 * g] = f0;
-            fv[2 * g + 1] = f1;
+            const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
+            const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
+            const float2 l2 = local_coord2(X0, X1, X2, tf[8], tf[9], tf[10], tf[11]);
+            int ix[2], iy[2], iz[2];
+            float fx[2], fy[2], fz[2];
+            axis_term2(l0, md.W, ix[0], ix[1], fx[0], fx[1]);
+            axis_term2(l1, md.H, iy[0], iy[1], fy[0], fy[1]);
+            axis_term2(l2, md.D, iz[0], iz[1], fz[0], fz[1]);
+            const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
+  #pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const bool inside = (fabsf(la[k][0]) <= 1.f) && (fabsf(la[k][1]) <= 1.f) && (fabsf(la[k][2]) <= 1.f);
+              float f0 = 0.f, f1 = 0.f;
+              if (inside) {
+                const int vb = ((m * md.D + iz[k]) * md.H + iy[k]) * md.W + ix[k];
+                if (md.gridx)
+                  interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
+                else
+                  interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
+              }
+              fv[k][2 * g] = f0;
+              fv[k][2 * g + 1] = f1;
+            }
           }
-          umma::store_chunk3(F, F_PLANE, p, 8 * warp, P, fv);
+          umma::store_chunk3(F, F_PLANE, pa, 8 * warp, P, fv[0]);
+          umma::store_chunk3(F, F_PLANE, pb, 8 * warp, P, fv[1]);
         }
       }
       umma::fence_async_smem();
@@ -364,6 +374,23 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
     }
     APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   }
+  // x-pair copy of the grid (ModelDev::gridx): 4 float4 corner loads per (point, grid) for
+  // point lists (renderer samples: 19.1 vs 21.6 ms per 512^2 x 128 frame); lattice sweeps hit
+  // L1 for most corners already and measured 2% slower with it, so they read the grid itself
+  static float4* gx = nullptr;
+  static int64_t gx_cap = 0;
+  const int64_t cells = int64_t(a.md.M) * a.md.D * a.md.H * a.md.W;
+  const char* eg = getenv("APMG_GRIDX");
+  const bool use_gx = a.mode == kFwdPts && !(eg && eg[0] == '0');
+  if (use_gx) {
+    if (cells > gx_cap) {
+      if (gx) APMG_CUDA_TRY(cudaFree(gx));
+      APMG_CUDA_TRY(cudaMalloc(&gx, sizeof(float4) * cells));
+      gx_cap = cells;
+    }
+    APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(cells, 8), 256, 0, st,
+                reinterpret_cast<const float2*>(a.md.grid), gx, cells);
+  }
   static bool attr = false;
   if (!attr) {
     APMG_CUDA_TRY(cudaFuncSetAttribute(itc::k_infer_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -375,6 +402,7 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const char* es = getenv("APMG_INFER_STAMPS");
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
+  b.md.gridx = use_gx ? gx : nullptr;
   if (a.mode == kFwdPts)
     APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   else

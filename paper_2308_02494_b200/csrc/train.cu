@@ -28,7 +28,6 @@ __global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const flo
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
                              const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx);
-__global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);
 constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
                              uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
