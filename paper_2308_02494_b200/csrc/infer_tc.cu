@@ -40,8 +40,9 @@ constexpr uint32_t OFF_X = OFF_H1 + 3 * H1_PLANE;     // [2][P][3] (tile parity)
 constexpr uint32_t OFF_TRU = OFF_X + 2 * P * 3 * 4;   // [3][P] truth values (tile index mod 3)
 constexpr uint32_t OFF_HEAD = OFF_TRU + 3 * P * 4;    // [WQ][P]
 constexpr uint32_t OFF_RED = OFF_HEAD + WQ * P * 4;   // [32] doubles
-constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // 4 mbarriers: z1 done, z2 done, F ready, h1 ready
-constexpr uint32_t OFF_TM = OFF_BAR + 32;
+constexpr int NQ = 4;  // z1 is issued in NQ K-slices, each as soon as its NW / NQ encoding warps are done
+constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // mbarriers: z1 done, z2 done, h1 ready, F slice 0..NQ-1 ready
+constexpr uint32_t OFF_TM = OFF_BAR + 8 * (3 + NQ);
 constexpr uint32_t OFF_W3 = OFF_TM + 16;              // [64]
 constexpr uint32_t OFF_TF = OFF_W3 + 64 * 4;          // [64][12] transforms (f32)
 constexpr uint32_t SMEM_BYTES = OFF_TF + 64 * 12 * 4;
@@ -110,8 +111,8 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   double* red = reinterpret_cast<double*>(sm + OFF_RED);
   uint64_t* bar1 = reinterpret_cast<uint64_t*>(sm + OFF_BAR);  // z1 committed
   uint64_t* bar2 = bar1 + 1;                                     // z2 committed
-  uint64_t* barF = bar1 + 2;                                     // F written by all worker warps
-  uint64_t* barH = bar1 + 3;                                     // h1 written by all worker warps
+  uint64_t* barF = bar1 + 3;  // barF[s]: F columns of K-slice s written by worker warps s NW/NQ .. (s+1) NW/NQ - 1
+  uint64_t* barH = bar1 + 2;                                     // h1 written by all worker warps
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
   float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
 
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   if (tid == 0) {
     umma::mbar_init(bar1, 1);
     umma::mbar_init(bar2, 1);
-    umma::mbar_init(barF, NW);
+    for (int q = 0; q < NQ; ++q) umma::mbar_init(barF + q, NW / NQ);
     umma::mbar_init(barH, NW);
     umma::fence_mbar_init();
   }
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   const uint32_t tmem = *tm_slot;
   const uint32_t TZ1 = tmem, TZ2 = tmem + 64;
   const uint32_t lane_base = uint32_t(32 * quarter) << 16;
-  const uint32_t sW1 = umma::smem_u32(W1), sW2 = umma::smem_u32(W2), sF = umma::smem_u32(F), sH1 = umma::smem_u32(H1);
+  const uint32_t base16 = umma::smem_u32(sm) >> 4;  // descriptors: base16 + compile-time fields
   const uint32_t idesc = umma::idesc_bf16(128, 64, false, false);
   const int ep_row = 32 * quarter + lane;  // M=128 accumulator: row = lane
   const int ep_col0 = EPC * wq;
@@ -188,15 +189,24 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
     // ---- MMA warp: z1 when the workers' F is complete, z2 when their h1 is ----
     uint32_t pf = 0, ph = 0;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      umma::mbar_wait(barF, pf);
-      pf ^= 1;
-      umma::fence_after_sync();
-      if (lane == 0) {
-        for (int kk = 0; kk < FE / 16; ++kk)
+      // z1 in NQ K-slices: slice s as soon as warps s NW/NQ .. have encoded its grids, so all but
+      // the last slice of the products overlap the slower warps' encode
 #pragma unroll
-          for (int q = 0; q < 6; ++q)
-            umma::mma_bf16(TZ1, umma::desc_kmajor(sF + kPA(q) * F_PLANE, P, kk),
-                           umma::desc_kmajor(sW1 + kPB(q) * W1_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
+      for (int sl = 0; sl < NQ; ++sl) {
+        umma::mbar_wait(barF + sl, pf);
+        umma::fence_after_sync();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = sl * (FE / 16 / NQ); kk < (sl + 1) * (FE / 16 / NQ); ++kk)
+#pragma unroll
+            for (int q = 0; q < 6; ++q)
+              umma::mma_bf16_c(TZ1, base16, umma::kmajor_c(OFF_F + kPA(q) * F_PLANE, P, kk),
+                               umma::kmajor_c(OFF_W1 + kPB(q) * W1_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
+        }
+        __syncwarp();
+      }
+      pf ^= 1;
+      if (lane == 0) {
         umma::commit(bar1);
       }
       __syncwarp();
@@ -204,11 +214,12 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
       ph ^= 1;
       umma::fence_after_sync();
       if (lane == 0) {
+#pragma unroll
         for (int kk = 0; kk < HID / 16; ++kk)
 #pragma unroll
           for (int q = 0; q < 6; ++q)
-            umma::mma_bf16(TZ2, umma::desc_kmajor(sH1 + kPA(q) * H1_PLANE, P, kk),
-                           umma::desc_kmajor(sW2 + kPB(q) * W2_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
+            umma::mma_bf16_c(TZ2, base16, umma::kmajor_c(OFF_H1 + kPA(q) * H1_PLANE, P, kk),
+                             umma::kmajor_c(OFF_W2 + kPB(q) * W2_PLANE, 64, kk), idesc, (kk | q) ? 1u : 0u);
         umma::commit(bar2);
       }
       __syncwarp();
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
       }
       umma::fence_async_smem();
       __syncwarp();
-      if (lane == 0) umma::mbar_arrive(barF);  // this warp's F columns are in place
+      if (lane == 0) umma::mbar_arrive(barF + warp / (NW / NQ));  // this warp's F columns are in place
       ITC_STAMP(2);
       publish_coords(nxt, it + 1);  // next tile's inputs (slots not read until then)
       // ---- head of the previous tile (overlaps z1 of this one); its worker barrier also

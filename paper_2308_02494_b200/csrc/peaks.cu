@@ -11,6 +11,10 @@
 //           (operands in smem, contents irrelevant); work = FLOP
 //   kind 5  warp shuffles (__shfl_sync, 32-bit); work = shuffle instructions (per warp)
 //   kind 7  L2 gather of random float4 (16-byte) elements; work = bytes loaded
+//   kind 9  tcgen05.mma kind::f16 (bf16), K=16, M = 128 (64 if table_bytes >= 1000), N =
+//           table_bytes % 1000, back to back into one accumulator, or M=128 N=64 alternating
+//           over 4 accumulators (table_bytes = 1):
+//           the per-instruction cost of the small products the MLP kernels issue; work = FLOP
 //   kind 8  L2 RED of random float4 (red.global.add.v4.f32); work = float4 REDs issued
 //   kind 6  shared-memory float atomic adds (red.shared.add.f32), 32 distinct banks per
 //           instruction; work = atomic instructions (per warp)
@@ -143,6 +147,46 @@ __global__ void __launch_bounds__(128) k_peak_tf32(int iters) {
   if (threadIdx.x < 32) umma::tmem_dealloc(tm, 256);
 }
 
+__global__ void __launch_bounds__(128) k_peak_bf16(int iters, int M, int N, int nacc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  unsigned char* A = sm;                  // [128][16] bf16 CM
+  unsigned char* B = sm + 128 * 16 * 2;   // [256][16] bf16 CM
+  for (int e = threadIdx.x; e < (128 + 256) * 16 * 2 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(sm)[e] = 0x3c003c00u;
+  if (threadIdx.x < 32) umma::tmem_alloc(&slot, 256);
+  if (threadIdx.x == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::fence_async_smem();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = umma::idesc_bf16(M, N, false, false);
+    const uint64_t da = umma::desc_kmajor(umma::smem_u32(A), M, 0);
+    const uint64_t db = umma::desc_kmajor(umma::smem_u32(B), N, 0);
+    if (nacc == 1) {
+      umma::mma_bf16(tm, da, db, idesc, 0u);
+      for (int it = 1; it < iters; it += 16)  // unrolled: the issue loop must not be the bound
+#pragma unroll
+        for (int u = 0; u < 16; ++u) umma::mma_bf16(tm, da, db, idesc, 1u);
+    } else {
+      for (int it = 0; it < iters; it += 16)
+#pragma unroll
+        for (int u = 0; u < 16; ++u) umma::mma_bf16(tm + 64 * (u & 3), da, db, idesc, it > 0 || u >= 4);
+    }
+    umma::commit(&bar);
+  }
+  umma::mbar_wait(&bar, 0);
+  umma::fence_after_sync();
+  umma::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) umma::tmem_dealloc(tm, 256);
+}
+
 __global__ void __launch_bounds__(256) k_peak_shfl(int iters, float* __restrict__ sink) {
   float v[4] = {float(threadIdx.x), 1.f, 2.f, 3.f};
   const int lane = threadIdx.x & 31;
@@ -225,6 +269,15 @@ extern "C" int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, i
       APMG_LAUNCH("peak_red4", k_peak_red4, grid, block, 0, st, static_cast<float*>(table),
                   uint32_t(table_bytes / 16 - 1), iters);
       *work = double(grid) * block * iters * 8;
+      return APMG_OK;
+    }
+    case 9: {
+      // table_bytes: N (16..256) + 1000 for M = 64 (else 128); 1 = N 64, 4 accumulators
+      const int nacc = table_bytes == 1 ? 4 : 1;
+      const int N = table_bytes == 1 ? 64 : int(table_bytes % 1000), M = table_bytes >= 1000 ? 64 : 128;
+      const int smem = (128 + 256) * 16 * 2;
+      APMG_LAUNCH("peak_bf16", k_peak_bf16, sms, 128, smem, st, iters, M, N, nacc);
+      *work = double(sms) * iters * 2.0 * M * N * 16;
       return APMG_OK;
     }
     case 6:

@@ -51,6 +51,12 @@ def main():
     out["fp32_tflops"] = probe(2, sink, 64, 4096)[0] / 1e12
     out["fp64_tflops"] = probe(3, sink, 64, 1024)[0] / 1e12
     out["tf32_tcgen05_tflops"] = probe(4, sink, 64, 4096)[0] / 1e12
+    # per-instruction cost of tcgen05.mma kind::f16 K=16 by shape (the MLP kernels issue small N)
+    for nb in (64, 128, 192, 256, 1064, 1128, 1256, 1):
+        f, dt = probe(9, sink, nb, 4096)
+        name = "bf16_m128n64k16_4acc" if nb == 1 else f"bf16_m{64 if nb >= 1000 else 128}n{nb % 1000}k16"
+        out[f"{name}_tflops"] = f / 1e12
+        out[f"{name}_cycles_per_mma"] = dt * 1.965e9 / 4096
     out["shfl_Ginstr_per_s"] = probe(5, sink, 64, 4096)[0] / 1e9
     out["shfl_per_clk_per_sm"] = out["shfl_Ginstr_per_s"] * 1e9 / (out["sms"] * 1.965e9)
     out["atoms_f32_Ginstr_per_s"] = probe(6, sink, 64, 1024)[0] / 1e9
