@@ -232,6 +232,60 @@ def _upload_staged(a: np.ndarray, out) -> None:
     st.synchronize()
 
 
+def _leading_chunks(shape, itemsize, cap):
+    """C-order pieces of an array of `shape` as tuples of slices, each at most `cap` bytes:
+    runs of whole leading-axis slabs, or (when one slab is larger) pieces of one slab."""
+    if len(shape) == 0:
+        return [()]
+    inner = int(np.prod(shape[1:], dtype=np.int64)) * itemsize
+    if inner <= cap:
+        k = max(1, cap // max(inner, 1))
+        return [(slice(i, min(i + k, shape[0])),) for i in range(0, shape[0], k)]
+    return [(i,) + rest for i in range(shape[0]) for rest in _leading_chunks(shape[1:], itemsize, cap)]
+
+
+def upload_view(view: np.ndarray, out) -> None:
+    """Any (strided, memory-mapped) float32 array view -> contiguous device tensor `out`, piece by
+    piece through the pinned ring: host threads gather each C-order piece of the view (page-cache /
+    disk reads of a memmap included) into a staging slot while the copy engine drains the
+    previous ones -- an ingest pipeline with no intermediate full host copy."""
+    t = torch()
+    bufs, events, pool = _staging()
+    flat = out.view(-1)
+    pieces = _leading_chunks(view.shape, view.itemsize, _STAGE_BYTES)
+    st = t.cuda.current_stream()
+    offs, o = [], 0
+    for sl in pieces:
+        n = int(view[sl].size)  # a view of the view: no data is touched
+        offs.append((o, n))
+        o += n
+    if o != flat.numel():
+        raise ValueError(f"upload_view: {o} elements into a {flat.numel()}-element tensor")
+
+    def fill(slot, i):
+        ev = events[slot]
+        if ev is not None:
+            ev.synchronize()
+        piece = view[pieces[i]]
+        dst = bufs[slot][:offs[i][1] * 4].view(t.float32).numpy()
+        np.copyto(dst.reshape(piece.shape), piece, casting="same_kind")
+
+    futs = [None] * _STAGE_SLOTS
+    for i in range(min(_STAGE_SLOTS, len(pieces))):
+        futs[i] = pool.submit(fill, i, i)
+    for i, (o, n) in enumerate(offs):
+        slot = i % _STAGE_SLOTS
+        futs[slot].result()
+        flat[o:o + n].copy_(bufs[slot][:n * 4].view(t.float32), non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(st)
+        events[slot] = ev
+        j = i + _STAGE_SLOTS
+        if j < len(pieces):
+            futs[slot] = pool.submit(fill, slot, j)
+    st.synchronize()
+
+
 def to_device(arr: np.ndarray, dtype=None):
     """Host numpy -> contiguous CUDA tensor (plumbing only); arrays of 4 MiB and more go
     through the pinned staging ring."""

@@ -564,3 +564,24 @@ def test_gridx_pair_copy_matches_plain_grid(monkeypatch):
     b = run()
     assert a.l_rec[0] == b.l_rec[0]
     np.testing.assert_allclose(a.l_rec, b.l_rec, rtol=1e-3)
+
+
+@pytest.mark.gpu
+def test_subvolume_ingest_pipeline_bit_exact(tmp_path):
+    """load_subvolume_device (memmap -> pinned staging ring -> GPU, no host copy of the brick)
+    returns exactly load_subvolume's voxels and value range, for slab-sized and row-split pieces."""
+    vol = PV.synth_volume((37, 29, 23), C1_BLOBS)
+    hdr = PV.save_volume(vol, tmp_path / "v.raw")
+    for lo, hi in [((0, 0, 0), (36, 28, 22)), ((3, 5, 2), (20, 27, 19)), ((7, 0, 22), (7, 28, 22))]:
+        ext = PV.Extent(lo=lo, hi=hi)
+        a = PV.load_subvolume(tmp_path / "v.raw", hdr, ext)
+        b = PV.load_subvolume_device(tmp_path / "v.raw", hdr, ext)
+        assert np.array_equal(a.data, L.to_host(b.device_data())) and (a.vmin, a.vmax) == (b.vmin, b.vmax)
+    big = np.random.default_rng(0).random((2, 3000, 1500), dtype=np.float32)  # one slab > 16 MiB slot
+    out = L.empty(big.shape, np.float32)
+    L.upload_view(big, out)
+    assert np.array_equal(L.to_host(out), big)
+    view = big[:, 100:2900, 7:1207]
+    out2 = L.empty(view.shape, np.float32)
+    L.upload_view(view, out2)
+    assert np.array_equal(L.to_host(out2), view)
