@@ -313,21 +313,33 @@ __global__ void __launch_bounds__(kTileThreads) k_recon(ReconArgs<T> a) {
 }
 
 // Deterministic reduction of the per-CTA partials: w grads and the f64 loss.
+constexpr int kFinLanes = 8;
+
 template <typename T>
 __global__ void k_recon_finalize(int nblocks, int F, const T* __restrict__ part_dw,
                                  const double* __restrict__ part_loss, int64_t n, T* dw1, T* dw2, T* dw3,
                                  double* loss, TrainCtl* ctl, double* l_rec_log) {
   if (ctl && ctl->skip) return;
   const int DW = kHidden * F + kHidden * kHidden + kHidden;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < DW; e += gridDim.x * blockDim.x) {
+  // kFinLanes lanes per weight element, each summing every kFinLanes-th CTA partial, then a
+  // shuffle tree: the 148-deep dependent add chain per element was latency-bound
+  // (launched with kFinLanes * DW threads rounded up to whole blocks: every lane reaches the shuffles)
+  const int sub = threadIdx.x % kFinLanes;
+  {
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) / kFinLanes;
     T acc = T(0);
-    for (int b = 0; b < nblocks; ++b) acc += part_dw[int64_t(b) * DW + e];
+    if (e < DW)
+      for (int b = sub; b < nblocks; b += kFinLanes) acc += part_dw[int64_t(b) * DW + e];
+#pragma unroll
+    for (int o = kFinLanes / 2; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o, kFinLanes);
+    if (sub == 0 && e < DW) {
     if (e < kHidden * F)
       dw1[e] = acc;
     else if (e < kHidden * F + kHidden * kHidden)
       dw2[e - kHidden * F] = acc;
     else
       dw3[e - kHidden * F - kHidden * kHidden] = acc;
+    }
   }
   if (blockIdx.x == 0) {
     __shared__ double red[32];
@@ -437,7 +449,7 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
     else
       APMG_LAUNCH("recon_fwd_bwd", (k_recon<T, false>), grid, kTileThreads, smem, st, a);
   }
-  const int fin_grid = int(ceil_div(int64_t(DW), 256));
+  const int fin_grid = int(ceil_div(int64_t(DW) * kFinLanes, 256));
   APMG_LAUNCH("recon_finalize", k_recon_finalize<T>, fin_grid, 256, 0, st, grid, md.F, part_dw, part_loss, n, dw1,
               dw2, dw3, loss, const_cast<TrainCtl*>(ctl), l_rec_log);
   return APMG_OK;
