@@ -187,6 +187,11 @@ size_t apmg_decomposed_workspace_bytes(int32_t bricks, int64_t n);
 int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
                             const double* scale, const double* offset, const float* pts, int64_t n,
                             float* out, void* workspace, size_t workspace_bytes, void* stream);
+/* apmg_decomposed_forward through the tensor-core sweep kernel per brick (the renderer's
+ * decomposed-field queries): within the forward gate of the exact path, not bit-equal to it. */
+int apmg_decomposed_forward_tc(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
+                               const double* scale, const double* offset, const float* pts, int64_t n, float* out,
+                               void* workspace, size_t workspace_bytes, void* stream);
 /* Lattice sweep of one model over the voxel box [x0,x1]x[y0,y1]x[z0,z1] of a
  * (W,H,D) lattice (axis_coords, volume.py:161-165), optionally through a
  * brick affine (scale/offset HOST f64[3] or NULL).  If truth != NULL the f64

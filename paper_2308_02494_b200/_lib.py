@@ -85,6 +85,8 @@ SIGNATURES = {
     "apmg_decomposed_workspace_bytes": (_SZ, [_I32, _I64]),
     "apmg_decomposed_forward": (C.c_int, [_MP, _I32, _I32, _I32, _I32, C.POINTER(_D), C.POINTER(_D), _P, _I64,
                                           _P, _P, _SZ, _P]),
+    "apmg_decomposed_forward_tc": (C.c_int, [_MP, _I32, _I32, _I32, _I32, C.POINTER(_D), C.POINTER(_D), _P, _I64,
+                                          _P, _P, _SZ, _P]),
     "apmg_lattice_sweep": (C.c_int, [_MP, _I32, _I32, _I32, C.POINTER(_I32), C.POINTER(_D), C.POINTER(_D), _P,
                                      _P, _P, _P]),
     "apmg_brick_sweep": (C.c_int, [_MP, _I32, _I32, _I32, C.POINTER(_I32), C.POINTER(_D), C.POINTER(_D), _P,

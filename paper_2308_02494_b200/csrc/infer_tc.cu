@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
         const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
         if (a.mode == kFwdPts) {
           a.out[i] = y;
+        } else if (a.mode == kFwdGather) {
+          a.gout[a.index[i]] = y;
         } else if (a.recon) {
           a.recon[voxel_of(a, i)] = y;
         }
@@ -239,12 +241,8 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
       Pre r{0.f, 0.f, 0.f, 0.f};
       const int t = tid - (NT - P);
       const int64_t i = tile * P + t;
-      if (a.mode == kFwdPts) {  // point list (renderer samples): coordinates as given
-        if (t >= 0 && tile < tiles && i < a.n) {
-          r.x0 = __ldg(a.pts + 3 * i);
-          r.x1 = __ldg(a.pts + 3 * i + 1);
-          r.x2 = __ldg(a.pts + 3 * i + 2);
-        }
+      if (a.mode != kFwdLattice) {  // point list / brick gather (renderer queries): fwd_point
+        if (t >= 0 && tile < tiles && i < a.n) fwd_point(a, i, r.x0, r.x1, r.x2);
         return r;
       }
       if (t >= 0 && tile < tiles && i < a.n) {
@@ -369,7 +367,7 @@ extern "C" int apmg_debug_infer_phases(long long* out) {
 
 bool infer_tc_eligible(const FwdArgs<float>& a) {
   const char* e = getenv("APMG_MLP");  // APMG_MLP=simt keeps the SIMT sweep (A/B tests)
-  return !(e && e[0] == 's') && (a.mode == kFwdLattice || (a.mode == kFwdPts && a.tc_points)) &&
+  return !(e && e[0] == 's') && (a.mode == kFwdLattice || ((a.mode == kFwdPts || a.mode == kFwdGather) && a.tc_points)) &&
          a.md.F == 128 && a.md.C == 2 && a.md.M == 64;
 }
 
@@ -392,7 +390,7 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   static int64_t gx_cap = 0;
   const int64_t cells = int64_t(a.md.M) * a.md.D * a.md.H * a.md.W;
   const char* eg = getenv("APMG_GRIDX");
-  const bool use_gx = a.mode == kFwdPts && !(eg && eg[0] == '0');
+  const bool use_gx = a.mode != kFwdLattice && !(eg && eg[0] == '0');
   if (use_gx) {
     if (cells > gx_cap) {
       if (gx) APMG_CUDA_TRY(cudaFree(gx));
@@ -414,7 +412,7 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
   b.md.gridx = use_gx ? gx : nullptr;
-  if (a.mode == kFwdPts)
+  if (a.mode != kFwdLattice)
     APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   else
     APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);

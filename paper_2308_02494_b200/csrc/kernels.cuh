@@ -57,4 +57,4 @@ size_t density_ws_bytes(int M, int64_t n);
 }  // namespace apmg
 
 int apmg_internal_forward_gather(const apmg_model* m, const double* sc, const double* of, const float* pts,
-                                 const int32_t* index, int64_t n, float* out, cudaStream_t st);
+                                 const int32_t* index, int64_t n, float* out, cudaStream_t st, int tc = 0);

@@ -517,9 +517,9 @@ extern "C" size_t apmg_decomposed_workspace_bytes(int32_t bricks, int64_t n) {
   return c.used + 256;
 }
 
-extern "C" int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
-                                       const double* scale, const double* offset, const float* pts, int64_t n,
-                                       float* out, void* workspace, size_t workspace_bytes, void* stream) {
+static int decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
+                              const double* scale, const double* offset, const float* pts, int64_t n, float* out,
+                              void* workspace, size_t workspace_bytes, void* stream, int tc) {
   APMG_ARG_CHECK(bricks == bi * bj * bk && bricks >= 1, "model count does not match brick counts");
   if (n <= 0) return APMG_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -557,10 +557,25 @@ extern "C" int apmg_decomposed_forward(const apmg_model* models, int32_t bricks,
   for (int b = 0; b < bricks; ++b) {
     if (!h_counts[b]) continue;
     int rc = apmg_internal_forward_gather(&models[b], scale + 3 * b, offset + 3 * b, pts, index + h_off[b],
-                                          h_counts[b], out, st);
+                                          h_counts[b], out, st, tc);
     if (rc) return rc;
   }
   // keep the host staging alive until the H2D copy has been consumed
   APMG_CUDA_TRY(cudaStreamSynchronize(st));
   return APMG_OK;
+}
+
+extern "C" int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
+                                       const double* scale, const double* offset, const float* pts, int64_t n,
+                                       float* out, void* workspace, size_t workspace_bytes, void* stream) {
+  return decomposed_forward(models, bricks, bi, bj, bk, scale, offset, pts, n, out, workspace, workspace_bytes, stream,
+                            0);
+}
+
+extern "C" int apmg_decomposed_forward_tc(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj,
+                                          int32_t bk, const double* scale, const double* offset, const float* pts,
+                                          int64_t n, float* out, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
+  return decomposed_forward(models, bricks, bi, bj, bk, scale, offset, pts, n, out, workspace, workspace_bytes, stream,
+                            1);
 }

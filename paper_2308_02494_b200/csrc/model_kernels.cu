@@ -624,7 +624,7 @@ extern "C" int apmg_brick_sweep(const apmg_model* m, int32_t w, int32_t h, int32
 
 // Grouped forward over one brick's point list (used by apmg_decomposed_forward).
 int apmg_internal_forward_gather(const apmg_model* m, const double* sc, const double* of, const float* pts,
-                                 const int32_t* index, int64_t n, float* out, cudaStream_t st) {
+                                 const int32_t* index, int64_t n, float* out, cudaStream_t st, int tc) {
   int rc = check_model(m);
   if (rc) return rc;
   APMG_ARG_CHECK(m->dtype == APMG_F32, "decomposed inference supports float32 brick models");
@@ -642,6 +642,7 @@ int apmg_internal_forward_gather(const apmg_model* m, const double* sc, const do
   a.gpts = pts;
   a.index = index;
   a.gout = out;
+  a.tc_points = tc;  // tensor-core sweep kernel (renderer queries) instead of the exact forward
   return launch_forward<float>(a, st);
 }
 
