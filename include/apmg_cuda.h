@@ -219,6 +219,11 @@ typedef struct apmg_train_config {
   int64_t plateau_max_triggers;
   uint64_t key0, key1; /* Philox key of TrainConfig.seed */
   int32_t train_transforms, plateau_enabled;
+  /* 1: run-to-run bit-deterministic training (the reference's determinism contract,
+   * test_acceptance.py:332-367): batch order within each spatial bucket restored by a stable
+   * pass, grid gradient accumulated in 64-bit fixed point (2^-44) with integer REDs.  0: float
+   * REDs in arrival order (faster; sums differ in the last bits between runs). */
+  int32_t deterministic, reserved;
 } apmg_train_config;
 
 typedef struct apmg_train_state apmg_train_state;

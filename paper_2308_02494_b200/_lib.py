@@ -36,6 +36,7 @@ class ApmgTrainConfigC(C.Structure):
         ("plateau_window", C.c_int64), ("plateau_threshold", C.c_double), ("plateau_factor", C.c_double),
         ("plateau_max_triggers", C.c_int64), ("key0", C.c_uint64), ("key1", C.c_uint64),
         ("train_transforms", C.c_int32), ("plateau_enabled", C.c_int32),
+        ("deterministic", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

@@ -27,7 +27,8 @@ struct FwdArgs {
   double sc0, sc1, sc2, of0, of1, of2;
   const float* truth;   // [LD][LH][LW] or null
   float* recon;         // [LD][LH][LW] or null
-  double* sse;          // accumulated (atomic f64) when truth != null
+  double* sse;          // accumulated when truth != null: sse_part[block] per CTA, then k_sse_finalize
+  double* sse_part;     // [gridDim.x] per-CTA sums (fixed-order final reduction: deterministic)
   // gather (kFwdGather): global f32 points through an index list
   const float* gpts;    // [*][3]
   const int32_t* index; // [n] point ids of this brick

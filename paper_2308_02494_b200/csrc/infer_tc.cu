@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   }
   if (a.truth) {
     const double s = block_sum(sse, red);
-    if (tid == 0) atomicAdd(a.sse, s);
+    if (tid == 0) a.sse_part[blockIdx.x] = s;
   }
   umma::fence_before_sync();
   __syncthreads();
@@ -412,10 +412,15 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
   b.md.gridx = use_gx ? gx : nullptr;
+  if (a.mode == kFwdLattice && a.truth) {
+    b.sse_part = sse_parts(grid);
+    APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
+  }
   if (a.mode != kFwdLattice)
     APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   else
     APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
+  if (a.mode == kFwdLattice && a.truth) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
   return APMG_OK;
 }
 

@@ -209,13 +209,44 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(int32_t* __restrict__ coun
 }
 
 __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
-                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out, const TrainCtl* ctl) {
+                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out,
+                                 int32_t* __restrict__ perm, const TrainCtl* ctl) {
   if (ctl->skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pos = atomicAdd(&cursor[key[i]], 1);
     c64_out[3 * pos] = c64[3 * i];
     c64_out[3 * pos + 1] = c64[3 * i + 1];
     c64_out[3 * pos + 2] = c64[3 * i + 2];
+    if (perm) perm[pos] = int32_t(i);
+  }
+}
+
+// Deterministic mode: the atomic cursor leaves the points of a bucket in arrival order; put them
+// back in batch order (one warp per bucket: rank = number of the bucket's points with a smaller
+// batch index), writing c64_out.  `end` holds each bucket's end offset after the scatter.
+__global__ void k_bucket_stable(const double* __restrict__ c64_in, const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ end, int nbuckets, double* __restrict__ c64_out,
+                                const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  const int lane = threadIdx.x & 31;
+  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbuckets; b += (gridDim.x * blockDim.x) >> 5) {
+    const int lo = b ? end[b - 1] : 0, n = end[b] - lo;
+    for (int k0 = 0; k0 < n; k0 += 32) {  // warp-uniform loops: every lane reaches the shuffles
+      const int k = k0 + lane;
+      const int pk = k < n ? perm[lo + k] : 0x7fffffff;
+      int rank = 0;
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int pj = j0 + lane < n ? perm[lo + j0 + lane] : 0x7fffffff;
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) rank += __shfl_sync(0xffffffffu, pj, t) < pk;
+      }
+      if (k < n) {
+        const int64_t src = lo + k, dst = lo + rank;
+        c64_out[3 * dst] = c64_in[3 * src];
+        c64_out[3 * dst + 1] = c64_in[3 * src + 1];
+        c64_out[3 * dst + 2] = c64_in[3 * src + 2];
+      }
+    }
   }
 }
 
@@ -396,12 +427,21 @@ __global__ void k_adam(T* __restrict__ p, const T* __restrict__ g, T* __restrict
 // element (cell c, channel ch) sums dgx[c].lo and dgx[c - 1].hi, and clears both.
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx) {
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx,
+                             unsigned long long* __restrict__ gfx, int64_t fx_elems) {
   if (ctl->skip) return;
   const T lr_t = T(ctl->lr_main_t), c1 = T(ctl->bc1_main), c2 = T(ctl->bc2_main);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const bool pair = sizeof(T) == 4 && dgx && i < gx_elems;
-    T gi = pair ? T(0) : g[i];
+    const bool fx = gfx && i < fx_elems;  // deterministic mode: fixed-point grid gradient
+    T gi = (pair || fx) ? T(0) : g[i];
+    if (fx) {
+      const unsigned long long q = gfx[i];
+      if (q) {
+        gfx[i] = 0ull;
+        gi = T(double(static_cast<long long>(q)) * kFxInv);
+      }
+    }
     if constexpr (sizeof(T) == 4) {
       if (pair) {
         const int64_t c = i >> 1, ch = i & 1;
@@ -417,7 +457,7 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
     p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    if (!pair) g[i] = T(0);
+    if (!pair && !fx) g[i] = T(0);
     if constexpr (sizeof(T) == 4) {
       if (gx && i < gx_elems) {
         const int64_t c = i >> 1, ch = i & 1;
@@ -429,9 +469,9 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
 }
 
 template __global__ void k_adam_train<float>(float*, float*, float*, float*, int64_t, const TrainCtl*, float*,
-                                             int64_t, float*);
+                                             int64_t, float*, unsigned long long*, int64_t);
 template __global__ void k_adam_train<double>(double*, double*, double*, double*, int64_t, const TrainCtl*, float*,
-                                              int64_t, float*);
+                                              int64_t, float*, unsigned long long*, int64_t);
 
 // gridx[c] = (grid[c], grid[c + 1]) for the flat two-channel cells c (zero past the end)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells) {

@@ -20,6 +20,12 @@
 
 namespace apmg {
 
+// fixed-point scale of the deterministic grid gradient: 2^44 (resolution 5.7e-14, range +-5.2e5)
+constexpr double kFxScale = 17592186044416.0, kFxInv = 1.0 / 17592186044416.0;
+__device__ __forceinline__ void red_fx(unsigned long long* addr, double v) {
+  atomicAdd(addr, static_cast<unsigned long long>(__double2ll_rn(v * kFxScale)));
+}
+
 template <typename T>
 struct ModelDev {
   int M, C, D, H, W, F, p;
@@ -37,6 +43,9 @@ struct ModelDev {
   // (dgridx[c] = d/d(grid[c]), d/d(grid[c + 1]) partial sums; float4 REDs, half the RED
   // operations): grad(grid[v]) = dgridx[v].lo + dgridx[v - 1].hi.  tc16 kernel only.
   bool grad_pairs = false;
+  // deterministic training: the grid gradient is accumulated as 64-bit fixed point (kFxScale)
+  // with integer REDs -- associative, so the sum is independent of arrival order
+  unsigned long long* dgrid_fx = nullptr;
 };
 
 template <typename T>
@@ -373,6 +382,7 @@ __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float
   }
 }
 
+template <bool FX = false>  // FX: deterministic fixed-point gradient (ModelDev::dgrid_fx)
 __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,
                                                           bool valid, int vbase, float fx, float fy, float fz,
                                                           float g0, float g1) {
@@ -405,6 +415,17 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
     }
   }
   if (!leader) return;
+  if constexpr (FX) {
+    unsigned long long* base = md.dgrid_fx + (size_t(vbase) << 1);
+    const int sy = 2 * md.W, sz = 2 * md.H * md.W;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      unsigned long long* a = base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1);
+      red_fx(a, v[c].x);
+      red_fx(a + 1, v[c].y);
+    }
+    return;
+  }
   if (md.grad_pairs) {
     float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
 #pragma unroll
@@ -425,6 +446,19 @@ __device__ __forceinline__ void scatter_grid_point(const ModelDev<T>& md, T* __r
   const Cell c = cell_of(md, md.tf + 16 * m, x0, x1, x2);
   if (!c.inside) return;
   const int C = md.C;
+  if (md.dgrid_fx) {  // deterministic mode: each contribution rounded to T, then fixed point
+    const int64_t fsy = int64_t(md.W) * C, fsz = int64_t(md.H) * md.W * C;
+    unsigned long long* fb = md.dgrid_fx + ((((int64_t)m * md.D + c.iz) * md.H + c.iy) * md.W + c.ix) * C;
+    for (int cz = 0; cz < 2; ++cz)
+      for (int cy = 0; cy < 2; ++cy)
+        for (int cx = 0; cx < 2; ++cx) {
+          const double w = mul_rn(mul_rn(cx ? c.fx : 1.0 - c.fx, cy ? c.fy : 1.0 - c.fy), cz ? c.fz : 1.0 - c.fz);
+          for (int ch = 0; ch < C; ++ch)
+            red_fx(fb + cz * fsz + cy * fsy + cx * C + ch,
+                   static_cast<double>(to_model<T>(mul_rn(static_cast<double>(g[ch * g_stride]), w))));
+        }
+    return;
+  }
   if constexpr (sizeof(T) == 4) {
     if (C == 2) {
       scatter_pair_f32(md, dgrid, m, c, g[0], g[g_stride]);

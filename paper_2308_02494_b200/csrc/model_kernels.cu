@@ -91,8 +91,38 @@ __global__ void __launch_bounds__(kTileThreads) k_forward(FwdArgs<T> a) {
   }
   if (a.mode == kFwdLattice && a.truth) {
     const double s = block_sum(sse, red);
-    if (tid == 0) atomicAdd(a.sse, s);
+    if (tid == 0) a.sse_part[blockIdx.x] = s;
   }
+}
+
+// *sse += sum of the per-CTA parts in index order (one warp: fixed shuffle tree)
+__global__ void k_sse_finalize(const double* __restrict__ part, int n, double* __restrict__ sse) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) *sse += s;
+}
+
+// per-CTA SSE partials of the lattice sweeps (grown on demand, never freed; one stream order)
+double* sse_parts(int n) {
+  static double* buf = nullptr;
+  static int cap = 0;
+  if (n > cap) {
+    if (buf) cudaFree(buf);
+    if (cudaMalloc(&buf, sizeof(double) * n) != cudaSuccess) {
+      buf = nullptr;
+      cap = 0;
+      return nullptr;
+    }
+    cap = n;
+  }
+  return buf;
+}
+
+int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st) {
+  APMG_LAUNCH("sse_finalize", k_sse_finalize, 1, 32, 0, st, part, n, sse);
+  return APMG_OK;
 }
 
 template <typename T>
@@ -113,7 +143,13 @@ int launch_forward(const FwdArgs<T>& a, cudaStream_t st) {
   APMG_ARG_CHECK(occ > 0, "forward tile does not fit in shared memory (F=%d)", a.md.F);
   const int64_t tiles = ceil_div(a.n, kTileP);
   const int grid = int(min64(tiles, int64_t(num_sms()) * occ));
-  APMG_LAUNCH("forward", k_forward<T>, grid, kTileThreads, smem, st, a);
+  FwdArgs<T> b = a;
+  if (a.mode == kFwdLattice && a.truth) {
+    b.sse_part = sse_parts(grid);
+    APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
+  }
+  APMG_LAUNCH("forward", k_forward<T>, grid, kTileThreads, smem, st, b);
+  if (a.mode == kFwdLattice && a.truth) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
   return APMG_OK;
 }
 
@@ -431,6 +467,8 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
   bool done = false;
   if constexpr (sizeof(T) == 4) {
     if (md.grad_pairs) APMG_ARG_CHECK(recon_tc_eligible(md) && use_tc16(), "x-pair gradients need the tc16 kernel");
+    if (md.dgrid_fx)
+      APMG_ARG_CHECK(!recon_tc_eligible(md) || use_tc16(), "deterministic gradients need the tc16 or SIMT kernel");
     if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
       grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms())));
       // default: bf16x3 all-tcgen05 kernel; APMG_RECON16=0 selects the tf32 / mma.sync one (A/B)

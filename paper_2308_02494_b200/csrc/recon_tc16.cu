@@ -50,8 +50,8 @@ constexpr uint32_t OFF_X = OFF_DZ1 + 3 * PL64x64;       // [2][P][3]
 constexpr uint32_t OFF_T = OFF_X + 2 * P * 3 * 4;       // [2][P]
 constexpr uint32_t OFF_G = OFF_T + 2 * P * 4;           // [P]
 constexpr uint32_t OFF_HEAD = OFF_G + P * 4;            // [WQ][P]
-constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [64]
-constexpr uint32_t OFF_RED = OFF_DW3 + HID * 4;         // [32] doubles
+constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [4 quarters][64]: dW3 per lane quarter, summed in order
+constexpr uint32_t OFF_RED = OFF_DW3 + 4 * HID * 4;     // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
@@ -107,6 +107,7 @@ __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX
 }
 
 // scatter of one (2 grids x 2 points) group (see recon_tc.cu)
+template <bool FX>
 __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const Args& a, const float* GF,
                                               uint32_t tmem_cache, int jq, int cnt, int warp, int lane) {
   if (a.skip & 1) return;
@@ -121,7 +122,7 @@ __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const A
     float2 g = make_float2(0.f, 0.f);
     if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
     if (a.aggregate == 2)
-      scatter_vertex_warp_gather(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
+      scatter_vertex_warp_gather<FX>(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
                                  __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
     else if (a.aggregate)
       scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
@@ -132,6 +133,7 @@ __device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const A
   }
 }
 
+template <bool FX>  // FX: deterministic training (fixed-point grid gradient)
 __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   extern __shared__ __align__(1024) unsigned char sm[];
   if (a.ctl && a.ctl->skip) return;
@@ -165,7 +167,6 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     const int r = e >> 3, c0 = (e & 7) * 8;
     umma::store_chunk3(W2, PL64x64, r, c0, 64, md.w2 + r * HID + c0);
   }
-  if (tid < HID) sDW3[tid] = 0.f;
   for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (tid < HID) sW3[tid] = md.w3[tid];
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   auto encode_tile = [&](const float* cX, int scatter_cnt, int64_t prefetch_tile, int prefetch_slot) {
 #pragma unroll 1
     for (int jq = 0; jq < GPW / 2; ++jq) {
-      if (scatter_cnt >= 0) scatter_group(md, a, GF, tmem_cache, jq, scatter_cnt, warp, lane);
+      if (scatter_cnt >= 0) scatter_group<FX>(md, a, GF, tmem_cache, jq, scatter_cnt, warp, lane);
       encode_group(cX, jq);
       if (jq == 0) {  // features k < 64 (grids 0-31) complete: first half of z1
         umma::fence_async_smem();
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       encode_tile(sX + ((it + 1) & 1) * 3 * P, cnt, next + gridDim.x, it + 2);
     } else {
 #pragma unroll 1
-      for (int jq = 0; jq < GPW / 2; ++jq) scatter_group(md, a, GF, tmem_cache, jq, cnt, warp, lane);
+      for (int jq = 0; jq < GPW / 2; ++jq) scatter_group<FX>(md, a, GF, tmem_cache, jq, cnt, warp, lane);
     }
   }
 
@@ -518,10 +519,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     v += __shfl_xor_sync(0xffffffffu, v, 4);
     v += __shfl_xor_sync(0xffffffffu, v, 8);
     v += __shfl_xor_sync(0xffffffffu, v, 16);
-    if (lane < 4) atomicAdd(&sDW3[ep_col0 + 8 * (c >> 1) + ec + (c & 1)], v);
+    if (lane < 4) sDW3[quarter * HID + ep_col0 + 8 * (c >> 1) + ec + (c & 1)] = v;  // one writer per slot
   }
   const double bl = block_sum(loss, red);  // contains __syncthreads
-  if (tid < HID) dst[HID * FE + HID * HID + tid] = sDW3[tid];
+  if (tid < HID)  // fixed-order sum over the lane quarters: run-to-run deterministic
+    dst[HID * FE + HID * HID + tid] = ((sDW3[tid] + sDW3[HID + tid]) + sDW3[2 * HID + tid]) + sDW3[3 * HID + tid];
   if (tid == 0) a.part_loss[blockIdx.x] = bl;
   umma::fence_before_sync();
   __syncthreads();
@@ -540,7 +542,9 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
                       cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    APMG_CUDA_TRY(cudaFuncSetAttribute(tc16::k_recon_tc16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    APMG_CUDA_TRY(cudaFuncSetAttribute(tc16::k_recon_tc16<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(tc16::SMEM_BYTES)));
+    APMG_CUDA_TRY(cudaFuncSetAttribute(tc16::k_recon_tc16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(tc16::SMEM_BYTES)));
     attr = true;
   }
@@ -550,7 +554,11 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
   tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, ea ? atoi(ea) : 2,
                (es && es[0] == '1') ? 1 : 0, 0};
   if (const char* sk = getenv("APMG_TC_SKIP")) a.skip = atoi(sk);
-  APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
+  if (md.dgrid_fx) a.aggregate = 2;  // the fixed-point (deterministic) scatter lives in the gather variant
+  if (md.dgrid_fx)
+    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<true>, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
+  else
+    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<false>, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
   return APMG_OK;
 }
 

@@ -27,13 +27,18 @@ __global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const flo
                               int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx);
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx,
+                             unsigned long long* __restrict__ gfx, int64_t fx_elems);
 constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
                              uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
 __global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl);
 __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
-                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out, const TrainCtl* ctl);
+                                 int32_t* __restrict__ cursor, double* __restrict__ c64_out,
+                                 int32_t* __restrict__ perm, const TrainCtl* ctl);
+__global__ void k_bucket_stable(const double* __restrict__ c64_in, const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ end, int nbuckets, double* __restrict__ c64_out,
+                                const TrainCtl* ctl);
 template <typename T>
 __global__ void k_sample_sorted(const double* __restrict__ c64, int64_t n, const float* __restrict__ vol, int w,
                                 int h, int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
@@ -142,6 +147,9 @@ struct apmg_train_state {
   uint64_t graph_launches = 0;
   // 8x8x8-bricked copy of the volume for the sorted sampler (owned; APMG_BRICKED=0 disables)
   float4* gridx = nullptr;  // x-pair grid copy (ModelDev::gridx), or null
+  unsigned long long* gfx = nullptr;  // deterministic mode: fixed-point grid gradient [grid elements]
+  int32_t* perm = nullptr;            // deterministic mode: batch index of each bucketed point
+  int64_t fx_elems = 0;
   float4* gradx = nullptr;  // x-pair grid gradient (ModelDev::grad_pairs), or null
   int64_t gx_cells = 0;
   float* vol_bricked = nullptr;
@@ -203,9 +211,16 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   float4* gridx = use_gx ? cv.take<float4>(cells) : nullptr;
   // ... and the x-pair grid gradient when the bf16x3 recon kernel runs (APMG_GRADX=0 off)
   const char* ed = getenv("APMG_GRADX");
-  const bool use_dgx = use_gx && recon_uses_tc16(*m) && !(ed && ed[0] == '0');
+  const bool det = c->deterministic != 0;
+  const bool use_dgx = use_gx && recon_uses_tc16(*m) && !(ed && ed[0] == '0') && !det;
   float4* gradx = use_dgx ? cv.take<float4>(cells) : nullptr;
+  const int64_t gel = cells * m->channels;
+  unsigned long long* gfx = det ? cv.take<unsigned long long>(gel) : nullptr;
+  int32_t* perm = det ? cv.take<int32_t>(B) : nullptr;
   if (s) {
+    s->gfx = gfx;
+    s->perm = perm;
+    s->fx_elems = det ? gel : 0;
     s->gridx = gridx;
     s->gradx = gradx;
     s->gx_cells = use_gx ? cells : 0;
@@ -306,6 +321,7 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   APMG_CUDA_TRY(cudaMemcpyAsync(s->bias, bias_table, sizeof(double) * 2 * cfg->iterations, cudaMemcpyHostToDevice, st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->grad, 0, es * s->off[4], st));
   if (s->gradx) APMG_CUDA_TRY(cudaMemsetAsync(s->gradx, 0, sizeof(float4) * s->gx_cells, st));
+  if (s->gfx) APMG_CUDA_TRY(cudaMemsetAsync(s->gfx, 0, sizeof(unsigned long long) * s->fx_elems, st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->am, 0, es * s->off[4], st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->av, 0, es * s->off[4], st));
   APMG_CUDA_TRY(cudaMemsetAsync(s->tm, 0, es * 16 * shape->grids, st));
@@ -332,6 +348,7 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   ModelDev<T> md = make_model_dev<T>(live);
   md.gridx = s->gridx;
   md.grad_pairs = s->gradx != nullptr;
+  md.dgrid_fx = s->gfx;
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
   if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
@@ -340,13 +357,19 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                 s->counts, s->ctl);
     APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
     APMG_LAUNCH("bucket_scatter", k_bucket_scatter, elementwise_grid(B, 8), 256, 0, st, s->c64_raw, s->key, B,
-                s->counts, s->c64_sorted, s->ctl);
+                s->counts, s->c64_sorted, s->perm, s->ctl);
+    const double* sorted = s->c64_sorted;
+    if (s->perm) {  // deterministic mode: batch order within each bucket (c64_raw is free by now)
+      APMG_LAUNCH("bucket_stable", k_bucket_stable, int(ceil_div(int64_t(kBuckets) * 32, 256)), 256, 0, st,
+                  s->c64_sorted, s->perm, s->counts, kBuckets, s->c64_raw, s->ctl);
+      sorted = s->c64_raw;
+    }
     if (s->vol_bricked)
-      APMG_LAUNCH("train_batch", k_sample_sorted_bricked<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B,
+      APMG_LAUNCH("train_batch", k_sample_sorted_bricked<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
                   s->vol_bricked, s->w, s->h, s->d, s->nbx, s->nby, static_cast<T*>(s->coords),
                   static_cast<T*>(s->targets), s->ctl);
     else
-      APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, s->c64_sorted, B,
+      APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
                   s->volume, s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
   } else {
     APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
@@ -360,7 +383,8 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   if (rc) return rc;
   APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
               static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
-              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx));
+              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx), s->gfx,
+              s->fx_elems);
   if (c.train_transforms) {
     rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, static_cast<const T*>(s->coords),
                               static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),

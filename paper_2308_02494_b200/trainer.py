@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -48,6 +49,10 @@ class TrainConfig:
     seed: int = 0
     train_transforms: bool = True
     plateau_enabled: bool = True
+    # not in the reference (always deterministic on the CPU): True makes GPU training
+    # bit-reproducible run to run (stable batch order, fixed-point grid gradients) at some
+    # speed cost; APMG_DETERMINISTIC=1 forces it for every session
+    deterministic: bool = False
 
     def __post_init__(self):
         if self.iterations < 0 or self.batch_size < 1:
@@ -178,7 +183,8 @@ class TrainSession:
             cfg.iterations, cfg.batch_size, cfg.lr_main, cfg.lr_transform, cfg.delay_start,
             cfg.transform_ma_window, cfg.transform_improve_threshold, cfg.hard_stop_iteration,
             cfg.plateau_window, cfg.plateau_threshold, cfg.plateau_factor, cfg.plateau_max_triggers,
-            int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)))
+            int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)),
+            int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"), 0)
         self.ws = L.workspace(L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg)))
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()

@@ -585,3 +585,54 @@ def test_subvolume_ingest_pipeline_bit_exact(tmp_path):
     out2 = L.empty(view.shape, np.float32)
     L.upload_view(view, out2)
     assert np.array_equal(L.to_host(out2), view)
+
+
+def _train_twice(cfgm, vol, **kw):
+    out = []
+    for _ in range(2):
+        m = PM.init_model(cfgm, seed=0, vmin=vol.vmin, vmax=vol.vmax)
+        cfg = P.TrainConfig(seed=0, plateau_enabled=False, deterministic=True, **kw)
+        m, log = P.train_single(m, vol, cfg)
+        out.append((m, log, P.psnr(m, vol)))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(64, 2, (32, 32, 32)), (2, 1, (4, 4, 4)), (8, 3, (6, 5, 4))])
+def test_deterministic_training_bit_identical(shape):
+    """TrainConfig(deterministic=True): two runs give bit-identical parameters, logs and PSNR
+    (the reference's run-to-run determinism, test_trainer.py:157-166 / test_acceptance.py:332-367),
+    on the tensor-core kernel and on the SIMT kernel (other shapes)."""
+    vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
+    g, c, r = shape
+    (m1, l1, p1), (m2, l2, p2) = _train_twice(PM.ModelConfig(grids=g, channels=c, resolution=r), vol,
+                                              iterations=24, batch_size=1 << 14, delay_start=8)
+    for k in ("grids", "w1", "w2", "w3", "transforms"):
+        assert np.array_equal(getattr(m1, k), getattr(m2, k)), k
+    assert l1.l_rec == l2.l_rec and l1.l_density == l2.l_density and p1 == p2
+
+
+@pytest.mark.gpu
+def test_deterministic_mode_tracks_default_mode():
+    """The deterministic mode changes summation order only: its trajectory stays within the
+    run-to-run noise of the default (float-RED) mode."""
+    vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
+    logs = []
+    for det in (False, True):
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=24, batch_size=1 << 14, delay_start=8, seed=0, plateau_enabled=False,
+                            deterministic=det)
+        logs.append(P.train_single(m, vol, cfg)[1])
+    np.testing.assert_allclose(logs[0].l_rec[0], logs[1].l_rec[0], rtol=1e-6)
+    np.testing.assert_allclose(logs[0].l_rec, logs[1].l_rec, rtol=1e-3)
+
+
+@pytest.mark.gpu
+def test_psnr_sweep_bit_reproducible():
+    """The lattice SSE is reduced per CTA then summed in a fixed order: PSNR repeats exactly."""
+    vol = PV.synth_volume((64, 48, 40), C1_BLOBS)
+    m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(16, 16, 16)), seed=1, vmin=vol.vmin,
+                      vmax=vol.vmax)
+    vals = {P.psnr(m, vol) for _ in range(4)}
+    assert len(vals) == 1
