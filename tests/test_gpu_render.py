@@ -236,3 +236,49 @@ def test_decomposed_tensor_core_queries():
         a = PR.render_frame(field, cam, PR.TransferFunction(), cfg)
         b = PR.render_frame(Proto(), cam, PR.TransferFunction(), cfg)
         np.testing.assert_allclose(a, b, atol=ATOL_MODEL, rtol=0)
+
+
+def test_decomposed_training_and_render_reproducible(tmp_path, monkeypatch):
+    """Criterion 10 (test_acceptance.py:332-367) in deterministic mode: decomposed training twice
+    gives byte-identical brick models and manifests (timers masked), and identical renders."""
+    import json
+    monkeypatch.setenv("APMG_DETERMINISTIC", "1")
+    vol = PV.synth_volume((12, 12, 12), [PV.BlobSpec(center=(0.1, 0.2, -0.3), sigma=(0.3, 0.4, 0.3))])
+    header = PV.save_volume(vol, tmp_path / "v.raw")
+    runs = []
+    for tag in ("a", "b"):
+        plan = P.plan_partition(vol.dims, 2, 2, 2, ghost=1)
+        P.train_decomposed(tmp_path / "v.raw", header, plan, PM.ModelConfig(grids=2, channels=1, resolution=(4, 4, 4)),
+                           P.TrainConfig(iterations=40, batch_size=64, delay_start=10, seed=9), tmp_path / tag)
+        bricks = b"".join((tmp_path / tag / f"brick_{i:04d}.apmg").read_bytes() for i in range(8))
+        man = json.loads((tmp_path / tag / "manifest.json").read_text())
+        for b in man["bricks"]:
+            b["train_seconds"] = 0.0
+        field = P.DecomposedField.load(tmp_path / tag / "manifest.json")
+        img = PR.render_frame(field, PR.Camera(eye=(0.3, 0.2, 2.8), look_at=(0, 0, 0), width=10, height=8),
+                              PR.TransferFunction(), PR.RenderConfig(samples_per_ray=12))
+        runs.append((bricks, json.dumps(man, sort_keys=True), img.tobytes()))
+    assert runs[0] == runs[1]
+
+
+def test_ghost_seam_criterion_9(tmp_path):
+    """Criterion 9 (test_acceptance.py:299-329): rendering a decomposed field across the brick
+    boundary, ghost 4 shows a smaller seam than ghost 0."""
+    ramp = np.linspace(0, 1, 64, dtype=np.float32)[None, None, :]
+    base = PV.synth_volume((64, 64, 64), [PV.BlobSpec(center=(0, 0, 0), sigma=(0.55, 0.5, 0.6), amplitude=0.6)])
+    vol = PV.Volume(dims=(64, 64, 64), data=base.host_data() + ramp)
+    header = PV.save_volume(vol, tmp_path / "g.raw")
+    mcfg = PM.ModelConfig(grids=4, channels=1, resolution=(6, 6, 6))
+    tcfg = P.TrainConfig(iterations=800, batch_size=1024, delay_start=200, seed=5, plateau_enabled=False)
+    cam = PR.Camera(eye=(0, 0, 3.0), look_at=(0, 0, 0), fov_deg=45, width=64, height=64)
+    tf = PR.TransferFunction(opacity_points=[(0.0, 0.05), (1.0, 0.9)])
+    seam = {}
+    for ghost in (0, 4):
+        plan = P.plan_partition(header.dims, 2, 1, 1, ghost=ghost)
+        out = tmp_path / f"ghost{ghost}"
+        P.train_decomposed(tmp_path / "g.raw", header, plan, mcfg, tcfg, out, workers=2)
+        img = PR.render_frame(P.DecomposedField.load(out / "manifest.json"), cam, tf,
+                              PR.RenderConfig(samples_per_ray=64))
+        cols = img[:, cam.width // 2 - 3: cam.width // 2 + 3, :3]
+        seam[ghost] = float(np.abs(np.diff(cols, axis=1)).max())
+    assert seam[4] < seam[0], seam
