@@ -414,3 +414,27 @@ def gen_train_c1_ensemble():
            "psnr_perturbed": [_c1_run(200, 50, p)[0] for p in (1, 2, 3, 4)],
            "c60": {"iterations": 60, "delay_start": 40, "psnr": [_c1_run(60, 40, p)[0] for p in (0, 1, 2, 3)]}}
     (OUT / "train_c1_ensemble.json").write_text(json.dumps(out, indent=1))
+
+
+def gen_crit5_ensemble():
+    """Acceptance criterion 5's configuration (8 grids 8^3 x1, 5000 iterations, batch 2048) run by
+    the reference: the adaptive PSNR unperturbed and under four one-ulp perturbations of the initial
+    grids, plus the frozen-transform PSNR of seeds 0-2 (~90 s per run on 2 cores).  Written to
+    crit5_ensemble.json (the committed numbers came from this function)."""
+    import json
+    vol = rvol.synth_volume((64, 64, 64), adaptivity_blobs())
+
+    def run(seed, adaptive, pert=0):
+        m = rmodel.init_model(rmodel.ModelConfig(grids=8, channels=1, resolution=(8, 8, 8)), seed=seed,
+                              vmin=vol.vmin, vmax=vol.vmax)
+        if pert:
+            rng = np.random.default_rng(pert)
+            mask = rng.uniform(size=m.grids.shape) < 0.5
+            m.grids[mask] = np.nextafter(m.grids[mask], np.float32(np.inf if pert % 2 else -np.inf))
+        m, _ = rtrain.train_single(m, vol, rtrain.TrainConfig(iterations=5000, batch_size=2048, seed=seed,
+                                                              train_transforms=adaptive, plateau_enabled=False))
+        return rtrain.psnr(m, vol)
+    out = {"adaptive_psnr_unperturbed": run(0, True), "adaptive_psnr_perturbed": [run(0, True, p) for p in (1, 2, 3, 4)],
+           "frozen_psnr_unperturbed": run(0, False),
+           "criterion_5_reference_gaps_seeds_0_1_2": [run(s, True) - run(s, False) for s in (0, 1, 2)]}
+    (OUT / "crit5_ensemble.json").write_text(json.dumps(out, indent=1))

