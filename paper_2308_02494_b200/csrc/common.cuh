@@ -31,6 +31,9 @@ int num_sms();
 void* pool_alloc(size_t bytes);
 void pool_free(void* p, size_t bytes);
 void release_pool();
+// stream-ordered scratch (runtime.cu)
+void* stream_alloc(size_t bytes, cudaStream_t st);
+void stream_free(void* p, cudaStream_t st);
 
 #define APMG_CUDA_TRY(expr)                                                                  \
   do {                                                                                       \

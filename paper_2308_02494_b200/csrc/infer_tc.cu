@@ -372,31 +372,25 @@ bool infer_tc_eligible(const FwdArgs<float>& a) {
 }
 
 int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
-  static float* tab = nullptr;  // per-axis coordinate tables (grown on demand, never freed)
-  static int64_t tab_cap = 0;
+  // per-call scratch, stream-ordered: per-axis coordinate tables (lattice sweeps), the x-pair
+  // grid copy (point lists), the per-CTA SSE partials
+  float* tab = nullptr;
   if (a.mode == kFwdLattice) {
     const int64_t need = int64_t(a.bw) + a.bh + ceil_div(a.n, int64_t(a.bw) * a.bh);
-    if (need > tab_cap) {
-      if (tab) APMG_CUDA_TRY(cudaFree(tab));
-      APMG_CUDA_TRY(cudaMalloc(&tab, sizeof(float) * need));
-      tab_cap = need;
-    }
+    tab = static_cast<float*>(stream_alloc(sizeof(float) * need, st));
+    APMG_ARG_CHECK(tab != nullptr, "out of device memory for the sweep tables");
     APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   }
   // x-pair copy of the grid (ModelDev::gridx): 4 float4 corner loads per (point, grid) for
   // point lists (renderer samples: 19.1 vs 21.6 ms per 512^2 x 128 frame); lattice sweeps hit
   // L1 for most corners already and measured 2% slower with it, so they read the grid itself
-  static float4* gx = nullptr;
-  static int64_t gx_cap = 0;
   const int64_t cells = int64_t(a.md.M) * a.md.D * a.md.H * a.md.W;
   const char* eg = getenv("APMG_GRIDX");
   const bool use_gx = a.mode != kFwdLattice && !(eg && eg[0] == '0');
+  float4* gx = nullptr;
   if (use_gx) {
-    if (cells > gx_cap) {
-      if (gx) APMG_CUDA_TRY(cudaFree(gx));
-      APMG_CUDA_TRY(cudaMalloc(&gx, sizeof(float4) * cells));
-      gx_cap = cells;
-    }
+    gx = static_cast<float4*>(stream_alloc(sizeof(float4) * cells, st));
+    APMG_ARG_CHECK(gx != nullptr, "out of device memory for the x-pair grid copy");
     APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(cells, 8), 256, 0, st,
                 reinterpret_cast<const float2*>(a.md.grid), gx, cells);
   }
@@ -411,17 +405,22 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const char* es = getenv("APMG_INFER_STAMPS");
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
-  b.md.gridx = use_gx ? gx : nullptr;
-  if (a.mode == kFwdLattice && a.truth) {
-    b.sse_part = sse_parts(grid);
+  b.md.gridx = gx;
+  const bool sse = a.mode == kFwdLattice && a.truth;
+  if (sse) {
+    b.sse_part = static_cast<double*>(stream_alloc(sizeof(double) * grid, st));
     APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
   }
   if (a.mode != kFwdLattice)
     APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   else
     APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
-  if (a.mode == kFwdLattice && a.truth) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
-  return APMG_OK;
+  int rc = APMG_OK;
+  if (sse) rc = launch_sse_finalize(b.sse_part, grid, a.sse, st);
+  stream_free(b.sse_part, st);
+  stream_free(gx, st);
+  stream_free(tab, st);
+  return rc;
 }
 
 }  // namespace apmg

@@ -42,8 +42,7 @@ bool recon_tc_eligible(const ModelDev<float>& md);
 bool recon_uses_tc16(const apmg_model& m);
 // grid for grid-stride elementwise kernels: enough 256-thread blocks for n, at most per_sm per SM
 int elementwise_grid(int64_t n, int per_sm);
-// per-CTA SSE partials of the lattice sweeps and their fixed-order sum into *sse (model_kernels.cu)
-double* sse_parts(int n);
+// fixed-order sum of the per-CTA SSE partials of a lattice sweep into *sse (model_kernels.cu)
 int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st);
 // gridx[c] = (grid[c], grid[c + 1]) over the flat two-channel cells (misc_kernels.cu)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);

@@ -104,22 +104,6 @@ __global__ void k_sse_finalize(const double* __restrict__ part, int n, double* _
   if (threadIdx.x == 0) *sse += s;
 }
 
-// per-CTA SSE partials of the lattice sweeps (grown on demand, never freed; one stream order)
-double* sse_parts(int n) {
-  static double* buf = nullptr;
-  static int cap = 0;
-  if (n > cap) {
-    if (buf) cudaFree(buf);
-    if (cudaMalloc(&buf, sizeof(double) * n) != cudaSuccess) {
-      buf = nullptr;
-      cap = 0;
-      return nullptr;
-    }
-    cap = n;
-  }
-  return buf;
-}
-
 int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st) {
   APMG_LAUNCH("sse_finalize", k_sse_finalize, 1, 32, 0, st, part, n, sse);
   return APMG_OK;
@@ -144,13 +128,16 @@ int launch_forward(const FwdArgs<T>& a, cudaStream_t st) {
   const int64_t tiles = ceil_div(a.n, kTileP);
   const int grid = int(min64(tiles, int64_t(num_sms()) * occ));
   FwdArgs<T> b = a;
-  if (a.mode == kFwdLattice && a.truth) {
-    b.sse_part = sse_parts(grid);
+  const bool sse = a.mode == kFwdLattice && a.truth;
+  if (sse) {
+    b.sse_part = static_cast<double*>(stream_alloc(sizeof(double) * grid, st));
     APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
   }
   APMG_LAUNCH("forward", k_forward<T>, grid, kTileThreads, smem, st, b);
-  if (a.mode == kFwdLattice && a.truth) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
-  return APMG_OK;
+  int rc = APMG_OK;
+  if (sse) rc = launch_sse_finalize(b.sse_part, grid, a.sse, st);
+  stream_free(b.sse_part, st);
+  return rc;
 }
 
 // ------------------------------------------------------------------ recon fwd+bwd

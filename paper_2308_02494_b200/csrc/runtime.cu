@@ -119,6 +119,32 @@ void release_pool() {
   g_pool.clear();
 }
 
+// Stream-ordered scratch for per-call temporaries (sweep tables, x-pair copies, SSE partials):
+// allocation and release are ordered on the caller's stream, so concurrent calls on different
+// streams never share a buffer.  The device's default pool keeps its memory between calls.
+void* stream_alloc(size_t bytes, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void stream_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 }  // namespace apmg
 
 using namespace apmg;
