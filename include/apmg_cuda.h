@@ -223,7 +223,9 @@ typedef struct apmg_train_config {
    * test_acceptance.py:332-367): batch order within each spatial bucket restored by a stable
    * pass, grid gradient accumulated in 64-bit fixed point (2^-44) with integer REDs.  0: float
    * REDs in arrival order (faster; sums differ in the last bits between runs). */
-  int32_t deterministic, reserved;
+  int32_t deterministic;
+  int32_t reserved; /* bit 0: plain launches, no CUDA graph (sessions driven concurrently from
+                     * several host threads: a capture must not overlap other threads' CUDA calls) */
 } apmg_train_config;
 
 typedef struct apmg_train_state apmg_train_state;

@@ -187,6 +187,7 @@ def ptr(t) -> C.c_void_p:
 _STAGE_BYTES = int(os.environ.get("APMG_STAGE_MB", "16")) << 20
 _STAGE_SLOTS = int(os.environ.get("APMG_STAGE_SLOTS", "8"))
 _stage = None
+_stage_lock = __import__("threading").Lock()  # one transfer through the ring at a time (worker threads)
 
 
 def _staging():
@@ -200,7 +201,7 @@ def _staging():
     return _stage
 
 
-def _upload_staged(a: np.ndarray, out) -> None:
+def __upload_staged_locked(a: np.ndarray, out) -> None:
     """Pageable host array -> device tensor through the pinned ring: host threads fill the
     slots (numpy copies release the GIL) while the copy engine drains the filled ones, so
     the host memcpy and the PCIe / C2C transfer overlap instead of running back to back
@@ -247,7 +248,7 @@ def _leading_chunks(shape, itemsize, cap):
     return [(i,) + rest for i in range(shape[0]) for rest in _leading_chunks(shape[1:], itemsize, cap)]
 
 
-def upload_view(view: np.ndarray, out) -> None:
+def _upload_view_locked(view: np.ndarray, out) -> None:
     """Any (strided, memory-mapped) float32 array view -> contiguous device tensor `out`, piece by
     piece through the pinned ring: host threads gather each C-order piece of the view (page-cache /
     disk reads of a memmap included) into a staging slot while the copy engine drains the
@@ -316,7 +317,7 @@ def workspace(nbytes: int):
     return empty((max(int(nbytes), 1),), np.uint8)
 
 
-def download_into(dev, out: np.ndarray) -> None:
+def _download_into_locked(dev, out: np.ndarray) -> None:
     """Contiguous device tensor -> existing contiguous host array of the same byte size,
     through the pinned ring: the copy engine fills slot i+1 while host threads drain slot i."""
     t = torch()
@@ -377,3 +378,18 @@ def exported_symbols() -> list[str]:
 
 def env_flag(name: str) -> bool:
     return os.environ.get(name, "") not in ("", "0", "false", "False")
+
+
+def _upload_staged(*args, **kw):
+    with _stage_lock:
+        return __upload_staged_locked(*args, **kw)
+
+
+def download_into(*args, **kw):
+    with _stage_lock:
+        return _download_into_locked(*args, **kw)
+
+
+def upload_view(*args, **kw):
+    with _stage_lock:
+        return _upload_view_locked(*args, **kw)

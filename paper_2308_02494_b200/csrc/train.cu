@@ -413,7 +413,7 @@ extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
     APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(s->gx_cells, 8), 256, 0, st,
                 reinterpret_cast<const float2*>(static_cast<float*>(s->main_params) + s->off[0]), s->gridx,
                 s->gx_cells);
-  if (graphs_enabled() && n >= kGraphIters) {
+  if (graphs_enabled() && !(s->cfg.reserved & 1) && n >= kGraphIters) {
     if (!s->graph) {
       int rc = run_direct(s, st);  // first iteration direct: one-time launch attributes set outside capture
       if (rc) return rc;

@@ -151,6 +151,11 @@ def _bias_table(n: int) -> np.ndarray:
     return tab
 
 
+# per-thread flag: sessions run from concurrent worker threads (train_decomposed workers > 1)
+# use plain launches -- a CUDA-graph capture must not overlap other threads' CUDA calls
+_concurrency = __import__("threading").local()
+
+
 class TrainSession:
     """Owns the device copy of one model during training (main group in one flat
     buffer laid out by ``apmg_main_layout``) and the native loop state."""
@@ -184,7 +189,8 @@ class TrainSession:
             cfg.transform_ma_window, cfg.transform_improve_threshold, cfg.hard_stop_iteration,
             cfg.plateau_window, cfg.plateau_threshold, cfg.plateau_factor, cfg.plateau_max_triggers,
             int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)),
-            int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"), 0)
+            int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"),
+            1 if getattr(_concurrency, "no_graph", False) else 0)
         self.ws = L.workspace(L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg)))
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()
