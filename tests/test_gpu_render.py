@@ -302,3 +302,21 @@ def test_concurrent_bricks_match_sequential(tmp_path, monkeypatch):
         out[workers] = b"".join((tmp_path / f"w{workers}" / f"brick_{i:04d}.apmg").read_bytes() for i in range(8))
     assert out[1] == out[4]
     print(f"8 bricks x 300 iterations: workers=1 {dt[1]:.2f} s, workers=4 {dt[4]:.2f} s")
+
+
+def test_rank_local_decomposed_field(tmp_path):
+    """A rank-local DecomposedField (bricks of other ranks are None) evaluates the points of its
+    own bricks exactly like the full field -- the owner side of forward_distributed."""
+    import torch
+    vol = PV.synth_volume((20, 18, 16), [PV.BlobSpec(center=(0.1, -0.2, 0.3), sigma=(0.4, 0.3, 0.5))])
+    header = PV.save_volume(vol, tmp_path / "v.raw")
+    plan = P.plan_partition(vol.dims, 2, 2, 1, ghost=1)
+    P.train_decomposed(tmp_path / "v.raw", header, plan, PM.ModelConfig(grids=4, channels=2, resolution=(4, 4, 4)),
+                       P.TrainConfig(iterations=8, batch_size=512, delay_start=2, seed=0), tmp_path / "out")
+    full = P.DecomposedField.load(tmp_path / "out" / "manifest.json")
+    local = P.DecomposedField(full.manifest, [m if b % 2 == 0 else None for b, m in enumerate(full.models)])
+    pts = np.random.default_rng(0).uniform(-1, 1, (4000, 3)).astype(np.float32)
+    own = P.spatial_hash(pts, 2, 2, 1) % 2 == 0
+    p = torch.from_numpy(pts[own]).cuda()
+    assert torch.equal(local.forward_dev(p), full.forward_dev(p))
+    assert torch.equal(local.forward_distributed(p), full.forward_dev(p))  # world 1: local
