@@ -241,3 +241,55 @@ def test_route_queries_gloo_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok and seen for _, ok, seen in res), res
+
+
+def _gather_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dims = (9, 7, 5)
+        cuts = ([0, 4, 8], [0, 3, 6], [0, 4])  # 2 x 2 x 1 bricks: inclusive boxes
+        boxes = []
+        for j in range(2):
+            for i in range(2):
+                x0, x1 = (0, 4) if i == 0 else (5, 8)
+                y0, y1 = (0, 3) if j == 0 else (4, 6)
+                boxes.append((x0, x1, y0, y1, 0, 4))
+        local = {}
+        for b, (x0, x1, y0, y1, z0, z1) in enumerate(boxes):
+            if b % world == rank:
+                zz, yy, xx = np.meshgrid(np.arange(z0, z1 + 1), np.arange(y0, y1 + 1), np.arange(x0, x1 + 1),
+                                         indexing="ij")
+                local[b] = torch.from_numpy((xx + 10 * yy + 100 * zz + 1000 * b).astype(np.float32))
+        full = D.gather_boxes(local, boxes, dims, world)
+        ok = True
+        if rank == 0:
+            zz, yy, xx = np.meshgrid(np.arange(5), np.arange(7), np.arange(9), indexing="ij")
+            owner = (xx >= 5).astype(int) + 2 * (yy >= 4).astype(int)
+            ok = bool(np.array_equal(full.numpy(), (xx + 10 * yy + 100 * zz + 1000 * owner).astype(np.float32)))
+        else:
+            ok = full is None
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_boxes_gloo_world2():
+    """Reconstructed-volume gather: boxes owned by two ranks land in one volume on rank 0."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res
