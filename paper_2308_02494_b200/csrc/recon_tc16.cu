@@ -43,10 +43,10 @@ constexpr uint32_t OFF_W1 = 0;                          // [64 i][128 k] x3
 constexpr uint32_t OFF_W2 = OFF_W1 + 3 * PL64x128;      // [64 j][64 i] x3
 constexpr uint32_t OFF_F = OFF_W2 + 3 * PL64x64;        // [64 p][128 k] x3
 constexpr uint32_t OFF_H1 = OFF_F + 3 * PL64x128;       // [64 p][64 i] x3
-constexpr uint32_t OFF_DZ2 = OFF_H1 + 3 * PL64x64;      // [64 p][64 j] x3
-constexpr uint32_t OFF_DZ1 = OFF_DZ2 + 3 * PL64x64;     // [64 p][64 i] x3
-constexpr uint32_t OFF_GF = OFF_H1;                     // f32 [64][128] (32 KB) over h1 | dz2
-constexpr uint32_t OFF_X = OFF_DZ1 + 3 * PL64x64;       // [2][P][3]
+constexpr uint32_t OFF_DZ2 = OFF_H1 + 3 * PL64x64;      // [64 p][64 j] x2 (the backward products use h, m)
+constexpr uint32_t OFF_DZ1 = OFF_DZ2 + 2 * PL64x64;     // [64 p][64 i] x2
+constexpr uint32_t OFF_GF = OFF_DZ1 + 2 * PL64x64;      // f32 [64][128]: lives until the next tile's gF
+constexpr uint32_t OFF_X = OFF_GF + P * FE * 4;         // [2][P][3]
 constexpr uint32_t OFF_T = OFF_X + 2 * P * 3 * 4;       // [2][P]
 constexpr uint32_t OFF_G = OFF_T + 2 * P * 4;           // [P]
 constexpr uint32_t OFF_HEAD = OFF_G + P * 4;            // [WQ][P]
@@ -59,10 +59,39 @@ constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
 constexpr uint32_t OFF_M1 = OFF_W3 + 64 * 4;            // (spare)
 constexpr uint32_t SMEM_BYTES = OFF_M1 + 64 * 4 * 2;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-static_assert(P * FE * 4 <= 6 * PL64x64, "gF buffer fits over h1 | dz2");
 
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t TC_A = 0, TC_B = 64, TC_DW1 = 128, TC_DW2 = 256, TC_CACHE = 320;
+// cell cache: 3 words per (grid, point) pair (base vertex, three 21-bit fractions), 12 columns per
+// encode group, two groups per warp, four warps per lane quarter = 96 columns per tile; two tiles
+// (parity) so the scatter of tile t can run after the encode of tile t+1
+constexpr uint32_t CACHE_TILE = 96;
+static_assert(TC_CACHE + 2 * CACHE_TILE <= TMEM_COLS, "tensor memory budget");
+
+// where the scatter of tile t runs: SQ_I pairs interleaved with the encode of tile t+1, SQ_C in the
+// z2 wait and SQ_E in the dz1 || dW2 wait of tile t+1, the rest in its gF || dW1 wait
+#ifndef TC16_SQ_I
+#define TC16_SQ_I 4
+#define TC16_SQ_C 1
+#define TC16_SQ_E 1
+#endif
+constexpr int SQ_I = TC16_SQ_I, SQ_C = TC16_SQ_C, SQ_E = TC16_SQ_E, SQ = 8;
+
+// fractions in [0, 1] as 21-bit fixed point (resolution 2^-21; the scatter weights only)
+__device__ __forceinline__ void pack_cell(int vbase, float fx, float fy, float fz, uint32_t* w) {
+  const uint32_t qx = min(__float2uint_rn(fx * 2097152.f), 2097151u);
+  const uint32_t qy = min(__float2uint_rn(fy * 2097152.f), 2097151u);
+  const uint32_t qz = min(__float2uint_rn(fz * 2097152.f), 2097151u);
+  w[0] = uint32_t(vbase);
+  w[1] = qx | (qy << 21);
+  w[2] = (qy >> 11) | (qz << 10);
+}
+__device__ __forceinline__ void unpack_cell(const uint32_t* w, int& vbase, float& fx, float& fy, float& fz) {
+  vbase = int(w[0]);
+  fx = float(w[1] & 0x1FFFFFu) * 4.76837158203125e-07f;
+  fy = float((w[1] >> 21) | ((w[2] & 0x3FFu) << 11)) * 4.76837158203125e-07f;
+  fz = float((w[2] >> 10) & 0x1FFFFFu) * 4.76837158203125e-07f;
+}
 
 // bf16x3 product q: (A plane, B plane) = hh, hm, mh, hl, lh, mm
 __host__ __device__ constexpr int kPA(int q) { return q == 2 ? 1 : (q == 4 ? 2 : (q == 5 ? 1 : 0)); }
@@ -106,30 +135,35 @@ __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX
   }
 }
 
-// scatter of one (2 grids x 2 points) group (see recon_tc.cu)
+// scatter of pairs [q0, q1) (q = 4 jq + u: grid 2 warp + 32 jq + u / 2, point lane + 32 (u % 2),
+// encode_group's order) of a tile whose cell cache starts at tmem_cache
 template <bool FX>
-__device__ __forceinline__ void scatter_group(const ModelDev<float>& md, const Args& a, const float* GF,
-                                              uint32_t tmem_cache, int jq, int cnt, int warp, int lane) {
+__device__ __forceinline__ void scatter_pairs(const ModelDev<float>& md, const Args& a, const float* GF,
+                                              uint32_t tmem_cache, int q0, int q1, int cnt, int warp, int lane) {
   if (a.skip & 1) return;
-  uint32_t cache[16];
-  umma::tmem_ld16u(tmem_cache + 16 * jq, cache);
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int h = u & 1;
-    const int m = 2 * warp + 32 * jq + (u >> 1), p = lane + 32 * h;  // encode_group's pair order
-    const int vbase = int(cache[4 * u]);
-    const bool valid = vbase >= 0 && p < cnt;
-    float2 g = make_float2(0.f, 0.f);
-    if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
-    if (a.aggregate == 2)
-      scatter_vertex_warp_gather<FX>(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
-                                 __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-    else if (a.aggregate)
-      scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, __uint_as_float(cache[4 * u + 1]),
-                              __uint_as_float(cache[4 * u + 2]), __uint_as_float(cache[4 * u + 3]), g.x, g.y);
-    else if (valid)
-      scatter_vertex_f32(md, a.dgrid, vbase, __uint_as_float(cache[4 * u + 1]), __uint_as_float(cache[4 * u + 2]),
-                         __uint_as_float(cache[4 * u + 3]), g.x, g.y);
+  for (int jq = 0; jq < 2; ++jq) {
+    if (q1 <= 4 * jq || q0 >= 4 * jq + 4) continue;  // warp-uniform
+    uint32_t cache[12];
+    umma::tmem_ld12u(tmem_cache + 12 * jq, cache);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = 4 * jq + u;
+      if (q < q0 || q >= q1) continue;
+      const int m = 2 * warp + 32 * jq + (u >> 1), p = lane + 32 * (u & 1);
+      int vbase;
+      float fx, fy, fz;
+      unpack_cell(cache + 3 * u, vbase, fx, fy, fz);
+      const bool valid = vbase >= 0 && p < cnt;
+      float2 g = make_float2(0.f, 0.f);
+      if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
+      if (a.aggregate == 2)
+        scatter_vertex_warp_gather<FX>(md, a.dgrid, valid, vbase, fx, fy, fz, g.x, g.y);
+      else if (a.aggregate)
+        scatter_vertex_warp_agg(md, a.dgrid, valid, vbase, fx, fy, fz, g.x, g.y);
+      else if (valid)
+        scatter_vertex_f32(md, a.dgrid, vbase, fx, fy, fz, g.x, g.y);
+    }
   }
 }
 
@@ -183,7 +217,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   const uint32_t tmem = *tm_slot;
   const uint32_t lane_base = uint32_t(32 * quarter) << 16;
   const uint32_t TA = tmem + TC_A, TB = tmem + TC_B, TDW1 = tmem + TC_DW1, TDW2 = tmem + TC_DW2;
-  const uint32_t tmem_cache = tmem + TC_CACHE + 8 * GPW * wq + lane_base;
+  // cell cache of tile parity b: tmem_cache0 + b * CACHE_TILE (+ 12 per encode group)
+  const uint32_t tmem_cache0 = tmem + TC_CACHE + 24 * wq + lane_base;
   // zero the TMEM-resident weight-gradient sums (warps 0-3 cover the four lane quarters)
   if (warp < 4) {
     uint32_t z[16];
@@ -219,11 +254,11 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   // encode of grids 2 warp + 32 jq + {0, 1} for points lane, lane + 32: the two points of a grid
   // share its transform and run in packed fp32x2 arithmetic; the two grids' four features of a
   // point are adjacent in F (one 8-byte store per plane)
-  auto encode_group = [&](const float* cX, int jq) {
+  auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache) {
     const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
     const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
     const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
-    uint32_t cache[16];
+    uint32_t cache[12];
     uint32_t fw[2][2][3];  // [grid jj][point h][plane]
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
@@ -250,10 +285,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
           else
             interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx[h], fy[h], fz[h], f0, f1);
         }
-        cache[4 * u] = uint32_t(vbase);
-        cache[4 * u + 1] = __float_as_uint(fx[h]);
-        cache[4 * u + 2] = __float_as_uint(fy[h]);
-        cache[4 * u + 3] = __float_as_uint(fz[h]);
+        pack_cell(vbase, fx[h], fy[h], fz[h], cache + 3 * u);
         umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
       }
     }
@@ -264,7 +296,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       for (int pl = 0; pl < 3; ++pl)
         *reinterpret_cast<uint2*>(F + pl * PL64x128 + o) = make_uint2(fw[0][h][pl], fw[1][h][pl]);
     }
-    umma::tmem_st16(tmem_cache + 16 * jq, cache);
+    umma::tmem_st8(tmem_cache + 12 * jq, cache);
+    umma::tmem_st4(tmem_cache + 12 * jq + 8, cache + 8);
   };
   // z1 = F W1^T over K-steps [k0, k1) (K = 16 each), committed when `last`
   auto issue_z1 = [&](int k0, int k1, bool last) {
@@ -277,11 +310,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
                          umma::kmajor_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kk, (kk | q) ? 1u : 0u);
     if (last) umma::commit(bar);
   };
-  auto encode_tile = [&](const float* cX, int scatter_cnt, int64_t prefetch_tile, int prefetch_slot) {
+  // encode of a tile into cache buffer `cache_enc`, with pairs [0, SQ_I) of the previous tile's
+  // scatter (cache buffer `cache_sc`, scatter_cnt points; < 0: none) interleaved group by group
+  auto encode_tile = [&](const float* cX, uint32_t cache_enc, uint32_t cache_sc, int scatter_cnt,
+                         int64_t prefetch_tile, int prefetch_slot) {
 #pragma unroll 1
     for (int jq = 0; jq < GPW / 2; ++jq) {
-      if (scatter_cnt >= 0) scatter_group<FX>(md, a, GF, tmem_cache, jq, scatter_cnt, warp, lane);
-      encode_group(cX, jq);
+      if (scatter_cnt >= 0)
+        scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
+      encode_group(cX, jq, cache_enc);
       if (jq == 0) {  // features k < 64 (grids 0-31) complete: first half of z1
         umma::fence_async_smem();
         __syncthreads();
@@ -298,10 +335,12 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   };
 
   int it = 0;
-  if (int64_t(blockIdx.x) < tiles) encode_tile(sX, -1, int64_t(blockIdx.x) + gridDim.x, 1);
+  if (int64_t(blockIdx.x) < tiles) encode_tile(sX, tmem_cache0, tmem_cache0, -1, int64_t(blockIdx.x) + gridDim.x, 1);
+  int cnt_prev = -1;  // the previous tile's scatter pairs [SQ_I, SQ) run in this tile's tensor-core waits
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
     const int cnt = int(min64(P, a.n - tile * P));
     const float* cT = sT + (it & 1) * P;
+    const uint32_t cache_cur = tmem_cache0 + (it & 1) * CACHE_TILE, cache_prev = tmem_cache0 + ((it + 1) & 1) * CACHE_TILE;
     TC16_STAMP(0);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
@@ -337,6 +376,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
                            umma::kmajor_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
       umma::commit(bar);
     }
+    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I, SQ_I + SQ_C, cnt_prev, warp, lane);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -396,8 +436,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
           d0[j] = a0 > 0.f ? __fmul_rn(g0, w) : 0.f;  // g_z2 (optim.py:143-145)
           d1[j] = a1 > 0.f ? __fmul_rn(g1, w) : 0.f;
         }
-        umma::store_pair3(DZ2, PL64x64, p0, ep_col0 + 8 * r + ec, 64, d0[0], d0[1]);
-        umma::store_pair3(DZ2, PL64x64, p1, ep_col0 + 8 * r + ec, 64, d1[0], d1[1]);
+        umma::store_pair2(DZ2, PL64x64, p0, ep_col0 + 8 * r + ec, 64, d0[0], d0[1]);
+        umma::store_pair2(DZ2, PL64x64, p1, ep_col0 + 8 * r + ec, 64, d1[0], d1[1]);
       }
     }
     umma::fence_async_smem();
@@ -419,6 +459,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
                            umma::mnmajor16_c(OFF_H1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
       umma::commit(bar);
     }
+    if (cnt_prev >= 0)
+      scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I + SQ_C, SQ_I + SQ_C + SQ_E, cnt_prev, warp, lane);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -432,8 +474,8 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
         if (!((h1pos >> e) & 1u)) v[e] = 0.f;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        umma::store_pair3(DZ1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
-        umma::store_pair3(DZ1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
+        umma::store_pair2(DZ1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
+        umma::store_pair2(DZ1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
       }
     }
     umma::fence_async_smem();
@@ -455,11 +497,12 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
                            umma::mnmajor16_c(OFF_F + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
       umma::commit(bar);
     }
+    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I + SQ_C + SQ_E, SQ, cnt_prev, warp, lane);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
     umma::fence_before_sync();
-    __syncthreads();  // h1 / dz2 consumed (dW2, dz1 done) before gF overwrites them
+    __syncthreads();  // every warp's scatter of the previous tile has read gF before it is overwritten
     umma::fence_after_sync();
     TC16_STAMP(7);
     // ---- gF epilogue: 32 columns per warp -> gF[p][k] ----
@@ -476,13 +519,14 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_before_sync();
     __syncthreads();
     TC16_STAMP(8);
-    // ---- scatter of this tile, interleaved with the encode of the next one ----
+    // ---- encode of the next tile with the first SQ_I pairs of this tile's scatter interleaved;
+    // the rest of the scatter runs in the next tile's tensor-core waits ----
     const int64_t next = tile + gridDim.x;
     if (next < tiles) {
-      encode_tile(sX + ((it + 1) & 1) * 3 * P, cnt, next + gridDim.x, it + 2);
+      encode_tile(sX + ((it + 1) & 1) * 3 * P, cache_prev, cache_cur, cnt, next + gridDim.x, it + 2);
+      cnt_prev = cnt;
     } else {
-#pragma unroll 1
-      for (int jq = 0; jq < GPW / 2; ++jq) scatter_group<FX>(md, a, GF, tmem_cache, jq, cnt, warp, lane);
+      scatter_pairs<FX>(md, a, GF, cache_cur, 0, SQ, cnt, warp, lane);
     }
   }
 
