@@ -319,10 +319,16 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       if (scatter_cnt >= 0)
         scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
       encode_group(cX, jq, cache_enc);
-      if (jq == 0) {  // features k < 64 (grids 0-31) complete: first half of z1
+      if (jq == 0) {
+        // features k < 64 (grids 0-31) complete: first half of z1.  Only warp 0 (which issues)
+        // waits for the other warps; they signal the named barrier and carry on with group 1
         umma::fence_async_smem();
-        __syncthreads();
-        issue_z1(0, FE / 32, false);
+        if (warp == 0) {
+          umma::named_sync(1, NT);
+          issue_z1(0, FE / 32, false);
+        } else {
+          umma::named_arrive(1, NT);
+        }
       }
     }
     umma::tmem_st_wait();
