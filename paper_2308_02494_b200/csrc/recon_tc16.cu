@@ -370,7 +370,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
-    __syncthreads();
+    // only the issuing warp waits for the stores; the others go on to their share of the
+    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
+    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
     umma::fence_after_sync();
     TC16_STAMP(2);
     // ---- z2 = h1 W2^T ----
@@ -448,7 +450,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
-    __syncthreads();
+    // only the issuing warp waits for the stores; the others go on to their share of the
+    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
+    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
     umma::fence_after_sync();
     TC16_STAMP(4);
     // ---- dz1 = dz2 W2 (-> acc A), dW2 += dz2^T h1 (-> TMEM sum) ----
@@ -486,7 +490,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
-    __syncthreads();
+    // only the issuing warp waits for the stores; the others go on to their share of the
+    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
+    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
     umma::fence_after_sync();
     TC16_STAMP(6);
     // ---- gF = dz1 W1 (-> acc A|B, N=128), dW1 += dz1^T F (-> TMEM sum) ----
