@@ -71,7 +71,7 @@ static_assert(TC_CACHE + 2 * CACHE_TILE <= TMEM_COLS, "tensor memory budget");
 // where the scatter of tile t runs: SQ_I pairs interleaved with the encode of tile t+1, SQ_C in the
 // z2 wait and SQ_E in the dz1 || dW2 wait of tile t+1, the rest in its gF || dW1 wait
 #ifndef TC16_SQ_I
-#define TC16_SQ_I 4
+#define TC16_SQ_I 3
 #define TC16_SQ_C 1
 #define TC16_SQ_E 1
 #endif
