@@ -413,26 +413,30 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
         sHead[wq * P + p1] = part1;
       }
     }
-    umma::fence_before_sync();
-    __syncthreads();
-    if (tid < P) {
-      float g = 0.f;
-      if (tid < cnt) {
-        float raw = sHead[tid];
-#pragma unroll
-        for (int q = 1; q < WQ; ++q) raw += sHead[q * P + tid];
-        const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
-        const float r = __fsub_rn(y, cT[tid]);
-        const float s = __fmul_rn(r, r);
-        a.sq[tile * P + tid] = s;
-        loss += double(s);
-        g = __fmul_rn(r, coef);
-      }
-      sG[tid] = g;
-    }
-    __syncthreads();
+    // the four warps of this lane quarter (warps q, q+4, q+8, q+12) own rows 16q..16q+15: they
+    // exchange their partial heads among themselves (named barrier 2 + q), no CTA barrier
+    umma::named_sync(2 + quarter, 128);
     {
-      const float g0 = sG[p0], g1 = sG[p1];
+      float gg[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int pr = k ? p1 : p0;
+        gg[k] = 0.f;
+        if (pr < cnt) {
+          float raw = sHead[pr];
+#pragma unroll
+          for (int q = 1; q < WQ; ++q) raw += sHead[q * P + pr];
+          const float y = __fadd_rn(__fmul_rn(raw, md.span), md.vmin);
+          const float r = __fsub_rn(y, cT[pr]);
+          const float sqe = __fmul_rn(r, r);
+          if (wq == 0 && (lane & 3) == 0) {  // one writer per point
+            a.sq[tile * P + pr] = sqe;
+            loss += double(sqe);
+          }
+          gg[k] = __fmul_rn(r, coef);
+        }
+      }
+      const float g0 = gg[0], g1 = gg[1];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         float d0[2], d1[2];
