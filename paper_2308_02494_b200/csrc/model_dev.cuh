@@ -392,43 +392,23 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
   const int rank = __popc(peers & ((1u << lane) - 1u));
   const bool leader = valid && (rank % (APMG_GATHER_CAP + 1)) == 0;
   float2 v[8];
-#if APMG_GATHER_CAP == 1
-  // one member per leader: straight-line code (no vote loop), so the compiler can interleave the
-  // shuffles and corner terms of consecutive pairs; a leader without a member adds zeros
+  // members of a leader: the next CAP set bits of peers above it, fetched one per round in
+  // straight-line code (no vote loop), so the compiler can interleave the shuffles and corner
+  // terms of consecutive pairs; a round without a member adds zeros
   {
-    const unsigned above = peers & (0xfffffffeu << lane);
-    const bool has = leader && above != 0u;
-    const int src = has ? __ffs(above) - 1 : lane;
-    const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
-    const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
-                ez = __shfl_sync(0xffffffffu, fz, src);
-    corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
-    corner_terms(has ? make_float2(h0, h1) : make_float2(0.f, 0.f), ex, ey, ez, v, true);
-  }
-#else
-  // this leader's members: the next CAP set bits of peers above this lane
-  unsigned rest = 0u;
-  if (leader) {
     unsigned above = peers & (0xfffffffeu << lane);
+    corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
 #pragma unroll
     for (int k = 0; k < APMG_GATHER_CAP; ++k) {
-      rest |= above & (0u - above);  // lowest set bit
+      const bool has = leader && above != 0u;
+      const int src = has ? __ffs(above) - 1 : lane;
       above &= above - 1u;
+      const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
+      const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
+                  ez = __shfl_sync(0xffffffffu, fz, src);
+      corner_terms(has ? make_float2(h0, h1) : make_float2(0.f, 0.f), ex, ey, ez, v, true);
     }
   }
-  corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
-#pragma unroll 1
-  for (int k = 0; k < APMG_GATHER_CAP && __any_sync(0xffffffffu, rest != 0u); ++k) {
-    const int src = rest ? __ffs(rest) - 1 : lane;
-    const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
-    const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
-                ez = __shfl_sync(0xffffffffu, fz, src);
-    if (rest) {
-      corner_terms(make_float2(h0, h1), ex, ey, ez, v, true);
-      rest &= rest - 1u;
-    }
-  }
-#endif
   if (!leader) return;
   if constexpr (FX) {
     unsigned long long* base = md.dgrid_fx + (size_t(vbase) << 1);
