@@ -155,8 +155,8 @@ __device__ __forceinline__ void scatter_pairs(const ModelDev<float>& md, const A
       float fx, fy, fz;
       unpack_cell(cache + 3 * u, vbase, fx, fy, fz);
       const bool valid = vbase >= 0 && p < cnt;
-      float2 g = make_float2(0.f, 0.f);
-      if (valid) g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));
+      float2 g = *reinterpret_cast<const float2*>(GF + gf_idx(p, 2 * m));  // p < 64: always in the buffer
+      if (!valid) g = make_float2(0.f, 0.f);
       if (a.aggregate == 2)
         scatter_vertex_warp_gather<FX>(md, a.dgrid, valid, vbase, fx, fy, fz, g.x, g.y);
       else if (a.aggregate)
@@ -279,11 +279,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
         const bool inside = (fabsf(la[h][0]) <= 1.f) && (fabsf(la[h][1]) <= 1.f) && (fabsf(la[h][2]) <= 1.f);
         const int vbase = inside ? ((m * md.D + iz[h]) * md.H + iy[h]) * md.W + ix[h] : -1;
         float f0 = 0.f, f1 = 0.f;
-        if (inside && !(a.skip & 2)) {
+        {  // straight-line: outside pairs gather cell 0 and are zeroed afterwards
+          const bool use = inside && !(a.skip & 2);
+          const int vb = use ? vbase : 0;
           if (md.gridx)
-            interp_pairx_f32(md.gridx, md.W, md.H * md.W, vbase, fx[h], fy[h], fz[h], f0, f1);
+            interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
           else
-            interp_pair_f32(md.grid, md.W, md.H * md.W, vbase, fx[h], fy[h], fz[h], f0, f1);
+            interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
+          f0 = use ? f0 : 0.f;
+          f1 = use ? f1 : 0.f;
         }
         pack_cell(vbase, fx[h], fy[h], fz[h], cache + 3 * u);
         umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   // scatter (cache buffer `cache_sc`, scatter_cnt points; < 0: none) interleaved group by group
   auto encode_tile = [&](const float* cX, uint32_t cache_enc, uint32_t cache_sc, int scatter_cnt,
                          int64_t prefetch_tile, int prefetch_slot) {
-#pragma unroll 1
+#pragma unroll
     for (int jq = 0; jq < GPW / 2; ++jq) {
       if (scatter_cnt >= 0)
         scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
