@@ -300,16 +300,15 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
   #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const bool inside = (fabsf(la[k][0]) <= 1.f) && (fabsf(la[k][1]) <= 1.f) && (fabsf(la[k][2]) <= 1.f);
-              float f0 = 0.f, f1 = 0.f;
-              if (inside) {
-                const int vb = ((m * md.D + iz[k]) * md.H + iy[k]) * md.W + ix[k];
-                if (md.gridx)
-                  interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
-                else
-                  interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
-              }
-              fv[k][2 * g] = f0;
-              fv[k][2 * g + 1] = f1;
+              // straight-line: an outside pair gathers cell 0 and is zeroed afterwards
+              const int vb = inside ? ((m * md.D + iz[k]) * md.H + iy[k]) * md.W + ix[k] : 0;
+              float f0, f1;
+              if (md.gridx)
+                interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
+              else
+                interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
+              fv[k][2 * g] = inside ? f0 : 0.f;
+              fv[k][2 * g + 1] = inside ? f1 : 0.f;
             }
           }
           umma::store_chunk3(F, F_PLANE, pa, 8 * warp, P, fv[0]);

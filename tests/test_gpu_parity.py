@@ -639,12 +639,15 @@ def test_psnr_sweep_bit_reproducible():
 
 
 @pytest.mark.gpu
-def test_criterion_6_decomposition_trend(tmp_path):
+def test_criterion_6_decomposition_trend(tmp_path, monkeypatch):
     """test_acceptance.py:190-222 on the GPU path: a 2x2x2 decomposition with <= 1/8 of the
     parameters per brick stays within 0.5 dB (median over three seeds) of one model."""
     vol = PV.synth_volume((64, 64, 64), [PV.BlobSpec(center=(-0.5, -0.35, 0.3), sigma=(0.12, 0.1, 0.14)),
                                          PV.BlobSpec(center=(0.5, 0.4, -0.25), sigma=(0.1, 0.13, 0.11),
                                                      amplitude=0.8)])
+    # deterministic mode: the trend is then a fixed outcome of the seeds rather than a draw from
+    # the float-atomics run-to-run noise (which spreads these short runs by ~1 dB)
+    monkeypatch.setenv("APMG_DETERMINISTIC", "1")
     header = PV.save_volume(vol, tmp_path / "v.raw")
     single_cfg = PM.ModelConfig(grids=8, channels=2, resolution=(16, 16, 16))
     brick_cfg = PM.ModelConfig(grids=4, channels=1, resolution=(8, 8, 8))
@@ -659,6 +662,7 @@ def test_criterion_6_decomposition_trend(tmp_path):
         P.train_decomposed(tmp_path / "v.raw", header, P.plan_partition(header.dims, 2, 2, 2, ghost=1), brick_cfg, cfg,
                            out, workers=2)
         deltas.append(P.psnr(P.DecomposedField.load(out / "manifest.json"), vol) - p_single)
+    print("criterion 6 deltas (decomposed - single, dB):", [round(d, 3) for d in deltas])
     assert float(np.median(deltas)) >= -0.5, deltas
 
 

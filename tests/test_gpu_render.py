@@ -261,9 +261,11 @@ def test_decomposed_training_and_render_reproducible(tmp_path, monkeypatch):
     assert runs[0] == runs[1]
 
 
-def test_ghost_seam_criterion_9(tmp_path):
+def test_ghost_seam_criterion_9(tmp_path, monkeypatch):
     """Criterion 9 (test_acceptance.py:299-329): rendering a decomposed field across the brick
-    boundary, ghost 4 shows a smaller seam than ghost 0."""
+    boundary, ghost 4 shows a smaller seam than ghost 0 (deterministic mode: a fixed outcome of
+    the seeds, not a draw from the float-atomics run-to-run noise)."""
+    monkeypatch.setenv("APMG_DETERMINISTIC", "1")
     ramp = np.linspace(0, 1, 64, dtype=np.float32)[None, None, :]
     base = PV.synth_volume((64, 64, 64), [PV.BlobSpec(center=(0, 0, 0), sigma=(0.55, 0.5, 0.6), amplitude=0.6)])
     vol = PV.Volume(dims=(64, 64, 64), data=base.host_data() + ramp)
@@ -281,6 +283,7 @@ def test_ghost_seam_criterion_9(tmp_path):
                               PR.RenderConfig(samples_per_ray=64))
         cols = img[:, cam.width // 2 - 3: cam.width // 2 + 3, :3]
         seam[ghost] = float(np.abs(np.diff(cols, axis=1)).max())
+    print("criterion 9 seams:", seam)
     assert seam[4] < seam[0], seam
 
 
