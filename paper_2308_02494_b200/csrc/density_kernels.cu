@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_grad32c(const float* __re
 }
 
 // k_dens_grad32c with two staged points per lane and step (p = 10): float2 accumulators
-__global__ void __launch_bounds__(kDensThreads) k_dens_grad32cx2(const float* __restrict__ tf, int M,
+__global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float* __restrict__ tf, int M,
                                                                  const float* __restrict__ x, int64_t n,
                                                                  const float* __restrict__ drho, int ch,
                                                                  double* __restrict__ part, const TrainCtl* ctl) {
@@ -596,36 +596,52 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_grad32cx2(const float* __
       sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], drho[g]);
     }
     __syncthreads();
-    for (int m = warp; m < M; m += nw) {
-      float a[13];
+    // two grids per pass (m, m + nw): independent chains for the scheduler, one read of the points
+    for (int m = warp; m < M; m += 2 * nw) {
+      const int m2 = m + nw;
+      const bool two = m2 < M;
+      float a[2][13];
 #pragma unroll
-      for (int e = 0; e < 13; ++e) a[e] = s_tf[13 * m + e];
-      float2 acc[13];
+      for (int e = 0; e < 13; ++e) {
+        a[0][e] = s_tf[13 * m + e];
+        a[1][e] = two ? s_tf[13 * m2 + e] : 0.f;
+      }
+      float2 acc[2][13];
 #pragma unroll
-      for (int e = 0; e < 13; ++e) acc[e] = make_float2(0.f, 0.f);
-#pragma unroll 2
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int e = 0; e < 13; ++e) acc[k][e] = make_float2(0.f, 0.f);
       for (int i = lane; i < cnt; i += 64) {
         const float4 q0 = sP[i];
         const float4 q1 = i + 32 < cnt ? sP[i + 32] : make_float4(0.f, 0.f, 0.f, 0.f);  // d_rho 0: no share
         const float2 X0 = make_float2(q0.x, q1.x), X1 = make_float2(q0.y, q1.y), X2 = make_float2(q0.z, q1.z);
-        float2 b, l[3], lp[3];
-        bump32x2(a, X0, X1, X2, b, l, lp);
-        const float2 w = f2mul(make_float2(q0.w, q1.w), b);
-        const float2 sc = f2mul(bc2(a[12]), w);
-        acc[0] = __fadd2_rn(acc[0], w);
+        const float2 W = make_float2(q0.w, q1.w);
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const float2 sl = f2mul(sc, lp[d]);
-          acc[1 + 3 * d] = f2fma(sl, X0, acc[1 + 3 * d]);
-          acc[2 + 3 * d] = f2fma(sl, X1, acc[2 + 3 * d]);
-          acc[3 + 3 * d] = f2fma(sl, X2, acc[3 + 3 * d]);
-          acc[10 + d] = __fadd2_rn(acc[10 + d], sl);
+        for (int k = 0; k < 2; ++k) {
+          float2 b, l[3], lp[3];
+          bump32x2(a[k], X0, X1, X2, b, l, lp);
+          const float2 w = f2mul(W, b);
+          const float2 sc = f2mul(bc2(a[k][12]), w);
+          acc[k][0] = __fadd2_rn(acc[k][0], w);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const float2 sl = f2mul(sc, lp[d]);
+            acc[k][1 + 3 * d] = f2fma(sl, X0, acc[k][1 + 3 * d]);
+            acc[k][2 + 3 * d] = f2fma(sl, X1, acc[k][2 + 3 * d]);
+            acc[k][3 + 3 * d] = f2fma(sl, X2, acc[k][3 + 3 * d]);
+            acc[k][10 + d] = __fadd2_rn(acc[k][10 + d], sl);
+          }
         }
       }
 #pragma unroll
-      for (int e = 0; e < 13; ++e) {
-        const double v = warp_sum(double(acc[e].x) + double(acc[e].y));
-        if (lane == 0) s_acc[13 * m + e] += v;
+      for (int k = 0; k < 2; ++k) {
+        if (k == 1 && !two) break;
+        const int mk = k ? m2 : m;
+#pragma unroll
+        for (int e = 0; e < 13; ++e) {
+          const double v = warp_sum(double(acc[k][e].x) + double(acc[k][e].y));
+          if (lane == 0) s_acc[13 * mk + e] += v;
+        }
       }
     }
   }
