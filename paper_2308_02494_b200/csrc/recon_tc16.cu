@@ -48,16 +48,14 @@ constexpr uint32_t OFF_DZ1 = OFF_DZ2 + 2 * PL64x64;     // [64 p][64 i] x2
 constexpr uint32_t OFF_GF = OFF_DZ1 + 2 * PL64x64;      // f32 [64][128]: lives until the next tile's gF
 constexpr uint32_t OFF_X = OFF_GF + P * FE * 4;         // [2][P][3]
 constexpr uint32_t OFF_T = OFF_X + 2 * P * 3 * 4;       // [2][P]
-constexpr uint32_t OFF_G = OFF_T + 2 * P * 4;           // [P]
-constexpr uint32_t OFF_HEAD = OFF_G + P * 4;            // [WQ][P]
+constexpr uint32_t OFF_HEAD = OFF_T + 2 * P * 4;        // [WQ][P] partial heads per lane-quarter warp
 constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [4 quarters][64]: dW3 per lane quarter, summed in order
 constexpr uint32_t OFF_RED = OFF_DW3 + 4 * HID * 4;     // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
-constexpr uint32_t OFF_M1 = OFF_W3 + 64 * 4;            // (spare)
-constexpr uint32_t SMEM_BYTES = OFF_M1 + 64 * 4 * 2;
+constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 constexpr uint32_t TMEM_COLS = 512;
@@ -183,7 +181,6 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   float* GF = reinterpret_cast<float*>(sm + OFF_GF);
   float* sX = reinterpret_cast<float*>(sm + OFF_X);
   float* sT = reinterpret_cast<float*>(sm + OFF_T);
-  float* sG = reinterpret_cast<float*>(sm + OFF_G);
   float* sHead = reinterpret_cast<float*>(sm + OFF_HEAD);
   float* sDW3 = reinterpret_cast<float*>(sm + OFF_DW3);
   double* red = reinterpret_cast<double*>(sm + OFF_RED);
