@@ -315,6 +315,19 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   // scatter (cache buffer `cache_sc`, scatter_cnt points; < 0: none) interleaved group by group
   auto encode_tile = [&](const float* cX, uint32_t cache_enc, uint32_t cache_sc, int scatter_cnt,
                          int64_t prefetch_tile, int prefetch_slot) {
+    // the tile after next: its coordinates / targets are fetched now (registers) and stored to
+    // shared memory after the encode, so the global-load latency hides behind it
+    float pf[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool pf_on = prefetch_tile < tiles && tid < P;
+    if (pf_on) {
+      const int64_t i = prefetch_tile * P + tid;
+      if (i < a.n) {
+        pf[0] = __ldg(a.coords + 3 * i);
+        pf[1] = __ldg(a.coords + 3 * i + 1);
+        pf[2] = __ldg(a.coords + 3 * i + 2);
+        pf[3] = __ldg(a.targets + i);
+      }
+    }
 #pragma unroll
     for (int jq = 0; jq < GPW / 2; ++jq) {
       if (scatter_cnt >= 0)
@@ -333,8 +346,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       }
     }
     umma::tmem_st_wait();
-    if (prefetch_tile < tiles)
-      load_tile(a, prefetch_tile, sX + (prefetch_slot & 1) * 3 * P, sT + (prefetch_slot & 1) * P, tid);
+    if (pf_on) {
+      float* dX = sX + (prefetch_slot & 1) * 3 * P;
+      dX[3 * tid] = pf[0];
+      dX[3 * tid + 1] = pf[1];
+      dX[3 * tid + 2] = pf[2];
+      sT[(prefetch_slot & 1) * P + tid] = pf[3];
+    }
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();  // F complete; every warp's scatter of the previous tile has read gF
