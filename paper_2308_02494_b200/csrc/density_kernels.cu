@@ -669,7 +669,7 @@ size_t density_ws_bytes(int M, int64_t n) {
   Carver c(nullptr, 0);
   c.take<double>(n);                          // rho
   c.take<double>(n);                          // d_s
-  c.take<double>(2 * size_t(d.nb1));          // part1
+  c.take<double>(2 * size_t(std::max(d.nb1, num_sms())));  // part1 (or the fused recon's per-CTA sums)
   c.take<double>(2 * size_t(d.nb1));          // part2
   c.take<double>(size_t(std::max(d.chunks, d.nbg)) * M * 13);  // part3
   c.take<double>(8);                                             // stats
@@ -681,16 +681,29 @@ static bool packed_density() {  // APMG_DENSITY_X2=0: the one-point-per-lane ker
   return !(e && e[0] == '0');
 }
 
+int density_rho_slots(int M, int64_t n, void* ws, size_t wsb, double** rho, double** part1) {
+  DensPlan d = dens_plan(M, n);
+  Carver c(ws, wsb);
+  *rho = c.take<double>(n);
+  c.take<double>(n);
+  *part1 = c.take<double>(2 * size_t(std::max(d.nb1, num_sms())));
+  if (!c.ok()) {
+    set_error("density workspace too small: need %zu, have %zu", c.used, wsb);
+    return APMG_E_WORKSPACE;
+  }
+  return APMG_OK;
+}
+
 template <typename T, typename TE>
 int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, double* loss, T* dtf,
                    double* rho_total, T* adam_m, T* adam_v, void* ws, size_t wsb, const TrainCtl* ctl,
-                   cudaStream_t st) {
+                   cudaStream_t st, int pre_nb) {
   APMG_ARG_CHECK(M <= kMaxGridsSmem, "density supports up to %d grids", kMaxGridsSmem);
   DensPlan d = dens_plan(M, n);
   Carver c(ws, wsb);
   double* rho = c.take<double>(n);
   double* d_s = c.take<double>(n);
-  double* part1 = c.take<double>(2 * size_t(d.nb1));
+  double* part1 = c.take<double>(2 * size_t(std::max(d.nb1, num_sms())));
   double* part2 = c.take<double>(2 * size_t(d.nb1));
   double* part3 = c.take<double>(size_t(std::max(d.chunks, d.nbg)) * M * 13);
   double* stats = c.take<double>(8);
@@ -701,8 +714,9 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
   int parts = d.chunks;  // gradient partials per grid handed to the finalize kernel
   const char* e64 = getenv("APMG_DENSITY64");  // force the all-fp64 per-pair path (A/B tests)
   const bool fast32 = (sizeof(T) == 4) && !(e64 && e64[0] == '1');
+  APMG_ARG_CHECK(!pre_nb || (fast32 && p == 10), "a precomputed rho needs the f32 p = 10 density path");
   if constexpr (sizeof(T) == 4) {
-    if (fast32) {
+    if (fast32 && !pre_nb) {
       const size_t smem32 = size_t(13) * M * sizeof(float);
       APMG_CUDA_TRY(
           cudaFuncSetAttribute(k_dens_rho32<TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem32)));
@@ -724,7 +738,7 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
     APMG_LAUNCH("density_rho", (k_dens_rho<T, TE>), d.nb1, kDensThreads, smem1, st, tf, M, p, x, err, n, rho, part1,
                 ctl);
   }
-  APMG_LAUNCH("density_stats", k_dens_stats1, 1, 1024, 0, st, part1, d.nb1, n, stats, ctl);
+  APMG_LAUNCH("density_stats", k_dens_stats1, 1, 1024, 0, st, part1, pre_nb ? pre_nb : d.nb1, n, stats, ctl);
   APMG_LAUNCH("density_target", k_dens_target<TE>, d.nb1, kDensThreads, 0, st, rho, err, n, stats, d_s, part2, ctl);
   APMG_LAUNCH("density_stats", k_dens_stats2, 1, 1024, 0, st, part2, d.nb1, n, stats, loss,
               const_cast<TrainCtl*>(ctl));
@@ -762,10 +776,10 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
 }
 
 template int launch_density<float, float>(float*, int, int, const float*, const float*, int64_t, double*, float*,
-                                          double*, float*, float*, void*, size_t, const TrainCtl*, cudaStream_t);
+                                          double*, float*, float*, void*, size_t, const TrainCtl*, cudaStream_t, int);
 template int launch_density<double, double>(double*, int, int, const double*, const double*, int64_t, double*,
                                             double*, double*, double*, double*, void*, size_t, const TrainCtl*,
-                                            cudaStream_t);
+                                            cudaStream_t, int);
 
 // ---- standalone elementwise helpers
 __global__ void k_feature_density_f64pts(const double* __restrict__ s_tf_g, int M, int p, const double* __restrict__ x,

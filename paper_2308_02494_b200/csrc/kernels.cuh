@@ -53,7 +53,13 @@ int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, c
 
 template <typename T, typename TE>
 int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, double* loss, T* dtf, double* rho_total,
-                   T* adam_m, T* adam_v, void* ws, size_t wsb, const TrainCtl* ctl, cudaStream_t st);
+                   T* adam_m, T* adam_v, void* ws, size_t wsb, const TrainCtl* ctl, cudaStream_t st,
+                   int pre_nb = 0);
+// the rho / partial-sum slots of launch_density's workspace, for a producer that fills them
+// ahead of it (the fused recon kernel; then launch_density(..., pre_nb = its CTA count))
+int density_rho_slots(int M, int64_t n, void* ws, size_t wsb, double** rho, double** part1);
+// the recon tc16 kernel's CTA count for a batch of n points
+int recon_tc16_grid(int64_t n);
 size_t density_ws_bytes(int M, int64_t n);
 
 }  // namespace apmg

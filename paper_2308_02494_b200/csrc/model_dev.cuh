@@ -46,6 +46,12 @@ struct ModelDev {
   // deterministic training: the grid gradient is accumulated as 64-bit fixed point (kFxScale)
   // with integer REDs -- associative, so the sum is independent of arrival order
   unsigned long long* dgrid_fx = nullptr;
+  // fused density pass (training, f32, p = 10; tc16 kernel only): the encoder's local
+  // coordinates also give the flat-top bumps, so the kernel writes rho per point
+  // (density.py:83-103) and per-CTA (sum rho, sum sq_err) partials -- the density step then
+  // starts at its statistics (optim.py:158-200)
+  double* rho_out = nullptr;
+  double* rho_part = nullptr;
 };
 
 template <typename T>

@@ -429,6 +429,8 @@ static bool use_tc16() {
   return !(e16 && e16[0] == '0');
 }
 
+int recon_tc16_grid(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms()))); }
+
 bool recon_uses_tc16(const apmg_model& m) {
   if (m.dtype != APMG_F32) return false;
   return use_tc16() && recon_tc_eligible(make_model_dev<float>(m));
@@ -457,7 +459,8 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
     if (md.dgrid_fx)
       APMG_ARG_CHECK(!recon_tc_eligible(md) || use_tc16(), "deterministic gradients need the tc16 or SIMT kernel");
     if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
-      grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms())));
+      grid = recon_tc16_grid(n);
+      APMG_ARG_CHECK(!md.rho_out || use_tc16(), "the fused density pass needs the tc16 kernel");
       // default: bf16x3 all-tcgen05 kernel; APMG_RECON16=0 selects the tf32 / mma.sync one (A/B)
       if (use_tc16())
         rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);

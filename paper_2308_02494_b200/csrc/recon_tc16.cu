@@ -55,7 +55,9 @@ constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
 constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
-constexpr uint32_t SMEM_BYTES = OFF_W3 + 64 * 4;
+constexpr uint32_t OFF_DET = OFF_W3 + 64 * 4;          // [64] |det A| (fused density)
+constexpr uint32_t OFF_RHO = OFF_DET + 64 * 4;         // [NW][P] per-warp partial rho (fused density)
+constexpr uint32_t SMEM_BYTES = OFF_RHO + NW * P * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 constexpr uint32_t TMEM_COLS = 512;
@@ -165,6 +167,30 @@ __device__ __forceinline__ void scatter_pairs(const ModelDev<float>& md, const A
   }
 }
 
+__device__ __forceinline__ float ex2_ftz(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// flat-top bump exp(-sum_d l_d^20) of density.py:83-103 (p = 10) for two points in f32, the
+// arithmetic of k_dens_rho32x2 (l^2 clamped at 4 so the power cannot overflow)
+__device__ __forceinline__ float2 bump_p10x2(float2 l0, float2 l1, float2 l2) {
+  float q[2];
+  const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float acc = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float s = fminf(la[h][d] * la[h][d], 4.f), s2 = s * s, s4 = s2 * s2, s8 = s4 * s4;
+      acc = fmaf(s8 * s, s, acc);
+    }
+    q[h] = acc;
+  }
+  return make_float2(ex2_ftz(q[0] * -1.4426950408889634f), ex2_ftz(q[1] * -1.4426950408889634f));
+}
+
 template <bool FX>  // FX: deterministic training (fixed-point grid gradient)
 __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -188,6 +214,9 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + OFF_TM);
   float* sTF = reinterpret_cast<float*>(sm + OFF_TF);
   float* sW3 = reinterpret_cast<float*>(sm + OFF_W3);
+  float* sDET = reinterpret_cast<float*>(sm + OFF_DET);
+  float* sRHO = reinterpret_cast<float*>(sm + OFF_RHO);
+  const bool rho_on = md.rho_out && (!a.ctl || a.ctl->density_on);
 
   // ---- stage weights (bf16x3, rows = output unit) ----
   for (int e = tid; e < 64 * 16; e += NT) {
@@ -200,6 +229,12 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   }
   for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (tid < HID) sW3[tid] = md.w3[tid];
+  if (rho_on && tid < md.M) {  // |det A| in f64, as density.py:72-80 (stage_transforms32)
+    const float* t = md.tf + 16 * tid;
+    const double c0 = double(t[5]) * t[10] - double(t[6]) * t[9], c1 = double(t[6]) * t[8] - double(t[4]) * t[10],
+                 c2 = double(t[4]) * t[9] - double(t[5]) * t[8];
+    sDET[tid] = float(fabs(double(t[0]) * c0 + double(t[1]) * c1 + double(t[2]) * c2));
+  }
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar, 1);
@@ -245,13 +280,14 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) dw3_acc[c] = 0.f;
   double loss = 0.0;
+  double srho = 0.0;  // fused density: sum of this CTA's rho
   uint32_t phase = 0;
   uint32_t h1pos = 0;  // [h1 > 0] bits of this thread's 8 elements (epilogue 1 -> dz1 epilogue)
 
   // encode of grids 2 warp + 32 jq + {0, 1} for points lane, lane + 32: the two points of a grid
   // share its transform and run in packed fp32x2 arithmetic; the two grids' four features of a
   // point are adjacent in F (one 8-byte store per plane)
-  auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache) {
+  auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache, float2& racc) {
     const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
     const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
     const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
@@ -264,6 +300,10 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
       const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
       const float2 l2 = local_coord2(X0, X1, X2, tf[8], tf[9], tf[10], tf[11]);
+      if (rho_on) {
+        const float2 b = bump_p10x2(l0, l1, l2);
+        racc = make_float2(fmaf(sDET[m], b.x, racc.x), fmaf(sDET[m], b.y, racc.y));
+      }
       int ix[2], iy[2], iz[2];
       float fx[2], fy[2], fz[2];
       axis_term2(l0, md.W, ix[0], ix[1], fx[0], fx[1]);
@@ -318,6 +358,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     // the tile after next: its coordinates / targets are fetched now (registers) and stored to
     // shared memory after the encode, so the global-load latency hides behind it
     float pf[4] = {0.f, 0.f, 0.f, 0.f};
+    float2 racc = make_float2(0.f, 0.f);
     const bool pf_on = prefetch_tile < tiles && tid < P;
     if (pf_on) {
       const int64_t i = prefetch_tile * P + tid;
@@ -332,7 +373,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     for (int jq = 0; jq < GPW / 2; ++jq) {
       if (scatter_cnt >= 0)
         scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
-      encode_group(cX, jq, cache_enc);
+      encode_group(cX, jq, cache_enc, racc);
       if (jq == 0) {
         // features k < 64 (grids 0-31) complete: first half of z1.  Only warp 0 (which issues)
         // waits for the other warps; they signal the named barrier and carry on with group 1
@@ -346,6 +387,10 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       }
     }
     umma::tmem_st_wait();
+    if (rho_on) {  // this warp's 4 grids; summed over the warps in order after the barrier
+      sRHO[warp * P + lane] = racc.x;
+      sRHO[warp * P + lane + 32] = racc.y;
+    }
     if (pf_on) {
       float* dX = sX + (prefetch_slot & 1) * 3 * P;
       dX[3 * tid] = pf[0];
@@ -371,6 +416,17 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     phase ^= 1;
     umma::fence_after_sync();
     TC16_STAMP(1);
+    if (rho_on && tid >= NT - P) {  // rho of this tile's points: the 16 warp partials in order
+      const int pt = tid - (NT - P);
+      float r = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) r += sRHO[w * P + pt];
+      const int64_t i = tile * P + pt;
+      if (i < a.n) {
+        md.rho_out[i] = double(r);
+        srho += double(r);
+      }
+    }
     // ---- epilogue 1: h1 = relu(z1) -> bf16x3; sign bits kept in a register ----
     {
       float v[8];
@@ -601,6 +657,13 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     if (lane < 4) sDW3[quarter * HID + ep_col0 + 8 * (c >> 1) + ec + (c & 1)] = v;  // one writer per slot
   }
   const double bl = block_sum(loss, red);  // contains __syncthreads
+  if (rho_on) {
+    const double br = block_sum(srho, red);
+    if (tid == 0) {  // the rho pass's (sum rho, sum sq_err) partials, one pair per CTA
+      md.rho_part[2 * blockIdx.x] = br;
+      md.rho_part[2 * blockIdx.x + 1] = bl;
+    }
+  }
   if (tid < HID)  // fixed-order sum over the lane quarters: run-to-run deterministic
     dst[HID * FE + HID * HID + tid] = ((sDW3[tid] + sDW3[HID + tid]) + sDW3[2 * HID + tid]) + sDW3[3 * HID + tid];
   if (tid == 0) a.part_loss[blockIdx.x] = bl;

@@ -349,6 +349,18 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   md.gridx = s->gridx;
   md.grad_pairs = s->gradx != nullptr;
   md.dgrid_fx = s->gfx;
+  // density pass fused into the recon kernel (APMG_FUSED_RHO=0: separate rho kernel, A/B)
+  int pre_nb = 0;
+  if constexpr (sizeof(T) == 4) {
+    const char* ef = getenv("APMG_FUSED_RHO");
+    const char* e64 = getenv("APMG_DENSITY64");
+    const char* ex2 = getenv("APMG_DENSITY_X2");
+    if (c.train_transforms && m.flat_top_p == 10 && recon_uses_tc16(live) && !(ef && ef[0] == '0') &&
+        !(e64 && e64[0] == '1') && !(ex2 && ex2[0] == '0')) {
+      if (int rc = density_rho_slots(m.grids, B, s->dens_ws, s->dens_wsb, &md.rho_out, &md.rho_part)) return rc;
+      pre_nb = recon_tc16_grid(B);
+    }
+  }
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
   if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
@@ -388,7 +400,7 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   if (c.train_transforms) {
     rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, static_cast<const T*>(s->coords),
                               static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),
-                              static_cast<T*>(s->tv), s->dens_ws, s->dens_wsb, s->ctl, st);
+                              static_cast<T*>(s->tv), s->dens_ws, s->dens_wsb, s->ctl, st, pre_nb);
     if (rc) return rc;
   }
   APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,

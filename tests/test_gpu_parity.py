@@ -685,3 +685,24 @@ def test_criterion_5_configuration_matches_reference_ensemble():
         gpu.append(P.psnr(m, vol))
     se = np.sqrt(ref.var(ddof=1) / len(ref) + max(np.var(gpu, ddof=1), ref.var(ddof=1)) / len(gpu))
     assert abs(np.mean(gpu) - ref.mean()) <= 3 * se, (gpu, ref.tolist())
+
+
+@pytest.mark.gpu
+def test_fused_density_pass_matches_separate(monkeypatch):
+    """The recon kernel's fused rho (bumps from the encoder's local coordinates, density.py:83-103)
+    feeds the same density step as the separate rho kernel (APMG_FUSED_RHO=0): the density loss
+    and the transform trajectory agree to f32 rounding."""
+    vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
+    out = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("APMG_FUSED_RHO", fused)
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=6, batch_size=1 << 14, delay_start=0, seed=0, plateau_enabled=False,
+                            deterministic=True)
+        m, log = P.train_single(m, vol, cfg)
+        out.append((m.transforms.copy(), np.asarray(log.l_density, dtype=np.float64)))
+    # the density step stops at the hard-stop fraction (0.8 of the run): the last entry is None
+    assert np.isfinite(out[1][1][:4]).all() and np.array_equal(np.isnan(out[1][1]), np.isnan(out[0][1]))
+    np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5, equal_nan=True)
+    np.testing.assert_allclose(out[1][0], out[0][0], rtol=0, atol=1e-5)
