@@ -579,10 +579,12 @@ __global__ void __launch_bounds__(kDensThreads) k_dens_grad32c(const float* __re
 // k_dens_grad32c with two staged points per lane and step (p = 10): float2 accumulators
 __global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float* __restrict__ tf, int M,
                                                                  const float* __restrict__ x, int64_t n,
-                                                                 const float* __restrict__ drho, int ch,
+                                                                 const double* __restrict__ d_s,
+                                                                 const double* __restrict__ stats, int ch,
                                                                  double* __restrict__ part, const TrainCtl* ctl) {
   if (ctl && (ctl->skip || !ctl->density_on)) return;
   extern __shared__ float4 sP[];                                   // [ch <= kGradCH] (x0, x1, x2, d_rho)
+  const double total = stats[0], S = stats[3];  // d_rho formed while staging (k_dens_drho32's value)
   double* s_acc = reinterpret_cast<double*>(sP + kGradCH);         // [M][13]
   float* s_tf = reinterpret_cast<float*>(s_acc + 13 * M);          // [M][13]
   stage_transforms32(tf, M, s_tf);
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float*
     __syncthreads();  // previous chunk consumed, transforms / accumulators staged
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
       const int64_t g = c0 + i;
-      sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], drho[g]);
+      sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], float((d_s[g] - S) / total));
     }
     __syncthreads();
     // two grids per pass (m, m + nw): independent chains for the scheduler, one read of the points
@@ -745,15 +747,16 @@ int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, do
   if constexpr (sizeof(T) == 4) {
     if (fast32) {
       float* drho = reinterpret_cast<float*>(rho);  // rho is dead once the target pass has run
-      APMG_LAUNCH("density_drho", k_dens_drho32, d.nb1, kDensThreads, 0, st, d_s, n, stats, drho, ctl);
+      const bool x2 = M <= kGradMaxM && p == 10 && packed_density();  // forms d_rho itself
+      if (!x2) APMG_LAUNCH("density_drho", k_dens_drho32, d.nb1, kDensThreads, 0, st, d_s, n, stats, drho, ctl);
       if (M <= kGradMaxM) {
         const size_t sm = grad32c_smem(M);
         const int ch = int(std::min<int64_t>(kGradCH, ceil_div(n, d.nbg)));  // one balanced chunk per block
         if (p == 10 && packed_density()) {
           APMG_CUDA_TRY(
               cudaFuncSetAttribute(k_dens_grad32cx2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-          APMG_LAUNCH("density_grad", k_dens_grad32cx2, d.nbg, kDensThreads, sm, st, tf, M, x, n, drho, ch, part3,
-                      ctl);
+          APMG_LAUNCH("density_grad", k_dens_grad32cx2, d.nbg, kDensThreads, sm, st, tf, M, x, n, d_s, stats, ch,
+                      part3, ctl);
         } else {
           APMG_CUDA_TRY(cudaFuncSetAttribute(k_dens_grad32c, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
           APMG_LAUNCH("density_grad", k_dens_grad32c, d.nbg, kDensThreads, sm, st, tf, M, p, x, n, drho, ch, part3,
