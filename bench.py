@@ -343,6 +343,13 @@ def main():
         m2 = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
         cfg2 = PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
                               plateau_enabled=False, seed=seed)
+        # one untimed warm-up call (first-use costs: staging ring, allocator pools, graph build)
+        mw = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
+        # (its own Volume object: a Volume caches its device copy, and the timed call must upload)
+        PT.train_single(mw, PV.Volume(dims=vshape, data=host_vol.data), PT.TrainConfig(iterations=max(W, 1), batch_size=BATCH, delay_start=0,
+                                                     transform_hard_stop_fraction=1.0, plateau_enabled=False,
+                                                     seed=seed))
+        del mw
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
