@@ -431,7 +431,38 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
                              unsigned long long* __restrict__ gfx, int64_t fx_elems) {
   if (ctl->skip) return;
   const T lr_t = T(ctl->lr_main_t), c1 = T(ctl->bc1_main), c2 = T(ctl->bc2_main);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+  int64_t i0 = 0;
+  if constexpr (sizeof(T) == 4) {
+    if (dgx && gx && !gfx) {
+      // x-pair grid cells, one two-channel cell per thread and step (8-byte accesses):
+      // grad(grid[c]) = dgx[c].lo + dgx[c - 1].hi, each half consumed (and cleared) by exactly
+      // one cell's thread; the packed copy gets gx[c].lo = gx[c - 1].hi = grid[c]
+      const int64_t cells = gx_elems >> 1;
+      float2* p2 = reinterpret_cast<float2*>(p);
+      float2* m2 = reinterpret_cast<float2*>(m);
+      float2* v2 = reinterpret_cast<float2*>(v);
+      float2* d2 = reinterpret_cast<float2*>(dgx);
+      float2* x2 = reinterpret_cast<float2*>(gx);
+      for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < cells;
+           c += int64_t(gridDim.x) * blockDim.x) {
+        const float2 lo = d2[2 * c], hi = c > 0 ? d2[2 * c - 1] : make_float2(0.f, 0.f);
+        const float g0 = lo.x + hi.x, g1 = lo.y + hi.y;
+        if (g0 == 0.f && g1 == 0.f) continue;
+        if (lo.x != 0.f || lo.y != 0.f) d2[2 * c] = make_float2(0.f, 0.f);
+        if (hi.x != 0.f || hi.y != 0.f) d2[2 * c - 1] = make_float2(0.f, 0.f);
+        float2 pc = p2[c], mc = m2[c], vc = v2[c];
+        adam_elem(pc.x, g0, mc.x, vc.x, lr_t, c1, c2);
+        adam_elem(pc.y, g1, mc.y, vc.y, lr_t, c1, c2);
+        p2[c] = pc;
+        m2[c] = mc;
+        v2[c] = vc;
+        x2[2 * c] = pc;
+        if (c > 0) x2[2 * c - 1] = pc;
+      }
+      i0 = 2 * cells;
+    }
+  }
+  for (int64_t i = i0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const bool pair = sizeof(T) == 4 && dgx && i < gx_elems;
     const bool fx = gfx && i < fx_elems;  // deterministic mode: fixed-point grid gradient
     T gi = (pair || fx) ? T(0) : g[i];
