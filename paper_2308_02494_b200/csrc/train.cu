@@ -49,6 +49,12 @@ __global__ void k_sample_sorted_bricked(const double* __restrict__ c64, int64_t 
                                         int w, int h, int d, int nbx, int nby, T* __restrict__ coords,
                                         T* __restrict__ targets, const TrainCtl* ctl);
 
+__global__ void k_cell_volume(const float* __restrict__ vol, int w, int h, int d, float4* __restrict__ out);
+template <typename T>
+__global__ void k_sample_sorted_cells(const double* __restrict__ c64, int64_t n, const float4* __restrict__ cells,
+                                      int w, int h, int d, T* __restrict__ coords, T* __restrict__ targets,
+                                      const TrainCtl* ctl);
+
 static bool sort_enabled() {
   const char* e = getenv("APMG_SORT");
   return !(e && e[0] == '0');
@@ -154,6 +160,7 @@ struct apmg_train_state {
   int64_t gx_cells = 0;
   float* vol_bricked = nullptr;
   size_t vol_bricked_bytes = 0;
+  bool vol_cells = false;  // vol_bricked holds the corner-replicated cell copy (k_cell_volume)
   int nbx = 0, nby = 0;
 };
 
@@ -285,7 +292,22 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   }
   {
     const char* eb = getenv("APMG_BRICKED");
-    if (s->sort && !(eb && eb[0] == '0')) {
+    // corner-replicated cells (APMG_CELLVOL=0: off) when 8x the volume stays within 16 GiB
+    const char* ec = getenv("APMG_CELLVOL");
+    const size_t cell_bytes = size_t(32) * size_t(w > 1 ? w - 1 : 1) * size_t(h > 1 ? h - 1 : 1) *
+                              size_t(d > 1 ? d - 1 : 1);
+    if (s->sort && !(ec && ec[0] == '0') && cell_bytes <= (size_t(16) << 30)) {
+      s->vol_bricked = static_cast<float*>(pool_alloc(cell_bytes));
+      if (s->vol_bricked) {
+        s->vol_bricked_bytes = cell_bytes;
+        s->vol_cells = true;
+        const int64_t nc = int64_t(cell_bytes / 32);
+        const int g = int(std::min<int64_t>(ceil_div(nc, 256), int64_t(num_sms()) * 32));
+        APMG_LAUNCH("cell_volume", k_cell_volume, g, 256, 0, st, volume, w, h, d,
+                    reinterpret_cast<float4*>(s->vol_bricked));
+      }
+    }
+    if (s->sort && !s->vol_cells && !(eb && eb[0] == '0')) {
       s->nbx = (w + 7) / 8;
       s->nby = (h + 7) / 8;
       const int nbz = (d + 7) / 8;
@@ -376,7 +398,11 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                   s->c64_sorted, s->perm, s->counts, kBuckets, s->c64_raw, s->ctl);
       sorted = s->c64_raw;
     }
-    if (s->vol_bricked)
+    if (s->vol_cells)
+      APMG_LAUNCH("train_batch", k_sample_sorted_cells<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
+                  reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, static_cast<T*>(s->coords),
+                  static_cast<T*>(s->targets), s->ctl);
+    else if (s->vol_bricked)
       APMG_LAUNCH("train_batch", k_sample_sorted_bricked<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
                   s->vol_bricked, s->w, s->h, s->d, s->nbx, s->nby, static_cast<T*>(s->coords),
                   static_cast<T*>(s->targets), s->ctl);
