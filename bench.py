@@ -1,19 +1,25 @@
 """Benchmark: APMGSRN training throughput (train points/sec) on B200.
 
-Workload (BASELINE.json configs[1], "C2"): 64 grids 32^3 x 2 features, MLP 2x64,
-fit a synthetic 512^3 blob volume (test_acceptance.py:156-164 blob list),
-batch 2^20, density loss on every timed iteration.  One "step" = one training
-iteration (Philox batch + fp64 targets + fused recon fwd/bwd + masked Adam +
-fp64 density step + scheduler), all device-resident.
+N = 1, workload "C2" (BASELINE.json configs[1]): 64 grids 32^3 x 2 features, MLP 2x64, fit a
+synthetic 512^3 blob volume (test_acceptance.py:156-164 blob list), batch 2^20, density loss on
+every timed iteration.  One "step" = one training iteration (Philox batch + fp64 targets + fused
+recon fwd/bwd + masked Adam + density step + scheduler), all device-resident.  ``value`` is
+device-timed (CUDA events on the session's stream); ``e2e`` is train_single through the public
+API with a host model and a host volume (uploads / downloads inside the timed region).
 
-N > 1 (torchrun): weak scaling -- rank r trains brick r of the 2x2x2
-decomposition of a synthetic 1024^3 volume (configs[3]); each brick is an
-independent model (ghost extent ~513^3), no data-path collective; the timing
-is the max over ranks.
+N > 1 (torchrun), workload "C4" (configs[3]): the whole 2x2x2 decomposition of a synthetic
+1024^3 volume (ghost 1, bricks of ~513^3) is fitted through ``train_decomposed``: rank r trains
+bricks flat % world == r (4 / 2 / 1 bricks at N = 2 / 4 / 8), one model per brick, K iterations
+each at batch 2^20, no data-path collective.  ``value`` = all bricks' training points / the max
+over ranks of that rank's device-timed training iterations; ``time_to_fit`` = the max over ranks
+of the whole train_decomposed call (brick ingest from the raw file, training, .apmg save, brick
+PSNR); the decomposed field's PSNR over the 1024^3 lattice comes from per-rank brick sweeps with
+the SSE all-reduced over NCCL.
 
-``--impl reference`` times the reference algorithm (the numpy oracle port; the
-reference itself is pure numpy and not installed on the GPU box) on the host
-cores on a bounded sample of the same workload.
+``--impl reference`` times the reference algorithm on the host cores: the numpy oracle port of
+apmg.train_single (the reference is pure numpy and is not installed on the GPU box), each
+iteration's batch split over all host threads, on the same workload (batch 2^20, same model,
+same volume).
 """
 from __future__ import annotations
 
@@ -117,71 +123,92 @@ def dist_setup():
     return None, 0, 1, local
 
 
-def brick_workload(rank, world):
-    """(volume dims, extent or None, description) of this rank's training unit."""
-    from paper_2308_02494_b200.decomposition import plan_partition
+def workload_config(world):
+    """The `config` object of both arms' JSON lines."""
     if world == 1:
-        return DIMS1, None, "C2: single model, synthetic 512^3 volume"
-    plan = plan_partition(DIMS_DECOMP, 2, 2, 2, ghost=1)
-    brick = plan.bricks[rank % plan.brick_count]
-    return DIMS_DECOMP, brick.ghost, f"C4: brick {rank % 8} of 2x2x2 over synthetic 1024^3 (ghost 1)"
+        return {"workload": "C2: single model, synthetic 512^3 volume", "global_batch": BATCH,
+                "model": "APMGSRN 64 grids 32^3 x2, MLP 2x64", "density_loss": "every timed iteration",
+                "parallelism": "single GPU (replicas only)",
+                "l2": "inputs larger than L2 (512 MiB volume); 16 MiB grids L2-resident by design"}
+    return {"workload": "C4: 2x2x2 bricks of synthetic 1024^3 (ghost 1), one model per brick, train_decomposed",
+            "global_batch": BATCH * min(world, 8), "model": "APMGSRN 64 grids 32^3 x2, MLP 2x64 per brick",
+            "density_loss": "every timed iteration", "parallelism": f"brick-sharded x{world} (flat % world)",
+            "l2": "inputs larger than L2 (~540 MB brick volume per session)"}
 
 
 # algorithmic work per training point (SURVEY 8d) -> per-kernel roofline rows
 ENC_BYTES = 8 * M * CH * 4          # 4,096 B of corner data gathered per point (encoder fwd)
 SCAT_BYTES = 8 * M * CH * 4         # 4,096 B of corner gradients reduced per point (encoder bwd)
-STREAM_BYTES = 12 + 4 + 4           # coords in, target in, squared error out
+RED4_PER_PT = 4 * M                 # x-pair layout: 4 float4 REDs per (point, grid) before aggregation
+MLP_FLOP = 74_112                   # 24,704 forward + 49,408 backward (SURVEY 8d)
+MLP_ISSUED = 24_704 * 6 + 49_152 * 3  # bf16x3: 6 products per forward GEMM, 3 per backward GEMM
+DENS_GRAD_FLOP = M * 100            # per point: bump (~35), l^(2p-1) powers, 13 accumulators x2
+INFER_ISSUED = 24_704 * 6           # C3 forward: 6 bf16x3 products per GEMM
+
+
+def _traffic(kernel):
+    """(dram bytes, l2 bytes) per launch of `kernel` from the newest profiles/traffic_*.json."""
+    files = sorted((ROOT / "profiles").glob("traffic_r*.json"))
+    if not files:
+        return None, None
+    v = json.loads(files[-1].read_text()).get(kernel)
+    if isinstance(v, dict):
+        return v.get("dram"), v.get("l2")
+    return v, None
+
+
+def _peaks2():
+    f = ROOT / "profiles" / "peaks_b200.json"
+    return json.loads(f.read_text()) if f.exists() else {}
 
 
 def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
-    """Dominant-kernel roofline.  Bytes are ALGORITHMIC bytes per launch (SURVEY 8d per-point
-    figure x the 2^20 points one launch processes); the grid gather/scatter traffic is served
-    by L2 (16 MiB grids stay resident), so the HBM copy peak is a conservative denominator."""
+    """Roofline of one kernel from its average device time per launch (CUDA events inside the
+    bench) and its ALGORITHMIC work per launch (SURVEY 8d per-point figure x 2^20 points).
+
+    k_recon_tc16 (encode -> tcgen05 MLP -> scatter): the 16 MiB grids and their x-pair copies are
+    L2-resident, so the encoder is bound by L2 gather bandwidth (the kernel issues float4 gathers:
+    peak = the random float4 gather probe) and the scatter by L2 RED throughput (float4 RED probe);
+    the MLP by the tensor pipe.  The primary (`bound: l2`) is the encoder gather, SURVEY 8d's and
+    north_star's metric; `components` gives all three and `serial_sum_frac` = sum of each part's
+    time at its peak / measured time (> 1 means the parts overlap or L1 serves part of them)."""
     t = ms_per_launch * 1e-3
-    per_point = {
-        "recon_fwd_bwd_tc": ENC_BYTES + SCAT_BYTES + STREAM_BYTES,
-        "recon_fwd_bwd": ENC_BYTES + SCAT_BYTES + STREAM_BYTES,
-        "density_grad": 12 + 4,
-        "density_rho": 12 + 4 + 8,
-        "train_batch": 8 * 4 + 16,
-    }
-    if kernel == "adam_main":
-        nbytes = 4_206_656 * 4 * 7
-    else:
-        nbytes = BATCH * per_point.get(kernel, float("nan"))
+    pk2 = _peaks2()
+    dram, l2b = _traffic(kernel)
+    base = {"kernel": kernel, "ms_per_launch": ms_per_launch, "traffic": dram, "l2_traffic": l2b,
+            "traffic_source": "ncu --set full dram__bytes_read+write.sum (lts__t_bytes.sum) per launch, "
+                              "profiles/traffic_r*.json"}
+    if kernel.startswith("recon_fwd_bwd") and pk2:
+        g_pk = pk2["l2_gather_float4_GBps_16MiB"]
+        r_pk = pk2.get("l2_red_float4_Gops_16MiB") or pk2["l2_red_float2_Gops_16MiB"]
+        g_ach = BATCH * ENC_BYTES / t / 1e9
+        r_ach = BATCH * RED4_PER_PT / t / 1e9
+        f_alg = BATCH * MLP_FLOP / t / 1e12
+        f_iss = BATCH * MLP_ISSUED / t / 1e12
+        comps = {
+            "encoder_gather": {"achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
+                               "work": "4,096 B/pt (64 grids x 4 float4 corner pairs)"},
+            "scatter_red": {"achieved": r_ach, "peak": r_pk, "unit": "G float4 RED/s", "frac": r_ach / r_pk,
+                            "work": "256 float4 REDs/pt before warp aggregation"},
+            "mlp_tensor": {"achieved": f_iss, "algorithmic": f_alg, "peak": pk["bf16_tflops"],
+                           "unit": "TFLOP/s issued (bf16x3 products)", "frac": f_iss / pk["bf16_tflops"],
+                           "work": "295,680 issued FLOP/pt (74,112 algorithmic)"}}
+        return {"bound": "l2", **base, "achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
+                "components": comps, "serial_sum_frac": sum(c["frac"] for c in comps.values()),
+                "peak_source": "profiles/peaks_b200.json (tools/peaks.py): random float4 gather / float4 RED "
+                               "over a 16 MiB table; MEASURED_PEAKS.json bf16 dense"}
+    if kernel == "density_grad" and pk2:
+        a = BATCH * DENS_GRAD_FLOP / t / 1e12
+        return {"bound": "fp32", **base, "achieved": a, "peak": pk2["fp32_tflops"], "unit": "TFLOP/s",
+                "frac": a / pk2["fp32_tflops"], "work": f"{DENS_GRAD_FLOP} FP32 FLOP/pt (64 grids x ~100)",
+                "peak_source": "profiles/peaks_b200.json fp32_tflops (FFMA probe)"}
+    per_point = {"train_batch": 32 + 24 + 8, "density_rho": 12 + 4 + 8, "batch_keys": 24 + 4,
+                 "bucket_scatter": 48}
+    nbytes = 4_206_656 * 4 * 7 if kernel == "adam_main" else BATCH * per_point.get(kernel, float("nan"))
     peak = pk.get("hbm_gbs", 6650.0)
     achieved = nbytes / t / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "traffic_r01.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(kernel)
-    out = {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-           "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
-           "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
-           "note": "algorithmic encoder gather + scatter bytes (4096+4096+20 B/pt); served from L2"}
-    pf = ROOT / "profiles" / "peaks_b200.json"
-    if kernel.startswith("recon_fwd_bwd") and pf.exists():
-        # SURVEY 8(d): encoder fwd is bound by L2 gather bandwidth, encoder bwd by L2 RED
-        # throughput -- algorithmic units of one launch against the probes of tools/peaks.py
-        pk2 = json.loads(pf.read_text())
-        g_ach = BATCH * ENC_BYTES / t / 1e9
-        r_ach = BATCH * (SCAT_BYTES // 8) / t / 1e9
-        fl_ach = BATCH * 74112 / t / 1e12
-        fl_iss = BATCH * (24704 * 6 + 49152 * 3) / t / 1e12
-        out["l2"] = {
-            "gather": {"achieved": g_ach, "peak": pk2["l2_gather_float2_GBps_16MiB"], "unit": "GB/s",
-                       "frac": g_ach / pk2["l2_gather_float2_GBps_16MiB"]},
-            "red": {"achieved": r_ach, "peak": pk2["l2_red_float2_Gops_16MiB"], "unit": "G float2 RED/s",
-                    "frac": r_ach / pk2["l2_red_float2_Gops_16MiB"]},
-            "mlp_tensor": {"achieved": fl_ach, "issued": fl_iss, "peak": pk["bf16_tflops"],
-                           "unit": "TFLOP/s (bf16 tensor pipe)", "frac": fl_iss / pk["bf16_tflops"],
-                           "note": "achieved = algorithmic MLP FLOP (74,112/pt); issued = bf16x3 products "
-                                   "(6 per forward, 3 per backward product: 295,680 FLOP/pt)"},
-            "peak_source": "profiles/peaks_b200.json (tools/peaks.py: random float2 over a 16 MiB table)",
-            "note": "gather and RED are the un-aggregated algorithmic counts (512 corner loads and 512 "
-                    "float2 REDs per point); warp coherence and aggregation let the kernel exceed the "
-                    "random-access RED probe"}
-    return out
+    return {"bound": "hbm", **base, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
 
 
 def kernel_table():
@@ -199,36 +226,52 @@ def kernel_table():
     return out
 
 
-def run_cpu_baseline(vol_host, seconds_budget=25.0):
-    """Oracle port (reference algorithm, numpy) on a bounded sample: batch 2^16, density on."""
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run_cpu_baseline(vol_host, iterations=3):
+    """cpu_baseline of the GPU arm: the oracle port of train_single (reference algorithm, numpy,
+    batch split over all host threads) on a bounded sample of the same workload: one warm-up and
+    `iterations` timed iterations at batch 2^20, density on, same model and volume."""
     from oracle import apmg_oracle as O
-    batch = 1 << 16
+    thr = host_threads()
     prm = O.init_params(M, CH, RES, seed=0, vmin=float(vol_host.min()), vmax=float(vol_host.max()))
     stamps = []
-    cfg = O.LoopConfig(iterations=4, batch_size=batch, delay_start=0, transform_hard_stop_fraction=1.0,
+    cfg = O.LoopConfig(iterations=iterations + 1, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
                        plateau_enabled=False, seed=0)
     t0 = time.perf_counter()
-    O.train_single(prm, vol_host, cfg, on_iteration=lambda it, p: stamps.append(time.perf_counter()))
+    O.train_single_threaded(prm, vol_host, cfg, thr, on_iteration=lambda it, p: stamps.append(time.perf_counter()))
     per_it = np.diff([t0] + stamps)[1:]  # drop the first (warm-up) iteration
-    rate = batch / float(np.mean(per_it))
-    return {"value": rate, "unit": METRIC, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"3 timed iterations (after 1 warm-up) of batch 2^16, density on, same model/512^3 volume; "
-                      f"numpy oracle restating apmg.train_single, {os.cpu_count()} host threads available"}
+    rate = BATCH / float(np.mean(per_it))
+    return {"value": rate, "unit": METRIC, "cores": thr, "kind": "port",
+            "sample": f"{iterations} timed iterations (after 1 warm-up) of the C2 workload at batch 2^20, density "
+                      f"on, same model / 512^3 volume; numpy oracle of apmg.train_single, each iteration's batch "
+                      f"split over {thr} host threads"}
 
 
 def run_reference(args):
-    dist, rank, world, _ = dist_setup() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 0, 1, 0)
+    """Reference arm: the oracle port of apmg.train_single on the host cores, on this arm's own
+    workload and batch (2^20), W untimed + K timed iterations, all host threads.  Under torchrun
+    only rank 0 runs (the others exit); at N > 1 the workload is one C4 brick model's iterations
+    (every brick runs the same per-iteration work)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import apmg_oracle as O
-    vol = O.synth_volume(DIMS1, BLOBS)
-    batch = 1 << 16
+    thr = host_threads()
+    dims = DIMS1 if world == 1 else tuple(n // 2 + 1 for n in DIMS_DECOMP)  # a C4 ghost brick is ~513^3
+    vol = O.synth_volume(dims, BLOBS)
     prm = O.init_params(M, CH, RES, seed=0, vmin=float(vol.min()), vmax=float(vol.max()))
     total = args.warmup + args.steps
-    cfg = O.LoopConfig(iterations=total, batch_size=batch, delay_start=0, transform_hard_stop_fraction=1.0,
+    cfg = O.LoopConfig(iterations=total, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
                        plateau_enabled=False, seed=0)
     stamps = []
-    budget = float(os.environ.get("APMG_REF_BUDGET_S", "150"))
+    budget = float(os.environ.get("APMG_REF_BUDGET_S", "1500"))
     t_start = time.perf_counter()
 
     class Budget(Exception):
@@ -236,26 +279,36 @@ def run_reference(args):
 
     def cb(it, p):
         stamps.append(time.perf_counter())
-        if it >= args.warmup and stamps[-1] - stamps[args.warmup - 1 if args.warmup else 0] > budget:
+        if it >= args.warmup and stamps[-1] - t_start > budget:
             raise Budget()
 
     try:
-        O.train_single(prm, vol, cfg, on_iteration=cb)
+        O.train_single_threaded(prm, vol, cfg, thr, on_iteration=cb)
     except Budget:
         pass
     t0 = stamps[args.warmup - 1] if args.warmup else t_start
     timed = len(stamps) - args.warmup
     dt = stamps[-1] - t0
-    value = timed * batch / dt
+    value = timed * BATCH / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world,
             "steps": timed, "warmup": args.warmup, "ms_per_step": 1e3 * dt / timed, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-            "config": {"workload": "C2 sample: 64 grids 32^3x2, MLP 2x64, synthetic 512^3, density on",
-                       "global_batch": batch, "note": "reference step = one iteration at batch 2^16 (bounded)"},
-            "cpu_baseline": {"value": value, "unit": METRIC, "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"{timed} iterations of batch 2^16 (numpy oracle of apmg.train_single)"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 model / f64 density and scatter sums (numpy)",
+            "data": "synthetic", "config": workload_config(world),
+            "cpu_baseline": {"value": value, "unit": METRIC, "cores": thr, "kind": "port",
+                             "sample": f"{timed} timed iterations (after {args.warmup} warm-up) at batch 2^20 of "
+                                       f"{'the C2 workload' if world == 1 else 'one C4 brick (513^3)'}; numpy "
+                                       f"oracle of apmg.train_single, batch split over {thr} host threads; rank 0 "
+                                       f"only"},
             "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if timed < args.steps:
+        line["note"] = f"stopped after {timed} of {args.steps} timed iterations (APMG_REF_BUDGET_S={budget:.0f})"
     print(json.dumps(line), flush=True)
+
+
+DTYPE = ("f32 params/activations; encoder lerps f32; MLP on tcgen05 as bf16x3 split products (6 per forward "
+         "GEMM ~2^-24, 3 per backward GEMM ~2^-16) with f32 accumulation; grid gradient f32 RED; density: "
+         "per-(point, grid) bumps in f32 (SFU exp2), per-point rho and all statistics / loss / transform-gradient "
+         "sums in f64; targets f64 trilinear; loss f64")
 
 
 def main():
@@ -271,6 +324,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return main_decomposed(args)
 
     import torch
     from paper_2308_02494_b200 import _lib as L
@@ -278,15 +333,12 @@ def main():
     from paper_2308_02494_b200 import trainer as PT
     from paper_2308_02494_b200 import volume as PV
 
-    dist, rank, world, local = dist_setup()
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(0)
     L.lib()
-    dims, extent, desc = brick_workload(rank, world)
     blobs = [PV.BlobSpec(c, s, a) for c, s, a in BLOBS]
-    vdev = PV.synth_volume_device(dims, blobs, extent=extent)
-    vshape = extent.shape() if extent is not None else dims
-    vol = PV.Volume.from_device(vshape, vdev)
-    seed = (0 ^ rank) & 0x7FFFFFFF
+    vdev = PV.synth_volume_device(DIMS1, blobs)
+    vol = PV.Volume.from_device(DIMS1, vdev)
+    seed = 0
     model = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
     K, W = args.steps, max(args.warmup, 3)
     KT = 5  # untimed iterations after the timed region, run with per-kernel CUDA events
@@ -295,21 +347,15 @@ def main():
     sess = PT.TrainSession(model, vol, cfg)
     sess.run(W)
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = L.lib().apmg_launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(0) as clk:
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
         e0.record(stream)
         sess.run(K)
         e1.record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     launches = L.lib().apmg_launch_count() - launches0
     ms = e0.elapsed_time(e1)
     # per-kernel shares from a separate, untimed pass (events around every launch perturb
@@ -321,84 +367,169 @@ def main():
     L.lib().apmg_kernel_timing_enable(0)
     ran, _ = sess.status()
     assert ran == W + K + KT, f"expected {W + K + KT} iterations, ran {ran}"
-    if dist:
-        t = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     log = sess.log()
     sess.close()
-    value = world * K * BATCH / (ms * 1e-3)
+    value = K * BATCH / (ms * 1e-3)
 
-    # dominant kernel and its roofline
-    dom = max(ktab.items(), key=lambda kv: kv[1]["total_ms"])
+    # dominant kernel and its roofline (+ the other step kernels' rows)
     pk = peaks()
-    roof = roofline_for(dom[0], dom[1]["total_ms"] / dom[1]["launches"], pk)
+    per_launch = {k: v["total_ms"] / v["launches"] for k, v in ktab.items() if v["launches"]}
+    dom = max(ktab.items(), key=lambda kv: kv[1]["total_ms"])[0]
+    roof = roofline_for(dom, per_launch[dom], pk)
+    roof["other_kernels"] = {k: {kk: r[kk] for kk in ("bound", "achieved", "peak", "unit", "frac")}
+                             for k in ("density_grad", "adam_main", "train_batch") if k in per_launch
+                             for r in [roofline_for(k, per_launch[k], pk)]}
     shares = {k: round((v["total_ms"] / KT) / (ms / K), 4)
               for k, v in sorted(ktab.items(), key=lambda kv: -kv[1]["total_ms"])}
 
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        host_vol = PV.Volume(dims=vshape, data=L.to_host(vdev))
+        host_vol = PV.Volume(dims=DIMS1, data=L.to_host(vdev))
         m2 = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
         cfg2 = PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
                               plateau_enabled=False, seed=seed)
-        # one untimed warm-up call (first-use costs: staging ring, allocator pools, graph build)
+        # one untimed warm-up call (first-use costs: staging ring, allocator pools, graph build);
+        # train_single hands its large blocks back at return, so the timed call allocates afresh
         mw = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
-        # (its own Volume object: a Volume caches its device copy, and the timed call must upload)
-        PT.train_single(mw, PV.Volume(dims=vshape, data=host_vol.data), PT.TrainConfig(iterations=max(W, 1), batch_size=BATCH, delay_start=0,
-                                                     transform_hard_stop_fraction=1.0, plateau_enabled=False,
-                                                     seed=seed))
+        PT.train_single(mw, PV.Volume(dims=DIMS1, data=host_vol.data),
+                        PT.TrainConfig(iterations=max(W, 1), batch_size=BATCH, delay_start=0,
+                                       transform_hard_stop_fraction=1.0, plateau_enabled=False, seed=seed))
         del mw
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
         t0 = time.perf_counter()
         _, log2 = PT.train_single(m2, host_vol, cfg2)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if dist:
-            tt = torch.tensor([dt], device="cuda" if dist.get_backend() == "nccl" else "cpu",
-                              dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
         params_b = 4 * m2.parameter_count()
-        e2e = {"value": world * K * BATCH / dt, "unit": METRIC,
+        e2e = {"value": K * BATCH / dt, "unit": METRIC,
                "h2d_bytes_per_step": int((host_vol.data.nbytes + params_b + 16 * K) / K),
                "d2h_bytes_per_step": int((params_b + 24 * K) / K),
                "setup_ms": round(1e3 * log2.setup_seconds, 2), "setup_split_ms": log2.setup_ms,
-               "wall_ms": round(1e3 * dt, 2),
+               "loop_ms": round(log2.loop_ms, 2), "wall_ms": round(1e3 * dt, 2),
                "note": f"paper_2308_02494_b200.train_single(host model, host Volume, iterations={K}): "
                        f"volume + parameter upload, device loop, parameter + log download"}
 
-    infer = None
-    if not args.no_inference:
-        infer = bench_inference(model_from_session=None) if world == 1 else \
-            bench_decomposed_inference(rank, world, dist)
+    infer = None if args.no_inference else bench_inference()
+    render = None if args.no_render else bench_render()
+    cpu = None if args.no_cpu_baseline else run_cpu_baseline(L.to_host(vdev))
 
-    render = None
-    if rank == 0 and world == 1 and not args.no_render:
-        render = bench_render()
+    line = {
+        "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DTYPE, "data": "synthetic", "config": workload_config(1),
+        "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
+        "kernel_share": shares, "e2e": e2e, "cpu_baseline": cpu, "inference": infer, "render": render,
+        "final_l_rec": log.l_rec[-1] if log.l_rec else None,
+    }
+    print(json.dumps(line), flush=True)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline(L.to_host(vdev))
 
+def main_decomposed(args):
+    """N > 1: the C4 workload through train_decomposed (see the module docstring)."""
+    import shutil
+    import tempfile
+
+    import torch
+    from paper_2308_02494_b200 import _lib as L
+    from paper_2308_02494_b200 import volume as PV
+    from paper_2308_02494_b200.decomposition import (DecomposedField, load_manifest, plan_partition,
+                                                     train_decomposed)
+    from paper_2308_02494_b200.model import ModelConfig
+    from paper_2308_02494_b200.trainer import TrainConfig
+
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) for the driver's log
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist, rank, world, local = dist_setup()
+    L.lib()
+    dev = torch.device("cuda", local)
+    K, W = args.steps, max(args.warmup, 3)
+    blobs = [PV.BlobSpec(c, s, a) for c, s, a in BLOBS]
+    work = Path(os.environ.get("APMG_C4_DIR", tempfile.gettempdir())) / "apmg_c4"
+    raw = work / "volume_1024.raw"
+    if rank == 0:  # synthetic 1024^3 on the device -> the raw little-endian file the API ingests
+        work.mkdir(parents=True, exist_ok=True)
+        v = PV.synth_volume_device(DIMS_DECOMP, blobs)
+        L.to_host(v).astype("<f4").tofile(raw)
+        del v
+        torch.cuda.empty_cache()
+    dist.barrier()
+    header = PV.VolumeHeader(dims=DIMS_DECOMP)
+    plan = plan_partition(DIMS_DECOMP, 2, 2, 2, ghost=1)
+    mcfg = ModelConfig(M, CH, RES)
+
+    def fit(iters, out):
+        tcfg = TrainConfig(iterations=iters, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
+                           plateau_enabled=False, seed=0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        man = train_decomposed(raw, header, plan, mcfg, tcfg, out)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        return man, e0.elapsed_time(e1), wall
+
+    fit(W, work / f"warm_{world}")  # untimed: first-use costs (graphs, pools, staging ring)
+    launches0 = L.lib().apmg_launch_count()
+    with ClockSampler(local) as clk:
+        man, fit_ms, wall = fit(K, work / f"fit_{world}")
+    launches = L.lib().apmg_launch_count() - launches0
+    mine = [b for b in range(plan.brick_count) if b % world == rank]
+    train_ms = sum(float(man.bricks[b]["loop_ms"]) for b in mine)
+    t = torch.tensor([train_ms, fit_ms, wall], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    train_ms, fit_ms, wall = (float(v) for v in t.tolist())
+    points = sum(int(b["iterations_run"]) * BATCH for b in man.bricks)
+    value = points / (train_ms * 1e-3)
+
+    # PSNR of the fitted decomposed field over the whole 1024^3 lattice: each rank sweeps the voxel
+    # boxes its bricks own (box-local truth from the same synthesis), SSE all-reduced over NCCL
+    field = DecomposedField.load(work / f"fit_{world}" / "manifest.json")
+    boxes = field.brick_boxes(DIMS_DECOMP)
+    truth = {}
+    for b in mine:
+        x0, x1, y0, y1, z0, z1 = boxes[b]
+        truth[b] = PV.synth_volume_device(DIMS_DECOMP, blobs, extent=PV.Extent(lo=(x0, y0, z0), hi=(x1, y1, z1)))
+    sse = L.zeros((1,), np.float64)
+    field.lattice_sse_local(mine, truth, None, sse)
+    sse = sse.to(dev)
+    dist.all_reduce(sse)
+    vmin = torch.tensor([min(float(b["vmin"]) for b in man.bricks)], device=dev, dtype=torch.float64)
+    vmax = torch.tensor([max(float(b["vmax"]) for b in man.bricks)], device=dev, dtype=torch.float64)
+    mse = float(sse.item()) / float(np.prod(DIMS_DECOMP))
+    span = float(vmax.item() - vmin.item())
+    psnr = 200.0 if mse == 0 else min(200.0, 10.0 * np.log10(span * span / mse))
+
+    infer = None if args.no_inference else bench_decomposed_inference(rank, world, dist)
     if rank == 0:
+        brick_bytes = sum(np.prod([h - l + 1 for l, h in zip(b["ghost_lo"], b["ghost_hi"])]) * 4 for b in man.bricks)
         line = {
             "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 (bf16x3 tensor-core MLP: 6-product forward, 3-product backward; f64 density statistics and loss)", "data": "synthetic",
-            "config": {"workload": desc, "global_batch": BATCH * world, "model": "APMGSRN 64 grids 32^3 x2, MLP 2x64",
-                       "density_loss": "every timed iteration", "parallelism": f"brick-sharded x{world}",
-                       "l2": "inputs larger than L2 (512 MiB+ volume per rank); 16 MiB grids L2-resident by design"},
-            "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
-            "kernel_share": shares, "e2e": e2e, "cpu_baseline": cpu, "inference": infer, "render": render,
-            "final_l_rec": log.l_rec[-1] if log.l_rec else None,
+            "ms_per_step": train_ms / (K * len(mine)), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": DTYPE, "data": "synthetic", "config": workload_config(world),
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+            "time_to_fit": {"ms": fit_ms, "wall_ms": 1e3 * wall, "bricks": plan.brick_count,
+                            "iterations_per_brick": K, "bricks_per_rank": [len([b for b in range(8) if b % world == r])
+                                                                           for r in range(world)],
+                            "note": "max over ranks of the train_decomposed call: raw-file ingest, training, "
+                                    ".apmg save and brick PSNR of every brick the rank owns"},
+            "train_ms_max_rank": train_ms,
+            "psnr_db": psnr, "psnr_note": "decomposed field over the 1024^3 lattice, per-rank brick sweeps, "
+                                          "SSE all-reduced over NCCL (after K iterations: throughput run)",
+            "e2e": {"value": points / wall, "unit": METRIC, "h2d_bytes_per_step": int(brick_bytes / K),
+                    "d2h_bytes_per_step": int(plan.brick_count * 4 * 4_207_680 / K),
+                    "note": "train_decomposed wall time, max over ranks: raw file -> pinned ring -> GPU per brick, "
+                            "device loop, model download + save"},
+            "cpu_baseline": None, "inference": infer,
         }
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    dist.barrier()
+    if rank == 0:
+        shutil.rmtree(work / f"warm_{world}", ignore_errors=True)
+    dist.destroy_process_group()
 
 
 def bench_render(size=512, samples=128, reps=5):
@@ -428,7 +559,7 @@ def bench_render(size=512, samples=128, reps=5):
                       f"mean alpha {float(img[..., 3].mean()):.3f}"}
 
 
-def bench_inference(model_from_session=None, dims=(1024, 1024, 1024)):
+def bench_inference(dims=(1024, 1024, 1024)):
     """C3: full-volume 1024^3 lattice sweep of one model (PSNR mode: fused forward + fp64 SSE)."""
     import torch
     from paper_2308_02494_b200 import _lib as L
@@ -453,8 +584,21 @@ def bench_inference(model_from_session=None, dims=(1024, 1024, 1024)):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     vox = dims[0] * dims[1] * dims[2]
+    pk = peaks()
+    t = ms * 1e-3
+    iss = vox * INFER_ISSUED / t / 1e12
+    dram, l2b = _traffic("infer_lattice_tc")
+    roof = {"bound": "tensor", "kernel": "infer_lattice_tc (k_infer_tc)", "achieved": iss, "peak": pk["bf16_tflops"],
+            "unit": "TFLOP/s issued (bf16x3: 6 products per GEMM, 147,456 FLOP/voxel)",
+            "frac": iss / pk["bf16_tflops"], "algorithmic_tflops": vox * 24_704 / t / 1e12,
+            "gather_bytes_per_s": vox * ENC_BYTES / t,
+            "gather_note": "4,096 B/voxel of corner data; lattice sweeps are coherent, most corners hit L1",
+            "traffic": dram, "l2_traffic": l2b,
+            "traffic_note": "ncu bytes per launch of the profiled 512^3 sweep (profiles/traffic_r*.json)",
+            "peak_source": "MEASURED_PEAKS.json bf16 dense"}
     return {"metric": "inference voxels/sec", "value": vox / (ms * 1e-3), "ms_per_sweep": ms,
-            "config": "C3: 1024^3 lattice, one 64x32^3x2 model, fused forward + fp64 SSE vs truth"}
+            "config": "C3: 1024^3 lattice, one 64x32^3x2 model, fused forward + fp64 SSE vs truth",
+            "roofline": roof}
 
 
 DIMS_C5 = (2048, 2048, 2048)

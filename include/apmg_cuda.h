@@ -252,26 +252,16 @@ int apmg_train_status(apmg_train_state* s, int64_t* iterations_run, int32_t* fin
 int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_density, double* lr, int64_t* stop_iteration,
                    int64_t* triggers, int64_t* n_triggers, void* stream);
 int apmg_train_destroy(apmg_train_state* s);
+/* Adam moments of the session (replaces reading optim.py:38-44 AdamState.m / .v after
+ * trainer.py:190-204): device copies into main_m / main_v (apmg_main_layout, grids channel-last)
+ * and tf_m / tf_v ((grids, 4, 4)); null destinations are skipped.  Stream-ordered. */
+int apmg_train_moments(apmg_train_state* s, void* main_m, void* main_v, void* tf_m, void* tf_v, void* stream);
 
-/* ---- tcgen05 self-test (one CTA, one GEMM; see csrc/umma_debug.cu) ---------- */
-int apmg_debug_umma_gemm(int32_t cfg, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
-                         float* D, void* stream);
-/* 16-bit self-test (csrc/umma_bf16_debug.cu): D[M][N] = A[M][K] . B[K][N] (row-major f32 in),
- * bf16x3 operands, mode bit 0 = B MN-major, bit 1 = A MN-major, split3: 6 products */
-int apmg_debug_umma_bf16(int32_t mode, int32_t M, int32_t K, int32_t N, int32_t split3, const float* A, const float* B,
-                         float* D, void* stream);
-/* clock64 stamps [16 tiles][12 phases] of CTA 0 of the last fused recon launch run with
- * APMG_TC_SKIP & 64 (profiling aid, tools/tc_phases.py) */
-int apmg_debug_tc_phases(long long* out);
-/* same for the tensor-core lattice sweep: [16 tiles][8 phases] (APMG_INFER_STAMPS=1) */
+/* clock64 stamps [16 tiles][8 phases] of CTA 0 of the last tensor-core lattice sweep run with
+ * APMG_INFER_STAMPS=1 (profiling aid, tools/infer_phases.py) */
 int apmg_debug_infer_phases(long long* out);
-/* same for the bf16x3 recon kernel: [16 tiles][12 phases] (APMG_TC_STAMPS=1) */
+/* same for the bf16x3 recon kernel: [16 tiles][12 phases] (APMG_TC_STAMPS=1, tools/tc16_phases.py) */
 int apmg_debug_tc16_phases(long long* out);
-/* roofline peak probes (csrc/peaks.cu, tools/peaks.py): kind 0 L2 float2 gather (7: float4), 1 L2 float2
- * RED, 2 FP32 FFMA, 3 FP64 DFMA, 4 tcgen05 kind::tf32, 5 warp shuffles; `table` is a device
- * buffer of table_bytes (power of two) for kinds 0-1 (a sink otherwise); *work receives the
- * work unit count of the launch (bytes, REDs, FLOP, FLOP, FLOP, shuffles). */
-int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, int32_t iters, double* work, void* stream);
 
 /* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
 /* plateau_step (trainer.py:118-138) on the same code the device controller runs.

@@ -652,3 +652,148 @@ def init_params(grids, channels, res, seed, vmin=0.0, vmax=1.0, p=10) -> Params:
     f32 = np.float32
     return Params(tf.astype(f32), gr.astype(f32), w1.astype(f32), w2.astype(f32), w3.astype(f32),
                   float(vmin), float(vmax), p)
+
+
+# ---------------------------------------------------------------- threaded CPU baseline
+def _chunks(n: int, parts: int):
+    step = -(-n // parts)
+    return [(s, min(n, s + step)) for s in range(0, n, step)]
+
+
+def _recon_partial(prm: Params, coords, targets, n_total):
+    """recon_loss_and_grads (optim.py:102-155) on one slice of the batch, with the global batch
+    size in the 2/N factor: partial weight gradients, partial f64 grid-gradient sums, sq."""
+    feats, terms = encode(prm, coords, keep_terms=True)
+    z1, h1, z2, h2, out = decode_chain(prm, feats)
+    resid = out - targets
+    sq = resid * resid
+    span = np.asarray(prm.vmax - prm.vmin, dtype=prm.dtype)
+    g_out = (resid * (np.asarray(2.0 / n_total, dtype=prm.dtype) * span))[:, None]
+    g_w3 = g_out.T @ h2
+    g_z2 = (g_out @ prm.w3) * (z2 > 0)
+    g_w2 = g_z2.T @ h1
+    g_z1 = (g_z2 @ prm.w2) * (z1 > 0)
+    g_w1 = g_z1.T @ feats
+    g_feat = g_z1 @ prm.w1
+    m, c = prm.grids.shape[:2]
+    d, h, w = prm.grids.shape[2:]
+    g_grids = np.zeros(prm.grids.shape, dtype=np.float64)
+    for g in range(m):
+        inside, (ix, iy, iz), (fx, fy, fz) = terms[g]
+        sel = np.nonzero(inside)[0]
+        if not len(sel):
+            continue
+        ix, iy, iz, fx, fy, fz = ix[sel], iy[sel], iz[sel], fx[sel], fy[sel], fz[sel]
+        idx, wts = [], []
+        for dz in (0, 1):
+            wz = fz if dz else 1.0 - fz
+            for dy in (0, 1):
+                wy = fy if dy else 1.0 - fy
+                for dx in (0, 1):
+                    wx = fx if dx else 1.0 - fx
+                    idx.append((iz + dz) * (h * w) + (iy + dy) * w + (ix + dx))
+                    wts.append(wx * wy * wz)
+        idx = np.concatenate(idx)
+        wts = np.concatenate(wts)
+        for ch in range(c):
+            contrib = np.tile(g_feat[sel, g * c + ch], 8) * wts
+            g_grids[g, ch] += np.bincount(idx, weights=contrib, minlength=d * h * w).reshape(d, h, w)
+    return sq, g_grids, g_w1, g_w2, g_w3
+
+
+def recon_loss_and_grads_threaded(prm: Params, coords, targets, pool, parts: int):
+    """recon_loss_and_grads over `parts` batch slices on a thread pool (numpy releases the GIL
+    in its kernels); partial sums added in slice order.  Same arithmetic per element; the batch
+    sums associate differently (CPU-baseline timing only -- parity uses the serial oracle)."""
+    targets = np.asarray(targets, dtype=prm.dtype).ravel()
+    coords = np.atleast_2d(np.asarray(coords, dtype=prm.dtype))
+    n = targets.size
+    futs = [pool.submit(_recon_partial, prm, coords[a:b], targets[a:b], n) for a, b in _chunks(n, parts)]
+    res = [f.result() for f in futs]
+    sq = np.concatenate([r[0] for r in res])
+    g_grids = res[0][1]
+    for r in res[1:]:
+        g_grids += r[1]
+    grads = {"grids": g_grids.astype(prm.dtype), "w1": sum(r[2] for r in res), "w2": sum(r[3] for r in res),
+             "w3": sum(r[4] for r in res)}
+    return float(np.mean(sq, dtype=np.float64)), sq, grads
+
+
+def density_loss_and_grads_threaded(prm: Params, coords, errors, pool, parts: int):
+    """density_loss_and_grads (optim.py:158-200) in three phases over batch slices: per-slice
+    rho, the global statistics (serial, O(N)), per-slice transform-gradient sums."""
+    x = np.atleast_2d(np.asarray(coords, dtype=np.float64))
+    errors = np.asarray(errors, dtype=np.float64).ravel()
+    p = prm.p
+    sl = _chunks(len(x), parts)
+    terms = [f.result() for f in [pool.submit(density_terms, prm.transforms, x[a:b], p) for a, b in sl]]
+    rho = np.concatenate([t[3] for t in terms])
+    det = terms[0][1]
+    total = rho.sum()
+    rho_s = normalize_density(rho)
+    star = warped_target(rho_s, errors, float(errors.mean()))
+    loss = kl_loss(rho_s, star)
+    n = rho.size
+    d_s = (np.log(rho_s + DENS_EPS) - np.log(star) + rho_s / (rho_s + DENS_EPS)) / n
+    d_rho = (d_s - (d_s * rho_s).sum()) / total
+    a = np.asarray(prm.transforms, dtype=np.float64)[:, :3, :3]
+    cof = np.stack([np.cross(a[:, 1], a[:, 2]), np.cross(a[:, 2], a[:, 0]), np.cross(a[:, 0], a[:, 1])], axis=1)
+
+    def part(k):
+        (lo, hi), (local, _, bump, _) = sl[k], terms[k]
+        with np.errstate(over="ignore", invalid="ignore"):
+            lpow = local * (local * local) ** (p - 1)
+        lpow = np.where(bump[:, :, None] > 0, lpow, 0.0)
+        wgt = d_rho[None, lo:hi] * bump
+        s = np.abs(det)[:, None] * wgt
+        return (wgt.sum(axis=1), np.einsum("mn,mnr,nc->mrc", s, lpow, x[lo:hi]),
+                np.einsum("mn,mnr->mr", s, lpow))
+
+    res = [f.result() for f in [pool.submit(part, k) for k in range(len(sl))]]
+    wsum = sum(r[0] for r in res)
+    g_a = (np.sign(det) * wsum)[:, None, None] * cof - 2.0 * p * sum(r[1] for r in res)
+    g_t = -2.0 * p * sum(r[2] for r in res)
+    g = np.zeros_like(prm.transforms)
+    g[:, :3, :3] = g_a.astype(prm.dtype)
+    g[:, :3, 3] = g_t.astype(prm.dtype)
+    return loss, {"transforms": g}
+
+
+def train_single_threaded(prm: Params, volume: np.ndarray, cfg: LoopConfig, threads: int, on_iteration=None):
+    """train_single (trainer.py:160-223) with each iteration's batch split over `threads` host
+    threads (the CPU baseline of bench.py --impl reference: the reference algorithm with all the
+    host threads it can use).  Plateau logic as the serial loop; returns the log."""
+    import concurrent.futures as cf
+    log = LoopLog()
+    rng = np.random.Generator(np.random.Philox(cfg.seed))
+    main = {"grids": prm.grids, "w1": prm.w1, "w2": prm.w2, "w3": prm.w3}
+    tfp = {"transforms": prm.transforms}
+    st_main, st_tf = AdamMoments(main), AdamMoments(tfp)
+    dhist: list = []
+    active = cfg.train_transforms
+    parts = max(1, threads)
+    with cf.ThreadPoolExecutor(max_workers=parts) as pool:
+        for it in range(cfg.iterations):
+            c64 = rng.uniform(-1.0, 1.0, size=(cfg.batch_size, 3))
+            tgt = np.concatenate([f.result() for f in [pool.submit(sample_volume, volume, c64[a:b])
+                                                       for a, b in _chunks(len(c64), parts)]]).astype(np.float32)
+            c32 = c64.astype(np.float32)
+            lr_loss, sq, grads = recon_loss_and_grads_threaded(prm, c32, tgt, pool, parts)
+            adam_update(main, grads, st_main, cfg.lr_main)
+            ld = None
+            if active and it >= cfg.delay_start:
+                if transform_should_stop(dhist, cfg, it):
+                    active = False
+                    log.transform_stop_iteration = it
+                else:
+                    ld, dg = density_loss_and_grads_threaded(prm, c32, np.asarray(sq, dtype=np.float64), pool,
+                                                             parts)
+                    adam_update(tfp, dg, st_tf, cfg.lr_transform)
+                    dhist.append(ld)
+            log.l_rec.append(lr_loss)
+            log.l_density.append(ld)
+            log.lr.append(cfg.lr_main)
+            log.iterations_run = it + 1
+            if on_iteration is not None:
+                on_iteration(it, prm)
+    return log

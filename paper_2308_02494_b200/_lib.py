@@ -101,15 +101,12 @@ SIGNATURES = {
     "apmg_train_log": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64),
                                  C.POINTER(_I64), C.POINTER(_I64), _P]),
     "apmg_train_destroy": (C.c_int, [_P]),
+    "apmg_train_moments": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "apmg_host_plateau_step": (C.c_int, [C.POINTER(_D), C.POINTER(_I64), C.POINTER(_I64), _I64, _D, _I64, _D]),
     "apmg_host_transform_stop": (C.c_int, [C.POINTER(_D), _I64, _I64, _D, _I64, _I64]),
     "apmg_host_pairwise_sum": (_D, [C.POINTER(_D), _I64]),
-    "apmg_debug_umma_gemm": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, _P, _P]),
-    "apmg_debug_tc_phases": (C.c_int, [_P]),
-    "apmg_debug_umma_bf16": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "apmg_debug_infer_phases": (C.c_int, [_P]),
     "apmg_debug_tc16_phases": (C.c_int, [_P]),
-    "apmg_peak_probe": (C.c_int, [_I32, _P, _I64, _I32, _P, _P]),
 }
 
 _lib = None
@@ -393,3 +390,28 @@ def download_into(*args, **kw):
 def upload_view(*args, **kw):
     with _stage_lock:
         return _upload_view_locked(*args, **kw)
+
+
+DEBUG_LIB_PATH = Path(__file__).resolve().parents[1] / "tools" / "libapmg_debug.so"
+DEBUG_SIGNATURES = {
+    "apmg_debug_umma_gemm": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "apmg_debug_umma_bf16": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "apmg_peak_probe": (C.c_int, [_I32, _P, _I64, _I32, _P, _P]),
+    "apmg_last_error": (C.c_char_p, []),
+}
+_debug = None
+
+
+def debug_lib():
+    """tools/libapmg_debug.so: tcgen05 self-tests and roofline probes (tests / tools only)."""
+    global _debug
+    if _debug is None:
+        if not DEBUG_LIB_PATH.exists():
+            raise ApmgLibraryError(f"{DEBUG_LIB_PATH} is not built; run `make`")
+        handle = C.CDLL(str(DEBUG_LIB_PATH))
+        for name, (res, args) in DEBUG_SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _debug = handle
+    return _debug

@@ -31,9 +31,33 @@ int num_sms();
 void* pool_alloc(size_t bytes);
 void pool_free(void* p, size_t bytes);
 void release_pool();
+size_t pool_cached_bytes();  // bytes held by the cache (free for reuse)
 // stream-ordered scratch (runtime.cu)
 void* stream_alloc(size_t bytes, cudaStream_t st);
 void stream_free(void* p, cudaStream_t st);
+// owns one stream-ordered scratch block: freed on every exit path of the launcher
+struct StreamScratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  StreamScratch() = default;
+  StreamScratch(size_t bytes, cudaStream_t s) : p(stream_alloc(bytes, s)), st(s) {}
+  StreamScratch(const StreamScratch&) = delete;
+  StreamScratch& operator=(const StreamScratch&) = delete;
+  StreamScratch& operator=(StreamScratch&& o) noexcept {
+    if (this != &o) {
+      stream_free(p, st);
+      p = o.p;
+      st = o.st;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  ~StreamScratch() { stream_free(p, st); }
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
 
 #define APMG_CUDA_TRY(expr)                                                                  \
   do {                                                                                       \

@@ -373,10 +373,12 @@ bool infer_tc_eligible(const FwdArgs<float>& a) {
 int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   // per-call scratch, stream-ordered: per-axis coordinate tables (lattice sweeps), the x-pair
   // grid copy (point lists), the per-CTA SSE partials
+  StreamScratch tab_s, gx_s, sse_s;
   float* tab = nullptr;
   if (a.mode == kFwdLattice) {
     const int64_t need = int64_t(a.bw) + a.bh + ceil_div(a.n, int64_t(a.bw) * a.bh);
-    tab = static_cast<float*>(stream_alloc(sizeof(float) * need, st));
+    tab_s = StreamScratch(sizeof(float) * need, st);
+    tab = tab_s.as<float>();
     APMG_ARG_CHECK(tab != nullptr, "out of device memory for the sweep tables");
     APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   }
@@ -388,7 +390,8 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const bool use_gx = a.mode != kFwdLattice && !(eg && eg[0] == '0');
   float4* gx = nullptr;
   if (use_gx) {
-    gx = static_cast<float4*>(stream_alloc(sizeof(float4) * cells, st));
+    gx_s = StreamScratch(sizeof(float4) * cells, st);
+    gx = gx_s.as<float4>();
     APMG_ARG_CHECK(gx != nullptr, "out of device memory for the x-pair grid copy");
     APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(cells, 8), 256, 0, st,
                 reinterpret_cast<const float2*>(a.md.grid), gx, cells);
@@ -407,19 +410,16 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   b.md.gridx = gx;
   const bool sse = a.mode == kFwdLattice && a.truth;
   if (sse) {
-    b.sse_part = static_cast<double*>(stream_alloc(sizeof(double) * grid, st));
+    sse_s = StreamScratch(sizeof(double) * grid, st);
+    b.sse_part = sse_s.as<double>();
     APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
   }
   if (a.mode != kFwdLattice)
     APMG_LAUNCH("infer_points_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
   else
     APMG_LAUNCH("infer_lattice_tc", itc::k_infer_tc, grid, itc::NTA, itc::SMEM_BYTES, st, b, tab);
-  int rc = APMG_OK;
-  if (sse) rc = launch_sse_finalize(b.sse_part, grid, a.sse, st);
-  stream_free(b.sse_part, st);
-  stream_free(gx, st);
-  stream_free(tab, st);
-  return rc;
+  if (sse) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
+  return APMG_OK;  // scratch released (stream-ordered) by the guards
 }
 
 }  // namespace apmg

@@ -48,8 +48,6 @@ int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
-int launch_recon_tc(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
-                    float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
 
 template <typename T, typename TE>
 int launch_density(T* tf, int M, int p, const T* x, const TE* err, int64_t n, double* loss, T* dtf, double* rho_total,

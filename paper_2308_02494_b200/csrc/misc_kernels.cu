@@ -488,9 +488,10 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
            c += int64_t(gridDim.x) * blockDim.x) {
         const float2 lo = d2[2 * c], hi = c > 0 ? d2[2 * c - 1] : make_float2(0.f, 0.f);
         const float g0 = lo.x + hi.x, g1 = lo.y + hi.y;
-        if (g0 == 0.f && g1 == 0.f) continue;
+        // clear both halves first: non-zero halves that cancel exactly still have to go
         if (lo.x != 0.f || lo.y != 0.f) d2[2 * c] = make_float2(0.f, 0.f);
         if (hi.x != 0.f || hi.y != 0.f) d2[2 * c - 1] = make_float2(0.f, 0.f);
+        if (g0 == 0.f && g1 == 0.f) continue;
         float2 pc = p2[c], mc = m2[c], vc = v2[c];
         adam_elem(pc.x, g0, mc.x, vc.x, lr_t, c1, c2);
         adam_elem(pc.y, g1, mc.y, vc.y, lr_t, c1, c2);

@@ -129,15 +129,15 @@ int launch_forward(const FwdArgs<T>& a, cudaStream_t st) {
   const int grid = int(min64(tiles, int64_t(num_sms()) * occ));
   FwdArgs<T> b = a;
   const bool sse = a.mode == kFwdLattice && a.truth;
+  StreamScratch sse_s;
   if (sse) {
-    b.sse_part = static_cast<double*>(stream_alloc(sizeof(double) * grid, st));
+    sse_s = StreamScratch(sizeof(double) * grid, st);
+    b.sse_part = sse_s.as<double>();
     APMG_ARG_CHECK(b.sse_part != nullptr, "out of device memory for the SSE partials");
   }
   APMG_LAUNCH("forward", k_forward<T>, grid, kTileThreads, smem, st, b);
-  int rc = APMG_OK;
-  if (sse) rc = launch_sse_finalize(b.sse_part, grid, a.sse, st);
-  stream_free(b.sse_part, st);
-  return rc;
+  if (sse) return launch_sse_finalize(b.sse_part, grid, a.sse, st);
+  return APMG_OK;  // scratch released (stream-ordered) by the guard
 }
 
 // ------------------------------------------------------------------ recon fwd+bwd
@@ -424,16 +424,11 @@ size_t recon_ws_bytes(int F, int64_t n) {
   return c.used + 256;
 }
 
-static bool use_tc16() {
-  const char* e16 = getenv("APMG_RECON16");
-  return !(e16 && e16[0] == '0');
-}
-
 int recon_tc16_grid(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), num_sms()))); }
 
 bool recon_uses_tc16(const apmg_model& m) {
   if (m.dtype != APMG_F32) return false;
-  return use_tc16() && recon_tc_eligible(make_model_dev<float>(m));
+  return recon_tc_eligible(make_model_dev<float>(m));
 }
 
 template <typename T>
@@ -455,17 +450,11 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
   }
   bool done = false;
   if constexpr (sizeof(T) == 4) {
-    if (md.grad_pairs) APMG_ARG_CHECK(recon_tc_eligible(md) && use_tc16(), "x-pair gradients need the tc16 kernel");
-    if (md.dgrid_fx)
-      APMG_ARG_CHECK(!recon_tc_eligible(md) || use_tc16(), "deterministic gradients need the tc16 or SIMT kernel");
-    if (recon_tc_eligible(md)) {  // tensor-core MLP path (tcgen05 forward + mma.sync backward)
+    if (md.grad_pairs) APMG_ARG_CHECK(recon_tc_eligible(md), "x-pair gradients need the tc16 kernel");
+    APMG_ARG_CHECK(!md.rho_out || recon_tc_eligible(md), "the fused density pass needs the tc16 kernel");
+    if (recon_tc_eligible(md)) {  // flagship shape: the bf16x3 all-tcgen05 kernel
       grid = recon_tc16_grid(n);
-      APMG_ARG_CHECK(!md.rho_out || use_tc16(), "the fused density pass needs the tc16 kernel");
-      // default: bf16x3 all-tcgen05 kernel; APMG_RECON16=0 selects the tf32 / mma.sync one (A/B)
-      if (use_tc16())
-        rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
-      else
-        rc = launch_recon_tc(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
+      rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
       if (rc) return rc;
       done = true;
     }

@@ -121,7 +121,6 @@ struct Args {
   const TrainCtl* ctl;
   int aggregate;
   int stamps;
-  int skip;  // APMG_TC_SKIP (timing experiments only, wrong results): 1 = no scatter, 2 = no gathers
 };
 
 __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX, float* sT, int tid) {
@@ -140,7 +139,6 @@ __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX
 template <bool FX>
 __device__ __forceinline__ void scatter_pairs(const ModelDev<float>& md, const Args& a, const float* GF,
                                               uint32_t tmem_cache, int q0, int q1, int cnt, int warp, int lane) {
-  if (a.skip & 1) return;
 #pragma unroll
   for (int jq = 0; jq < 2; ++jq) {
     if (q1 <= 4 * jq || q0 >= 4 * jq + 4) continue;  // warp-uniform
@@ -317,7 +315,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
         const int vbase = inside ? ((m * md.D + iz[h]) * md.H + iy[h]) * md.W + ix[h] : -1;
         float f0 = 0.f, f1 = 0.f;
         {  // straight-line: outside pairs gather cell 0 and are zeroed afterwards
-          const bool use = inside && !(a.skip & 2);
+          const bool use = inside;
           const int vb = use ? vbase : 0;
           if (md.gridx)
             interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
@@ -679,6 +677,14 @@ extern "C" int apmg_debug_tc16_phases(long long* out) {
   return APMG_OK;
 }
 
+// the flagship shape (64 grids x 2 channels -> 128 features) runs this kernel; APMG_MLP=simt
+// forces the SIMT tile kernel (A/B tests)
+bool recon_tc_eligible(const ModelDev<float>& md) {
+  const char* e = getenv("APMG_MLP");
+  const bool tc_on = !(e && e[0] == 's');
+  return tc_on && md.F == 128 && md.C == 2 && md.M == 64;
+}
+
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl,
                       cudaStream_t st) {
@@ -694,8 +700,7 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
   const char* es = getenv("APMG_TC_STAMPS");
   // APMG_SCATTER_AGG: 0 plain REDs, 1 tree-reduced, 2 (default) leader-gather aggregation
   tc16::Args a{md, n, coords, targets, sq, dgrid, part_dw, part_loss, ctl, ea ? atoi(ea) : 2,
-               (es && es[0] == '1') ? 1 : 0, 0};
-  if (const char* sk = getenv("APMG_TC_SKIP")) a.skip = atoi(sk);
+               (es && es[0] == '1') ? 1 : 0};
   if (md.dgrid_fx) a.aggregate = 2;  // the fixed-point (deterministic) scatter lives in the gather variant
   if (md.dgrid_fx)
     APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<true>, grid, tc16::NT, tc16::SMEM_BYTES, st, a);

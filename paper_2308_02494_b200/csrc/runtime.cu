@@ -113,6 +113,13 @@ void pool_free(void* p, size_t bytes) {
   g_pool.emplace(bytes, p);
 }
 
+size_t pool_cached_bytes() {
+  std::lock_guard<std::mutex> lk(g_pmu);
+  size_t t = 0;
+  for (auto& kv : g_pool) t += kv.first;
+  return t;
+}
+
 void release_pool() {
   std::lock_guard<std::mutex> lk(g_pmu);
   for (auto& kv : g_pool) cudaFree(kv.second);

@@ -292,11 +292,19 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   }
   {
     const char* eb = getenv("APMG_BRICKED");
-    // corner-replicated cells (APMG_CELLVOL=0: off) when 8x the volume stays within 16 GiB
+    // corner-replicated cells (APMG_CELLVOL=0: off) when 8x the volume stays within 16 GiB and
+    // within a quarter of the device memory that is free (cudaMemGetInfo) or already cached by
+    // the block pool, so the copy never crowds out the caller's own (torch) allocations
     const char* ec = getenv("APMG_CELLVOL");
     const size_t cell_bytes = size_t(32) * size_t(w > 1 ? w - 1 : 1) * size_t(h > 1 ? h - 1 : 1) *
                               size_t(d > 1 ? d - 1 : 1);
-    if (s->sort && !(ec && ec[0] == '0') && cell_bytes <= (size_t(16) << 30)) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    const size_t cell_budget = std::min(size_t(16) << 30, (free_b + pool_cached_bytes()) / 4);
+    if (s->sort && !(ec && ec[0] == '0') && cell_bytes <= cell_budget) {
       s->vol_bricked = static_cast<float*>(pool_alloc(cell_bytes));
       if (s->vol_bricked) {
         s->vol_bricked_bytes = cell_bytes;
@@ -504,6 +512,23 @@ extern "C" int apmg_train_status(apmg_train_state* s, int64_t* iterations_run, i
   APMG_CUDA_TRY(cudaStreamSynchronize(st));
   if (iterations_run) *iterations_run = c.iterations_run;
   if (finished) *finished = c.finished;
+  return APMG_OK;
+}
+
+// Adam state of the session (optim.py:38-44 AdamState: the m / v moments) -- checkpointing and
+// parity inspection.  Device-to-device copies on `stream`; main_m / main_v take the main group's
+// flat layout (apmg_main_layout, grids channel-last), tf_m / tf_v the (grids, 4, 4) transforms.
+// Any destination may be null.
+extern "C" int apmg_train_moments(apmg_train_state* s, void* main_m, void* main_v, void* tf_m, void* tf_v,
+                                  void* stream) {
+  APMG_ARG_CHECK(s != nullptr, "null state");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = s->shape.dtype == APMG_F32 ? 4 : 8;
+  const size_t mb = es * size_t(s->off[4]), tb = es * 16 * size_t(s->shape.grids);
+  if (main_m) APMG_CUDA_TRY(cudaMemcpyAsync(main_m, s->am, mb, cudaMemcpyDeviceToDevice, st));
+  if (main_v) APMG_CUDA_TRY(cudaMemcpyAsync(main_v, s->av, mb, cudaMemcpyDeviceToDevice, st));
+  if (tf_m) APMG_CUDA_TRY(cudaMemcpyAsync(tf_m, s->tm, tb, cudaMemcpyDeviceToDevice, st));
+  if (tf_v) APMG_CUDA_TRY(cudaMemcpyAsync(tf_v, s->tv, tb, cudaMemcpyDeviceToDevice, st));
   return APMG_OK;
 }
 

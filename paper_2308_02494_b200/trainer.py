@@ -81,6 +81,7 @@ class TrainLog:
     wall_seconds: float = 0.0
     setup_seconds: float = 0.0  # volume / parameter upload and session creation (train_single)
     setup_ms: dict = field(default_factory=dict)  # its split (TrainSession.setup_ms)
+    loop_ms: float = 0.0  # device time of the iterations (CUDA events on the session's stream)
 
     def records(self):
         stop = self.transform_stop_iteration
@@ -154,6 +155,23 @@ def _bias_table(n: int) -> np.ndarray:
 # per-thread flag: sessions run from concurrent worker threads (train_decomposed workers > 1)
 # use plain launches -- a CUDA-graph capture must not overlap other threads' CUDA calls
 _concurrency = __import__("threading").local()
+
+# The library caches its large per-session blocks (the corner-replicated training volume, up to
+# a quarter of free device memory) so back-to-back sessions skip cudaMalloc / cudaFree.  A
+# standalone train_single hands them back to the device when it returns; train_decomposed holds
+# the cache across its bricks (hold_block_cache) and releases it at the end.
+_cache_holders = [0]
+
+
+class hold_block_cache:
+    def __enter__(self):
+        _cache_holders[0] += 1
+        return self
+
+    def __exit__(self, *exc):
+        _cache_holders[0] -= 1
+        if _cache_holders[0] == 0 and L._lib is not None:  # nothing cached before the library loads
+            L.lib().apmg_release_cached()
 
 
 class TrainSession:
@@ -263,6 +281,26 @@ class TrainSession:
         log.plateau_trigger_iterations = [int(v) for v in trig[:ntrig.value]]
         return log
 
+    def moments(self) -> dict:
+        """Adam state after the iterations run so far (optim.py:38-44): host arrays in the
+        reference's shapes -- {"grids" | "w1" | "w2" | "w3" | "transforms": (m, v)}."""
+        t = self._torch
+        mm, mv = L.zeros((self.off[4],), self.dt), L.zeros((self.off[4],), self.dt)
+        tm, tv = L.zeros(tuple(self.tf.shape), self.dt), L.zeros(tuple(self.tf.shape), self.dt)
+        L.check(L.lib().apmg_train_moments(self.state, L.ptr(mm), L.ptr(mv), L.ptr(tm), L.ptr(tv),
+                                           L.stream_handle()), "train_moments")
+        c, o = self.model.config, self.off
+        out = {}
+        for name, (a, b) in (("m", (mm, tm)), ("v", (mv, tv))):
+            g = a[o[0]:o[0] + self.model.grids.size].view(c.grids, *c.resolution, c.channels)
+            out.setdefault("grids", {})[name] = L.to_host(g.permute(0, 4, 1, 2, 3).contiguous())
+            for k, i in (("w1", 1), ("w2", 2), ("w3", 3)):
+                shp = getattr(self.model, k).shape
+                out.setdefault(k, {})[name] = L.to_host(a[o[i]:o[i] + int(np.prod(shp))]).reshape(shp)
+            out.setdefault("transforms", {})[name] = L.to_host(b).reshape(self.model.transforms.shape)
+        t.cuda.current_stream().synchronize()
+        return {k: (v["m"], v["v"]) for k, v in out.items()}
+
     def close(self) -> None:
         if self.state:
             L.lib().apmg_train_destroy(self.state)
@@ -288,6 +326,9 @@ def train_single(model: ApmgModel, volume: Volume, cfg: TrainConfig, on_iteratio
     t0 = time.perf_counter()
     sess = TrainSession(model, volume, cfg)
     setup = time.perf_counter() - t0  # apmg_train_create returns synchronised
+    tcuda = L.torch().cuda
+    ev0, ev1 = tcuda.Event(enable_timing=True), tcuda.Event(enable_timing=True)
+    ev0.record()
     try:
         if on_iteration is None:
             done = 0
@@ -308,13 +349,17 @@ def train_single(model: ApmgModel, volume: Volume, cfg: TrainConfig, on_iteratio
                 sess.push_params()
                 if finished:
                     break
+        ev1.record()
         sess.pull_params()
         log = sess.log()
     finally:
         sess.close()
+        if _cache_holders[0] == 0:
+            L.lib().apmg_release_cached()
     log.wall_seconds = time.perf_counter() - t0
     log.setup_seconds = setup
     log.setup_ms = {k: round(v, 2) for k, v in sess.setup_ms.items()}
+    log.loop_ms = float(ev0.elapsed_time(ev1))
     return model, log
 
 

@@ -372,16 +372,7 @@ def gen_render():
     np.savez_compressed(OUT / "render.npz", **out)
 
 
-if __name__ == "__main__":
-    which = sys.argv[1:] or ["encode_forward", "recon", "density", "adam", "philox", "volume",
-                             "train_small", "hash_decomp", "psnr", "train_c1"]
-    for name in which:
-        t0 = time.perf_counter()
-        globals()["gen_" + name]()
-        print(f"{name}: {time.perf_counter() - t0:.1f}s", flush=True)
-
-
-def _c1_run(iters, delay, pert):
+def _c1_run(iters, delay, pert, batch=2 ** 14):
     """C1-shaped reference run; pert > 0 nudges a random half of the initial grid values by one
     ulp (the size of a different summation order) to measure the reference's own sensitivity."""
     vol = rvol.synth_volume((128, 128, 128), adaptivity_blobs())
@@ -391,7 +382,7 @@ def _c1_run(iters, delay, pert):
         rng = np.random.default_rng(pert)
         mask = rng.uniform(size=m.grids.shape) < 0.5
         m.grids[mask] = np.nextafter(m.grids[mask], np.float32(np.inf if pert % 2 else -np.inf))
-    cfg = rtrain.TrainConfig(iterations=iters, batch_size=2 ** 14, delay_start=delay, seed=0, plateau_enabled=False)
+    cfg = rtrain.TrainConfig(iterations=iters, batch_size=batch, delay_start=delay, seed=0, plateau_enabled=False)
     m, log = rtrain.train_single(m, vol, cfg)
     return rtrain.psnr(m, vol), log
 
@@ -438,3 +429,67 @@ def gen_crit5_ensemble():
            "frozen_psnr_unperturbed": run(0, False),
            "criterion_5_reference_gaps_seeds_0_1_2": [run(s, True) - run(s, False) for s in (0, 1, 2)]}
     (OUT / "crit5_ensemble.json").write_text(json.dumps(out, indent=1))
+
+
+
+def gen_to_local():
+    """model.py:179-182 to_local on sheared/translated transforms, f32 and f64, incl. points that
+    map outside [-1, 1]^3 (the exported apmg_to_local)."""
+    out = {}
+    rng = np.random.default_rng(77)
+    for tag, dt in (("f32", np.float32), ("f64", np.float64)):
+        for k in range(3):
+            tf = np.eye(4, dtype=dt)
+            tf[:3, :3] += rng.normal(scale=0.3, size=(3, 3)).astype(dt)
+            tf[:3, 3] = rng.normal(scale=0.4, size=3).astype(dt)
+            pts = rng.uniform(-1.3, 1.3, (1000 + 7 * k, 3)).astype(dt)
+            out[f"{tag}_{k}_tf"] = tf
+            out[f"{tag}_{k}_pts"] = pts
+            out[f"{tag}_{k}_local"] = rmodel.to_local(tf, pts)
+    np.savez_compressed(OUT / "to_local.npz", **out)
+
+C1_300_MEMBERS = (0, 1, 2, 3, 4, 5)
+
+
+def gen_train_c1_300_member(pert):
+    """BASELINE.md section 3's C1 parity configuration run by the reference (trainer.py:160-223):
+    300 iterations, delay_start 100 (hard stop at 240), batch 2^16, plateau off, seed 0.
+    ``pert`` 0 is the unperturbed run; 1..5 nudge a random half of the initial grid values by one
+    ulp (the reference's own sensitivity to rounding).  ~30 min per member on 2 cores; members
+    run as separate processes and are merged by gen_train_c1_300."""
+    import json
+    t0 = time.perf_counter()
+    p, log = _c1_run(300, 100, int(pert), batch=2 ** 16)
+    rec = {"pert": int(pert), "psnr": p, "wall_seconds": time.perf_counter() - t0,
+           "l_rec": [float(v) for v in log.l_rec],
+           "l_density": [None if v is None else float(v) for v in log.l_density],
+           "transform_stop_iteration": log.transform_stop_iteration}
+    (OUT / f"_c1_300_m{int(pert)}.json").write_text(json.dumps(rec))
+
+
+def gen_train_c1_300():
+    """Merge the per-member runs into train_c1_300.json (the committed fixture)."""
+    import json
+    mem = [json.loads((OUT / f"_c1_300_m{p}.json").read_text()) for p in C1_300_MEMBERS]
+    out = {"config": {"iterations": 300, "batch_size": 2 ** 16, "delay_start": 100, "seed": 0,
+                      "plateau_enabled": False, "volume": "128^3 adaptivity blobs",
+                      "model": "64 grids 32^3 x2, init_model(seed=0)",
+                      "perturbation": "one-ulp nudge of a random half of the initial grid values"},
+           "psnr_unperturbed": mem[0]["psnr"],
+           "psnr_perturbed": [m["psnr"] for m in mem[1:]],
+           "unperturbed_log": {k: mem[0][k] for k in ("l_rec", "l_density", "transform_stop_iteration")},
+           "wall_seconds": [m["wall_seconds"] for m in mem],
+           "generated_by": "tests/golden/make_golden.py train_c1_300_member <p> + train_c1_300 (reference, CPU)"}
+    (OUT / "train_c1_300.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["encode_forward", "recon", "density", "adam", "philox", "volume",
+                             "train_small", "hash_decomp", "psnr", "train_c1"]
+    if which[0] == "train_c1_300_member":
+        gen_train_c1_300_member(which[1])
+        sys.exit(0)
+    for name in which:
+        t0 = time.perf_counter()
+        globals()["gen_" + name]()
+        print(f"{name}: {time.perf_counter() - t0:.1f}s", flush=True)

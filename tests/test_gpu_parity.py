@@ -706,3 +706,31 @@ def test_fused_density_pass_matches_separate(monkeypatch):
     assert np.isfinite(out[1][1][:4]).all() and np.array_equal(np.isnan(out[1][1]), np.isnan(out[0][1]))
     np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5, equal_nan=True)
     np.testing.assert_allclose(out[1][0], out[0][0], rtol=0, atol=1e-5)
+
+
+@pytest.mark.parametrize("tag", ["f32_0", "f32_1", "f32_2", "f64_0", "f64_1", "f64_2"])
+def test_to_local_export_bit_exact(golden, tag):
+    """The exported apmg_to_local (model.py:179-182 to_local) vs the reference's own outputs."""
+    g = golden("to_local")
+    out = PM.to_local(g[tag + "_tf"], g[tag + "_pts"])
+    assert out.dtype == g[tag + "_local"].dtype
+    assert np.array_equal(out, g[tag + "_local"])
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 28), (1, 24, 20), (24, 1, 20), (24, 20, 1)])
+def test_cell_volume_sampler_matches_row_major(monkeypatch, dims):
+    """The default training target sampler (corner-replicated cells, k_cell_volume +
+    k_sample_sorted_cells) vs the row-major fp64 sampler (volume.py:147-199) on the same sorted
+    batch: the first iteration's l_rec is bit-equal (deterministic mode: fixed bucket order),
+    including volumes with a size-1 axis (the collapsed strides)."""
+    vol = PV.synth_volume(dims, C1_BLOBS)
+    out = []
+    for cellvol, bricked in (("1", "1"), ("0", "0")):
+        monkeypatch.setenv("APMG_CELLVOL", cellvol)
+        monkeypatch.setenv("APMG_BRICKED", bricked)
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(8, 8, 8)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=2, batch_size=1 << 14, delay_start=0, seed=3, plateau_enabled=False,
+                            transform_hard_stop_fraction=1.0, deterministic=True)
+        out.append(P.train_single(m, vol, cfg)[1].l_rec)
+    assert out[0] == out[1], out

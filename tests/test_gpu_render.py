@@ -253,7 +253,7 @@ def test_decomposed_training_and_render_reproducible(tmp_path, monkeypatch):
         bricks = b"".join((tmp_path / tag / f"brick_{i:04d}.apmg").read_bytes() for i in range(8))
         man = json.loads((tmp_path / tag / "manifest.json").read_text())
         for b in man["bricks"]:
-            b["train_seconds"] = 0.0
+            b["train_seconds"] = b["loop_ms"] = 0.0
         field = P.DecomposedField.load(tmp_path / tag / "manifest.json")
         img = PR.render_frame(field, PR.Camera(eye=(0.3, 0.2, 2.8), look_at=(0, 0, 0), width=10, height=8),
                               PR.TransferFunction(), PR.RenderConfig(samples_per_ray=12))

@@ -18,7 +18,7 @@ def run(mode, M, K, N, split3, seed=0):
     ref = A.astype(np.float64) @ B.astype(np.float64)
     d = L.zeros((M, N), np.float32)
     a_d, b_d = L.to_device(A), L.to_device(B)
-    L.check(L.lib().apmg_debug_umma_bf16(mode, M, K, N, split3, L.ptr(a_d), L.ptr(b_d), L.ptr(d),
+    L.check(L.debug_lib().apmg_debug_umma_bf16(mode, M, K, N, split3, L.ptr(a_d), L.ptr(b_d), L.ptr(d),
                                          L.stream_handle()), "umma_bf16")
     got = L.to_host(d).astype(np.float64)
     return float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))

@@ -35,6 +35,19 @@ def test_library_exports_every_header_symbol():
     assert lib.apmg_version().startswith(b"apmg-b200")
 
 
+def test_libraries_resolve_every_symbol():
+    """No undefined library-internal symbol (a dropped source file shows up here, not on the GPU
+    box); the tools' debug library (self-tests, peak probes) loads separately."""
+    import subprocess
+    for path in (L.LIB_PATH, L.DEBUG_LIB_PATH):
+        und = subprocess.run(["nm", "-D", "--undefined-only", str(path)], capture_output=True, text=True).stdout
+        assert "apmg" not in und, und
+    dbg = L.debug_lib()
+    for s in L.DEBUG_SIGNATURES:
+        assert hasattr(dbg, s), s
+    assert not hasattr(L.lib(), "apmg_peak_probe")  # probes and self-tests stay out of the product library
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", str(L.LIB_PATH)], capture_output=True, text=True).stdout

@@ -172,3 +172,29 @@ def test_hash_and_decomposed_forward(golden):
     assert np.array_equal(out, g["dec_out"])
     p = O.psnr(lambda q: O.decomposed_forward(models, counts, scale, offset, q), g["dec_vol"])
     assert p == pytest.approx(float(g["dec_psnr"]), abs=1e-9)
+
+
+@pytest.mark.parametrize("tag", ["f32_0", "f32_1", "f32_2", "f64_0", "f64_1", "f64_2"])
+def test_to_local_bit_exact(golden, tag):
+    """oracle.grid_local vs the reference's to_local (model.py:179-182), incl. einsum's
+    dtype-dependent summation order."""
+    g = golden("to_local")
+    assert np.array_equal(O.grid_local(g[tag + "_tf"], g[tag + "_pts"]), g[tag + "_local"])
+
+
+def test_threaded_cpu_baseline_matches_serial_oracle():
+    """The bench's reference arm (oracle.train_single_threaded: batch slices on host threads)
+    takes the same training steps as the serial restatement, up to the association of the
+    batch sums."""
+    prm = O.init_params(8, 2, (8, 8, 8), seed=1, vmin=0.0, vmax=1.0)
+    prm.transforms[:, :3, :3] += np.random.default_rng(2).normal(scale=0.1, size=(8, 3, 3)).astype(np.float32)
+    vol = O.synth_volume((20, 18, 16), [((0.1, -0.2, 0.3), (0.4, 0.3, 0.5), 1.0)])
+    cfg = O.LoopConfig(iterations=3, batch_size=3000, delay_start=1, transform_hard_stop_fraction=1.0,
+                       plateau_enabled=False, seed=4)
+    a, b = prm.copy(), prm.copy()
+    la = O.train_single(a, vol, cfg)
+    lb = O.train_single_threaded(b, vol, cfg, threads=3)
+    np.testing.assert_allclose(lb.l_rec, la.l_rec, rtol=1e-6)
+    np.testing.assert_allclose([v or 0.0 for v in lb.l_density], [v or 0.0 for v in la.l_density], rtol=1e-6)
+    for k in ("grids", "w1", "w2", "w3", "transforms"):
+        np.testing.assert_allclose(getattr(b, k), getattr(a, k), rtol=0, atol=2e-5)

@@ -18,13 +18,13 @@ def probe(kind, table, nbytes, iters):
     work = C.c_double()
     st = L.stream_handle()
     for _ in range(2):
-        L.check(L.lib().apmg_peak_probe(kind, L.ptr(table), nbytes, iters, C.byref(work), st), "probe")
+        L.check(L.debug_lib().apmg_peak_probe(kind, L.ptr(table), nbytes, iters, C.byref(work), st), "probe")
     best = float("inf")
     s = torch.cuda.current_stream()
     for _ in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        L.check(L.lib().apmg_peak_probe(kind, L.ptr(table), nbytes, iters, C.byref(work), st), "probe")
+        L.check(L.debug_lib().apmg_peak_probe(kind, L.ptr(table), nbytes, iters, C.byref(work), st), "probe")
         e1.record(s)
         e1.synchronize()
         best = min(best, e0.elapsed_time(e1) * 1e-3)
