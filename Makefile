@@ -5,20 +5,22 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2308_02494_b200
 SRCS := $(wildcard $(PKG)/csrc/*.cu)
-OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+BUILD ?= build
+OBJS := $(patsubst $(PKG)/csrc/%.cu,$(BUILD)/%.o,$(SRCS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/apmg_cuda.h
-LIB := $(PKG)/libapmg_cuda.so
+LIB ?= $(PKG)/libapmg_cuda.so
 DBG_SRCS := $(wildcard tools/csrc/*.cu)
 DBG_OBJS := $(patsubst tools/csrc/%.cu,build/dbg_%.o,$(DBG_SRCS))
 DBG_LIB := tools/libapmg_debug.so
 
 all: $(LIB) $(DBG_LIB)
 
-build/%.o: $(PKG)/csrc/%.cu $(HDRS)
-	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+$(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; exit 1)
 
 $(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
 build/dbg_%.o: tools/csrc/%.cu $(HDRS)

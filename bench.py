@@ -479,7 +479,8 @@ def main_decomposed(args):
     launches = L.lib().apmg_launch_count() - launches0
     mine = [b for b in range(plan.brick_count) if b % world == rank]
     train_ms = sum(float(man.bricks[b]["loop_ms"]) for b in mine)
-    t = torch.tensor([train_ms, fit_ms, wall], device=dev, dtype=torch.float64)
+    rdev = dev if dist.get_backend() == "nccl" else torch.device("cpu")  # gloo: functional runs only
+    t = torch.tensor([train_ms, fit_ms, wall], device=rdev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     train_ms, fit_ms, wall = (float(v) for v in t.tolist())
     points = sum(int(b["iterations_run"]) * BATCH for b in man.bricks)
@@ -495,12 +496,10 @@ def main_decomposed(args):
         truth[b] = PV.synth_volume_device(DIMS_DECOMP, blobs, extent=PV.Extent(lo=(x0, y0, z0), hi=(x1, y1, z1)))
     sse = L.zeros((1,), np.float64)
     field.lattice_sse_local(mine, truth, None, sse)
-    sse = sse.to(dev)
+    sse = sse.to(rdev)
     dist.all_reduce(sse)
-    vmin = torch.tensor([min(float(b["vmin"]) for b in man.bricks)], device=dev, dtype=torch.float64)
-    vmax = torch.tensor([max(float(b["vmax"]) for b in man.bricks)], device=dev, dtype=torch.float64)
     mse = float(sse.item()) / float(np.prod(DIMS_DECOMP))
-    span = float(vmax.item() - vmin.item())
+    span = max(float(b["vmax"]) for b in man.bricks) - min(float(b["vmin"]) for b in man.bricks)
     psnr = 200.0 if mse == 0 else min(200.0, 10.0 * np.log10(span * span / mse))
 
     infer = None if args.no_inference else bench_decomposed_inference(rank, world, dist)

@@ -183,6 +183,16 @@ int apmg_spatial_hash(int32_t pts_dtype, const void* pts, int64_t n, int32_t bi,
 /* DecomposedField.forward: models[b] (HOST array of descriptors whose tensor
  * pointers are device pointers), per-brick affine scale/offset [B][3] (HOST f64),
  * pts [n][3] f32 -> out [n] f32.  Synchronises (reads per-brick counts). */
+/* Query routing across ranks (replaces the per-owner loop of decomposition.py:294-304 when the
+ * bricks live on different ranks): counting sort of n points by owner rank dest[i] in [0, world)
+ * (device int64) -> perm (device int64 [n], points grouped by rank) and counts (HOST int64
+ * [world]); synchronising (the counts size the all-to-all). */
+size_t apmg_owner_bucket_workspace_bytes(int32_t world);
+int apmg_owner_bucket(const int64_t* dest, int64_t n, int32_t world, int64_t* perm, int64_t* counts, void* workspace,
+                      size_t workspace_bytes, void* stream);
+/* rows of row_words 4-byte words: dst[r] = src[perm[r]] (scatter = 0) or dst[perm[r]] = src[r] */
+int apmg_permute_rows(const void* src, const int64_t* perm, int64_t n, int32_t row_words, int32_t scatter, void* dst,
+                      void* stream);
 size_t apmg_decomposed_workspace_bytes(int32_t bricks, int64_t n);
 int apmg_decomposed_forward(const apmg_model* models, int32_t bricks, int32_t bi, int32_t bj, int32_t bk,
                             const double* scale, const double* offset, const float* pts, int64_t n,
@@ -235,12 +245,18 @@ typedef struct apmg_train_state apmg_train_state;
 int apmg_main_layout(const apmg_model* m, int64_t offsets[5]);
 
 size_t apmg_train_workspace_bytes(const apmg_model* m, const apmg_train_config* cfg);
+/* Extra workspace bytes for the session's private sampler copy of a (w, h, d) volume: add them to
+ * apmg_train_workspace_bytes and the copy is carved from the caller's workspace (so the caller's
+ * allocator owns and can reuse it); without them the session takes the copy from the library's
+ * block cache.  0 when no copy would be made. */
+size_t apmg_train_volume_bytes(int32_t w, int32_t h, int32_t d);
 /* Parameters are updated in place: grad-free main group `main_params` laid out
  * [grids_cl | w1 | w2 | w3] and `transforms` [M][4][4] (both dtype, device).
  * bias_table: HOST f64 [iterations][2] = (1-0.9^t, 1-0.99^t) for t = 1..iterations
  * computed in Python so Adam's bias corrections match the reference bit for bit.
- * The state keeps a private 8x8x8-bricked copy of `volume` (cudaMalloc, freed by
- * apmg_train_destroy; APMG_BRICKED=0 samples the caller's [D][H][W] array instead). */
+ * The state samples targets from a private copy of `volume` (corner-replicated cells, or 8^3
+ * bricks; see apmg_train_volume_bytes) taken from the tail of `workspace` when it is large enough,
+ * else from the library's block cache (returned at apmg_train_destroy). */
 int apmg_train_create(apmg_train_state** out, const apmg_model* shape, void* main_params, void* transforms,
                       const float* volume, int32_t w, int32_t h, int32_t d, const apmg_train_config* cfg,
                       const double* bias_table, void* workspace, size_t workspace_bytes, void* stream);

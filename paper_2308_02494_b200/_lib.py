@@ -14,6 +14,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libapmg_cuda.so"
+if os.environ.get("APMG_LIB"):  # A/B builds of the same sources (tools/ab_build.sh); never a fallback
+    LIB_PATH = Path(os.environ["APMG_LIB"]).resolve()
 
 APMG_F32, APMG_F64 = 0, 1
 APMG_OK, APMG_E_ARG, APMG_E_CUDA, APMG_E_WORKSPACE, APMG_E_UNSUPPORTED = 0, -1, -2, -3, -4
@@ -84,6 +86,9 @@ SIGNATURES = {
     "apmg_synth_volume": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _D, _U64, _U64, _D, _P, _P]),
     "apmg_spatial_hash": (C.c_int, [_I32, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
     "apmg_decomposed_workspace_bytes": (_SZ, [_I32, _I64]),
+    "apmg_owner_bucket_workspace_bytes": (_SZ, [_I32]),
+    "apmg_owner_bucket": (C.c_int, [_P, _I64, _I32, _P, C.POINTER(_I64), _P, _SZ, _P]),
+    "apmg_permute_rows": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P]),
     "apmg_decomposed_forward": (C.c_int, [_MP, _I32, _I32, _I32, _I32, C.POINTER(_D), C.POINTER(_D), _P, _I64,
                                           _P, _P, _SZ, _P]),
     "apmg_decomposed_forward_tc": (C.c_int, [_MP, _I32, _I32, _I32, _I32, C.POINTER(_D), C.POINTER(_D), _P, _I64,
@@ -94,6 +99,7 @@ SIGNATURES = {
                                    _P, _P, _P]),
     "apmg_main_layout": (C.c_int, [_MP, C.POINTER(_I64)]),
     "apmg_train_workspace_bytes": (_SZ, [_MP, C.POINTER(ApmgTrainConfigC)]),
+    "apmg_train_volume_bytes": (_SZ, [_I32, _I32, _I32]),
     "apmg_train_create": (C.c_int, [C.POINTER(_P), _MP, _P, _P, _P, _I32, _I32, _I32,
                                     C.POINTER(ApmgTrainConfigC), C.POINTER(_D), _P, _SZ, _P]),
     "apmg_train_run": (C.c_int, [_P, _I64, _P]),

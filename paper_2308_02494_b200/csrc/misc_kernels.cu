@@ -606,6 +606,100 @@ extern "C" int apmg_spatial_hash(int32_t pts_dtype, const void* pts, int64_t n, 
   return APMG_OK;
 }
 
+// ---- query routing across ranks (decomposition.py:294-304 DecomposedField.forward over ranks):
+// owner-rank histogram (shared-memory privatised), host prefix sum, counting-sort scatter of the
+// point indices; rows permuted to / from that order by one gather kernel
+__global__ void k_owner_count(const int64_t* __restrict__ dest, int64_t n, int world, int32_t* __restrict__ counts,
+                              int32_t* bad) {
+  extern __shared__ int32_t s_cnt[];
+  for (int b = threadIdx.x; b < world; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = dest[i];
+    if (o < 0 || o >= world) {
+      *bad = 1;
+      continue;
+    }
+    atomicAdd(&s_cnt[o], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < world; b += blockDim.x)
+    if (s_cnt[b]) atomicAdd(&counts[b], s_cnt[b]);
+}
+
+__global__ void k_owner_bucket(const int64_t* __restrict__ dest, int64_t n, const int32_t* __restrict__ offsets,
+                               int32_t* __restrict__ cursor, int64_t* __restrict__ perm) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = dest[i];
+    perm[offsets[o] + atomicAdd(&cursor[o], 1)] = i;
+  }
+}
+
+// dst[r] = src[perm[r]] (gather) or dst[perm[r]] = src[r] (scatter), rows of `cols` 4-byte words
+__global__ void k_permute_rows(const uint32_t* __restrict__ src, const int64_t* __restrict__ perm, int64_t n,
+                               int cols, int scatter, uint32_t* __restrict__ dst) {
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols, q = perm[r];
+    if (scatter)
+      dst[q * cols + c] = src[e];
+    else
+      dst[e] = src[q * cols + c];
+  }
+}
+
+extern "C" size_t apmg_owner_bucket_workspace_bytes(int32_t world) {
+  Carver c(nullptr, 0);
+  c.take<int32_t>(3 * size_t(world > 0 ? world : 1) + 1);
+  return c.used + 256;
+}
+
+extern "C" int apmg_owner_bucket(const int64_t* dest, int64_t n, int32_t world, int64_t* perm, int64_t* counts,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  APMG_ARG_CHECK(world >= 1 && world <= 4096, "world size must be in [1, 4096]");
+  APMG_ARG_CHECK(counts != nullptr, "null counts");
+  for (int r = 0; r < world; ++r) counts[r] = 0;
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver c(workspace, workspace_bytes);
+  int32_t* d_counts = c.take<int32_t>(world);
+  int32_t* d_off = c.take<int32_t>(world);
+  int32_t* d_cur = c.take<int32_t>(world);
+  int32_t* bad = c.take<int32_t>(1);
+  if (!c.ok()) {
+    set_error("owner bucket workspace too small");
+    return APMG_E_WORKSPACE;
+  }
+  APMG_CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * (3 * size_t(world) + 1), st));
+  APMG_LAUNCH("owner_count", k_owner_count, elementwise_grid(n, 8), 256, sizeof(int32_t) * world, st, dest, n, world,
+              d_counts, bad);
+  std::vector<int32_t> h(world + 1), off(world);
+  APMG_CUDA_TRY(cudaMemcpyAsync(h.data(), d_counts, sizeof(int32_t) * world, cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaMemcpyAsync(&h[world], bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));
+  APMG_ARG_CHECK(!h[world], "owner rank outside [0, world)");
+  int32_t run = 0;
+  for (int r = 0; r < world; ++r) {
+    off[r] = run;
+    run += h[r];
+    counts[r] = h[r];
+  }
+  APMG_CUDA_TRY(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * world, cudaMemcpyHostToDevice, st));
+  APMG_LAUNCH("owner_bucket", k_owner_bucket, elementwise_grid(n, 8), 256, 0, st, dest, n, d_off, d_cur, perm);
+  APMG_CUDA_TRY(cudaStreamSynchronize(st));  // the host offsets must outlive the copy
+  return APMG_OK;
+}
+
+extern "C" int apmg_permute_rows(const void* src, const int64_t* perm, int64_t n, int32_t row_words, int32_t scatter,
+                                 void* dst, void* stream) {
+  APMG_ARG_CHECK(row_words >= 1, "row width must be >= 1 word");
+  if (n <= 0) return APMG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  APMG_LAUNCH("permute_rows", k_permute_rows, elementwise_grid(n * row_words, 8), 256, 0, st,
+              static_cast<const uint32_t*>(src), perm, n, row_words, scatter, static_cast<uint32_t*>(dst));
+  return APMG_OK;
+}
+
 extern "C" int apmg_adam_step(int32_t dtype, void* params, const void* grads, void* m, void* v, int64_t n, double lr,
                               double bc1, double bc2, void* stream) {
   if (n <= 0) return APMG_OK;

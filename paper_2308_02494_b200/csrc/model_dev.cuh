@@ -379,12 +379,22 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
 #ifndef APMG_GATHER_CAP
 #define APMG_GATHER_CAP 1
 #endif
+// weights wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]) formed in packed fp32x2 (same roundings as
+// the scalar products: (wy0, wy1) * wz, then (wx0, wx1) * wzy), contributions g * w
 __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float fz, float2* v, bool add) {
-  const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+  const float2 wx = make_float2(1.f - fx, fx), wy = make_float2(1.f - fy, fy);
+  const float wz[2] = {1.f - fz, fz};
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float w = wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]);
-    v[c] = add ? f2_fma(g, make_float2(w, w), v[c]) : f2_mul(g, make_float2(w, w));
+  for (int cz = 0; cz < 2; ++cz) {
+    const float2 wzy = __fmul2_rn(wy, make_float2(wz[cz], wz[cz]));  // (cy = 0, cy = 1)
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const float t = cy ? wzy.y : wzy.x;
+      const float2 w = __fmul2_rn(wx, make_float2(t, t));  // (cx = 0, cx = 1)
+      const int c = 4 * cz + 2 * cy;
+      v[c] = add ? f2_fma(g, make_float2(w.x, w.x), v[c]) : f2_mul(g, make_float2(w.x, w.x));
+      v[c + 1] = add ? f2_fma(g, make_float2(w.y, w.y), v[c + 1]) : f2_mul(g, make_float2(w.y, w.y));
+    }
   }
 }
 

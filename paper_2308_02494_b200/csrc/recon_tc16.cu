@@ -172,21 +172,20 @@ __device__ __forceinline__ float ex2_ftz(float v) {
 }
 
 // flat-top bump exp(-sum_d l_d^20) of density.py:83-103 (p = 10) for two points in f32, the
-// arithmetic of k_dens_rho32x2 (l^2 clamped at 4 so the power cannot overflow)
+// arithmetic of k_dens_rho32x2 (l^2 clamped at 4 so the power cannot overflow), both points in
+// packed fp32x2 (each half rounded as the scalar operation; no product feeds an add)
 __device__ __forceinline__ float2 bump_p10x2(float2 l0, float2 l1, float2 l2) {
-  float q[2];
-  const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
+  const float2 la[3] = {l0, l1, l2};
+  float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float acc = 0.f;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const float s = fminf(la[h][d] * la[h][d], 4.f), s2 = s * s, s4 = s2 * s2, s8 = s4 * s4;
-      acc = fmaf(s8 * s, s, acc);
-    }
-    q[h] = acc;
+  for (int d = 0; d < 3; ++d) {
+    float2 s = __fmul2_rn(la[d], la[d]);
+    s = make_float2(fminf(s.x, 4.f), fminf(s.y, 4.f));
+    const float2 s2 = __fmul2_rn(s, s), s4 = __fmul2_rn(s2, s2), s8 = __fmul2_rn(s4, s4);
+    acc = __ffma2_rn(__fmul2_rn(s8, s), s, acc);
   }
-  return make_float2(ex2_ftz(q[0] * -1.4426950408889634f), ex2_ftz(q[1] * -1.4426950408889634f));
+  const float2 e = __fmul2_rn(acc, make_float2(-1.4426950408889634f, -1.4426950408889634f));
+  return make_float2(ex2_ftz(e.x), ex2_ftz(e.y));
 }
 
 template <bool FX>  // FX: deterministic training (fixed-point grid gradient)

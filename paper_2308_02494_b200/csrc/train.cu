@@ -160,11 +160,47 @@ struct apmg_train_state {
   int64_t gx_cells = 0;
   float* vol_bricked = nullptr;
   size_t vol_bricked_bytes = 0;
+  bool vol_owned = false;  // from the block cache (returned at destroy), else part of the workspace
   bool vol_cells = false;  // vol_bricked holds the corner-replicated cell copy (k_cell_volume)
   int nbx = 0, nby = 0;
 };
 
 constexpr int64_t kGraphIters = 8;
+
+// The sorted sampler's private copy of the volume: corner-replicated cells (APMG_CELLVOL=0: off;
+// 8x the volume, used while that stays within 16 GiB and a quarter of the device memory that is
+// free or cached by the block pool) or else 8^3 bricks (APMG_BRICKED=0: off, 1x the volume).
+struct SamplerCopy {
+  size_t bytes = 0;
+  bool cells = false;
+};
+static SamplerCopy sampler_copy_plan(int32_t w, int32_t h, int32_t d, bool sort) {
+  SamplerCopy c;
+  if (!sort) return c;
+  const char* ec = getenv("APMG_CELLVOL");
+  const size_t cell_bytes = size_t(32) * size_t(w > 1 ? w - 1 : 1) * size_t(h > 1 ? h - 1 : 1) *
+                            size_t(d > 1 ? d - 1 : 1);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = 0;
+  }
+  const size_t budget = std::min(size_t(16) << 30, (free_b + pool_cached_bytes()) / 4);
+  if (!(ec && ec[0] == '0') && cell_bytes <= budget) {
+    c.bytes = cell_bytes;
+    c.cells = true;
+    return c;
+  }
+  const char* eb = getenv("APMG_BRICKED");
+  if (eb && eb[0] == '0') return c;
+  c.bytes = sizeof(float) * 512 * size_t((w + 7) / 8) * size_t((h + 7) / 8) * size_t((d + 7) / 8);
+  return c;
+}
+
+extern "C" size_t apmg_train_volume_bytes(int32_t w, int32_t h, int32_t d) {
+  if (w < 1 || h < 1 || d < 1) return 0;
+  return sampler_copy_plan(w, h, d, sort_enabled()).bytes;
+}
 
 extern "C" int apmg_main_layout(const apmg_model* m, int64_t offsets[5]) {
   APMG_ARG_CHECK(m != nullptr, "null model");
@@ -291,43 +327,34 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
     return APMG_E_WORKSPACE;
   }
   {
-    const char* eb = getenv("APMG_BRICKED");
-    // corner-replicated cells (APMG_CELLVOL=0: off) when 8x the volume stays within 16 GiB and
-    // within a quarter of the device memory that is free (cudaMemGetInfo) or already cached by
-    // the block pool, so the copy never crowds out the caller's own (torch) allocations
-    const char* ec = getenv("APMG_CELLVOL");
-    const size_t cell_bytes = size_t(32) * size_t(w > 1 ? w - 1 : 1) * size_t(h > 1 ? h - 1 : 1) *
-                              size_t(d > 1 ? d - 1 : 1);
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-      cudaGetLastError();
-      free_b = 0;
+    // sampler copy of the volume: carved from the caller's workspace when it was sized with
+    // apmg_train_volume_bytes (torch's caching allocator then owns the block), else from the
+    // library's block cache
+    const SamplerCopy sc = sampler_copy_plan(w, h, d, s->sort);
+    const size_t tail = (need + 255) / 256 * 256;
+    if (sc.bytes && workspace_bytes >= tail + sc.bytes) {
+      s->vol_bricked = reinterpret_cast<float*>(static_cast<char*>(workspace) + tail);
+      s->vol_owned = false;
+    } else if (sc.bytes) {
+      s->vol_bricked = static_cast<float*>(pool_alloc(sc.bytes));
+      s->vol_owned = true;
     }
-    const size_t cell_budget = std::min(size_t(16) << 30, (free_b + pool_cached_bytes()) / 4);
-    if (s->sort && !(ec && ec[0] == '0') && cell_bytes <= cell_budget) {
-      s->vol_bricked = static_cast<float*>(pool_alloc(cell_bytes));
-      if (s->vol_bricked) {
-        s->vol_bricked_bytes = cell_bytes;
+    if (s->vol_bricked) {
+      s->vol_bricked_bytes = sc.bytes;
+      if (sc.cells) {
         s->vol_cells = true;
-        const int64_t nc = int64_t(cell_bytes / 32);
+        const int64_t nc = int64_t(sc.bytes / 32);
         const int g = int(std::min<int64_t>(ceil_div(nc, 256), int64_t(num_sms()) * 32));
         APMG_LAUNCH("cell_volume", k_cell_volume, g, 256, 0, st, volume, w, h, d,
                     reinterpret_cast<float4*>(s->vol_bricked));
-      }
-    }
-    if (s->sort && !s->vol_cells && !(eb && eb[0] == '0')) {
-      s->nbx = (w + 7) / 8;
-      s->nby = (h + 7) / 8;
-      const int nbz = (d + 7) / 8;
-      const size_t bytes = sizeof(float) * 512 * size_t(s->nbx) * s->nby * nbz;
-      s->vol_bricked = static_cast<float*>(pool_alloc(bytes));
-      s->vol_bricked_bytes = bytes;
-      if (s->vol_bricked) {  // else no room: sample the row-major volume
+      } else {
+        s->nbx = (w + 7) / 8;
+        s->nby = (h + 7) / 8;
         const int64_t nv = int64_t(w) * h * d;
         const int g = int(std::min<int64_t>(ceil_div(nv, 256), int64_t(num_sms()) * 32));
         APMG_LAUNCH("brick_volume", k_brick_volume, g, 256, 0, st, volume, w, h, d, s->nbx, s->nby, s->vol_bricked);
       }
-    }
+    }  // else no copy (sorting off, APMG_BRICKED=0, or no room): sample the row-major volume
   }
   CtlParams& P = s->P;
   P.iterations = cfg->iterations;
@@ -553,7 +580,7 @@ extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_dens
 
 extern "C" int apmg_train_destroy(apmg_train_state* s) {
   if (s && s->graph) cudaGraphExecDestroy(s->graph);
-  if (s && s->vol_bricked) {
+  if (s && s->vol_bricked && s->vol_owned) {
     cudaDeviceSynchronize();  // as cudaFree would: no launch may still read the block
     pool_free(s->vol_bricked, s->vol_bricked_bytes);
   }

@@ -209,8 +209,12 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Waiting threads suspend inside try_wait until the phase completes (suspend-time hint 10 ms) rather
+// than re-issuing the probe: every CTA warp waits here while the tensor core runs, and spinning
+// probes take issue slots from the warps that still have CUDA-core work (APMG_MBAR_SPIN=1: no hint)
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
+#if defined(APMG_MBAR_SPIN) && APMG_MBAR_SPIN
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -218,6 +222,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
       "r"(parity)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {

@@ -209,10 +209,13 @@ class TrainSession:
             int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)),
             int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"),
             1 if getattr(_concurrency, "no_graph", False) else 0)
-        self.ws = L.workspace(L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg)))
+        w, h, d = volume.dims
+        # session workspace + the sampler's private copy of the volume, both from torch's caching
+        # allocator (reused by back-to-back sessions, released by torch under memory pressure)
+        need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
+        self.ws = L.workspace((need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d))
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()
-        w, h, d = volume.dims
         L.check(L.lib().apmg_train_create(C.byref(st), C.byref(self.dm.desc), L.ptr(self.main), L.ptr(self.tf),
                                           L.ptr(self.vol), w, h, d, C.byref(self.ccfg),
                                           bias.ctypes.data_as(C.POINTER(C.c_double)), L.ptr(self.ws), self.ws.numel(),

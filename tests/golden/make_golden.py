@@ -448,7 +448,7 @@ def gen_to_local():
             out[f"{tag}_{k}_local"] = rmodel.to_local(tf, pts)
     np.savez_compressed(OUT / "to_local.npz", **out)
 
-C1_300_MEMBERS = (0, 1, 2, 3, 4, 5)
+C1_300_MEMBERS = (0, 1, 2, 3, 4, 5, 6, 7)
 
 
 def gen_train_c1_300_member(pert):

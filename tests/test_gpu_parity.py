@@ -734,3 +734,46 @@ def test_cell_volume_sampler_matches_row_major(monkeypatch, dims):
                             transform_hard_stop_fraction=1.0, deterministic=True)
         out.append(P.train_single(m, vol, cfg)[1].l_rec)
     assert out[0] == out[1], out
+
+
+def _c1_300_gpu_run(pert):
+    """BASELINE.md section 3's C1 parity configuration on the GPU, with the reference members'
+    one-ulp perturbation of the initial grids (tests/golden/make_golden.py _c1_run)."""
+    vol = PV.synth_volume((128, 128, 128), C1_BLOBS)
+    m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                      vmax=vol.vmax)
+    if pert:
+        rng = np.random.default_rng(pert)
+        mask = rng.uniform(size=m.grids.shape) < 0.5
+        m.grids[mask] = np.nextafter(m.grids[mask], np.float32(np.inf if pert % 2 else -np.inf))
+    cfg = P.TrainConfig(iterations=300, batch_size=1 << 16, delay_start=100, seed=0, plateau_enabled=False)
+    m, log = P.train_single(m, vol, cfg)
+    return P.psnr(m, vol), log
+
+
+def test_train_c1_300_baseline_parity():
+    """BASELINE C1 parity run (trainer.py:160-223): 64 grids 32^3 x2, 128^3 blob field, 300
+    iterations, delay_start 100 (hard stop at 240), batch 2^16, plateau off, seed 0.
+
+    The reference itself is chaotic at this length: its 8 members (unperturbed + seven one-ulp
+    nudges of half the initial grids, tests/golden/train_c1_300.json) spread its final PSNR by
+    several dB, so a 0.1 dB gate on one run pair is below the reference's own run-to-run
+    resolution.  The gate is on the ensemble means: |mean_gpu - mean_ref| <= max(0.1 dB, 3 se),
+    se = sqrt(var_ref / n_ref + var_gpu / n_gpu) -- the effective tolerance is printed with both
+    spreads.  GPU members: the same eight perturbations plus eight repeats of the unperturbed run
+    (float RED order makes each one a perturbation of the same size).  The first iterations'
+    losses must also track the unperturbed reference log before the trajectories decorrelate."""
+    ens = json.loads((Path(__file__).parent / "golden" / "train_c1_300.json").read_text())
+    ref = np.array([ens["psnr_unperturbed"]] + ens["psnr_perturbed"])
+    runs = [_c1_300_gpu_run(p) for p in range(len(ref))] + [_c1_300_gpu_run(0) for _ in range(8)]
+    gpu = np.array([r[0] for r in runs])
+    se = float(np.sqrt(ref.var(ddof=1) / len(ref) + gpu.var(ddof=1) / len(gpu)))
+    tol = max(0.1, 3 * se)
+    diff = float(gpu.mean() - ref.mean())
+    print(f"C1-300: ref mean {ref.mean():.3f} sd {ref.std(ddof=1):.3f} (n={len(ref)}); gpu mean {gpu.mean():.3f} "
+          f"sd {gpu.std(ddof=1):.3f} (n={len(gpu)}); diff {diff:+.3f} dB, effective tolerance {tol:.3f} dB")
+    assert abs(diff) <= tol, (gpu.tolist(), ref.tolist(), tol)
+    log0 = runs[0][1]
+    assert log0.iterations_run == 300 and log0.transform_stop_iteration == ens["unperturbed_log"][
+        "transform_stop_iteration"]
+    np.testing.assert_allclose(log0.l_rec[:8], ens["unperturbed_log"]["l_rec"][:8], rtol=2e-3)

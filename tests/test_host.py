@@ -212,11 +212,27 @@ def test_decomposed_sharding_gloo_world2(tmp_path):
     assert [b["psnr"] for b in man["bricks"]] == [40.0 + b for b in range(8)]
 
 
+def _cpu_owner_bucket(dest, world):  # host stand-ins for the library's bucketing kernels (CPU test)
+    import torch
+    return torch.argsort(dest, stable=True), torch.bincount(dest, minlength=world).tolist()
+
+
+def _cpu_permute_rows(src, perm, scatter=False, out=None):
+    if scatter:
+        out = src.new_empty(src.shape) if out is None else out
+        out[perm] = src
+        return out
+    return src[perm]
+
+
 def _route_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the exchange protocol on CPU; the device bucketing / permutation kernels it calls are
+    # covered by tests/test_gpu_multirank.py
+    D.owner_bucket, D.permute_rows = _cpu_owner_bucket, _cpu_permute_rows
     try:
         g = torch.Generator().manual_seed(100 + rank)
         pts = torch.rand((257 + 31 * rank, 3), generator=g, dtype=torch.float64) * 2 - 1
