@@ -46,10 +46,6 @@ int elementwise_grid(int64_t n, int per_sm);
 int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st);
 // gridx[c] = (grid[c], grid[c + 1]) over the flat two-channel cells (misc_kernels.cu)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);
-// two-group ping-pong variant of the same step (recon_pp.cu; APMG_RECON=pp)
-bool recon_pp_selected();
-int launch_recon_pp(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
-                    float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
 

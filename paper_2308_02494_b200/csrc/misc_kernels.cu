@@ -662,10 +662,10 @@ extern "C" int apmg_owner_bucket(const int64_t* dest, int64_t n, int32_t world, 
   if (n <= 0) return APMG_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carver c(workspace, workspace_bytes);
-  int32_t* d_counts = c.take<int32_t>(world);
-  int32_t* d_off = c.take<int32_t>(world);
-  int32_t* d_cur = c.take<int32_t>(world);
-  int32_t* bad = c.take<int32_t>(1);
+  int32_t* d_counts = c.take<int32_t>(3 * size_t(world) + 1);  // counts | offsets | cursors | flag
+  int32_t* d_off = d_counts + world;
+  int32_t* d_cur = d_off + world;
+  int32_t* bad = d_cur + world;
   if (!c.ok()) {
     set_error("owner bucket workspace too small");
     return APMG_E_WORKSPACE;

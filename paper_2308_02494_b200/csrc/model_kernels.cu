@@ -454,8 +454,7 @@ int launch_recon(const ModelDev<T>& md, int64_t n, const T* coords, const T* tar
     APMG_ARG_CHECK(!md.rho_out || recon_tc_eligible(md), "the fused density pass needs the tc16 kernel");
     if (recon_tc_eligible(md)) {  // flagship shape: the bf16x3 all-tcgen05 kernel
       grid = recon_tc16_grid(n);
-      rc = recon_pp_selected() ? launch_recon_pp(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st)
-                               : launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
+      rc = launch_recon_tc16(md, n, coords, targets, sq, dgrid, part_dw, part_loss, grid, ctl, st);
       if (rc) return rc;
       done = true;
     }
