@@ -54,53 +54,76 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks + throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line).
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    The C2 timed region is ~40 ms, shorter than nvidia-smi's sampling loop, so the clocks are read
+    through NVML (the library nvidia-smi uses) by a thread polling every ~2 ms while the region
+    runs; nvidia-smi -lms 5 is the fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index: int):
         self.index = index
-        self.rows, self.proc = [], None
+        self.rows, self.max_mhz, self.source = [], None, None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-            t0 = time.time()
-            while not self.rows and time.time() - t0 < 3.0:  # nvidia-smi needs a moment to start
-                time.sleep(0.02)
-            self.rows.clear()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            masks = [(name, getattr(N, attr)) for name, attr in self.REASONS]
+
+            def poll():
+                while not self._stop.is_set():
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                      [name for name, m in masks if r & m]))
+                    time.sleep(0.002)
+
+            self.source = "nvml"
+        except Exception:  # pragma: no cover - NVML missing: nvidia-smi in a loop
+            def poll():
+                try:
+                    proc = subprocess.Popen(
+                        ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                         "--format=csv,noheader,nounits", "-lms", "5"], stdout=subprocess.PIPE,
+                        stderr=subprocess.DEVNULL, text=True)
+                except FileNotFoundError:
+                    return
+                names = [n for n, _ in self.REASONS[:4]]
+                for line in proc.stdout:
+                    if self._stop.is_set():
+                        break
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                        self.max_mhz = float(parts[1])
+                        self.rows.append((float(parts[0]), [names[i] for i in range(4) if parts[2 + i] == "Active"]))
+                proc.terminate()
+
+            self.source = "nvidia-smi"
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self.thread.join(timeout=5)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].strip() == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no clock samples"], "source": self.source}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[1]})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def dist_setup():
@@ -176,7 +199,7 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
     pk2 = _peaks2()
     dram, l2b = _traffic(kernel)
     base = {"kernel": kernel, "ms_per_launch": ms_per_launch, "traffic": dram, "l2_traffic": l2b,
-            "traffic_source": "ncu --set full dram__bytes_read+write.sum (lts__t_bytes.sum) per launch, "
+            "traffic_source": "ncu --set full: dram__bytes_read+write.sum (l2_traffic: 32 x lts__t_sectors.sum) per launch, "
                               "profiles/traffic_r*.json"}
     if kernel.startswith("recon_fwd_bwd") and pk2:
         g_pk = pk2["l2_gather_float4_GBps_16MiB"]

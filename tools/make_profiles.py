@@ -33,15 +33,21 @@ def full_capture(rep):
     rr = list(csv.reader(raw.splitlines()))
     hdr, units = rr[0], rr[1]
     want = {"Kernel Name": None, "gpu__time_duration.sum": "dur", "dram__bytes_read.sum": "dram_read",
-            "dram__bytes_write.sum": "dram_write", "lts__t_bytes.sum": "l2_bytes",
+            "dram__bytes_write.sum": "dram_write", "lts__t_sectors.sum": "l2_sectors",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct",
             "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_pct",
             "launch__registers_per_thread": "regs", "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
-            "smsp__inst_executed.sum": "warp_instructions"}
+            "smsp__inst_executed.sum": "warp_instructions",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+            "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1_lsu_wavefront_pct",
+            "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors",
+            "lts__t_sectors_srcunit_tex_op_red.sum": "l2_red_sectors",
+            "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum": "l1_ld_hit_sectors",
+            "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum": "l1_ld_sectors"}
     idx = {k: hdr.index(k) for k in want if k in hdr}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+    scale = {"sector": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
              "msecond": 1e-3, "second": 1}
     out = []
     for r in rr[2:]:

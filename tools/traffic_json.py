@@ -1,4 +1,4 @@
-"""profiles/traffic_<tag>.json: DRAM bytes (read + write) per launch of each kernel bench.py
+"""profiles/traffic_<tag>.json: DRAM bytes (read + write) and L2 bytes (32 x lts__t_sectors) per launch of each kernel bench.py
 names in its roofline, taken from the `--set full` summaries make_profiles.py wrote."""
 import json
 import sys
@@ -17,7 +17,8 @@ def main(tag, *summaries):
         for k in json.loads((ROOT / "profiles" / f"{s}.json").read_text()).get("full", []):
             for pre, name in NAMES.items():
                 if k["kernel"].startswith(pre) and name not in out:
-                    out[name] = float(k["dram_read"]) + float(k["dram_write"])
+                    out[name] = {"dram": float(k["dram_read"]) + float(k["dram_write"]),
+                                 "l2": 32.0 * float(k.get("l2_sectors", 0.0)) or None}
     (ROOT / "profiles" / f"traffic_{tag}.json").write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
