@@ -398,7 +398,13 @@ __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float
   }
 }
 
-template <bool FX = false>  // FX: deterministic fixed-point gradient (ModelDev::dgrid_fx)
+// deterministic mode (FX): every cell costs 16 scalar integer REDs instead of 4 float4 REDs, so
+// larger leader blocks pay there (the float sums inside a block run in lane order: still
+// deterministic once the batch order inside each bucket is fixed)
+#ifndef APMG_FX_GATHER_CAP
+#define APMG_FX_GATHER_CAP 3
+#endif
+template <bool FX = false, int CAP = (FX ? APMG_FX_GATHER_CAP : APMG_GATHER_CAP)>  // FX: fixed-point gradient
 __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,
                                                           bool valid, int vbase, float fx, float fy, float fz,
                                                           float g0, float g1) {
@@ -406,7 +412,7 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
   const int key = valid ? vbase : -1 - lane;
   const unsigned peers = __match_any_sync(0xffffffffu, key);
   const int rank = __popc(peers & ((1u << lane) - 1u));
-  const bool leader = valid && (rank % (APMG_GATHER_CAP + 1)) == 0;
+  const bool leader = valid && (rank % (CAP + 1)) == 0;
   float2 v[8];
   // members of a leader: the next CAP set bits of peers above it, fetched one per round in
   // straight-line code (no vote loop), so the compiler can interleave the shuffles and corner
@@ -415,7 +421,7 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
     unsigned above = peers & (0xfffffffeu << lane);
     corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
 #pragma unroll
-    for (int k = 0; k < APMG_GATHER_CAP; ++k) {
+    for (int k = 0; k < CAP; ++k) {
       const bool has = leader && above != 0u;
       const int src = has ? __ffs(above) - 1 : lane;
       above &= above - 1u;
