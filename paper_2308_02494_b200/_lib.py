@@ -187,7 +187,7 @@ def ptr(t) -> C.c_void_p:
     return C.c_void_p(0 if t is None else t.data_ptr())
 
 
-_STAGE_BYTES = int(os.environ.get("APMG_STAGE_MB", "16")) << 20
+_STAGE_BYTES = int(os.environ.get("APMG_STAGE_MB", "32")) << 20
 _STAGE_SLOTS = int(os.environ.get("APMG_STAGE_SLOTS", "8"))
 _stage = None
 _stage_lock = __import__("threading").Lock()  # one transfer through the ring at a time (worker threads)

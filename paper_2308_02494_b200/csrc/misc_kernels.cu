@@ -344,6 +344,57 @@ __global__ void k_sample_sorted_cells(const double* __restrict__ c64, int64_t n,
   }
 }
 
+// Float sessions with the corner-replicated volume: the fp64 target is sampled while the batch is
+// generated (one 32-byte cell record per point, so the Philox order costs the same DRAM sectors as
+// bucket order) and the bucket scatter moves 16-byte (x, y, z, target) records straight into the
+// recon kernel's coordinate / target arrays: no f64 coordinate round trip, no separate sampling
+// pass.  Same values as k_batch_keys + k_bucket_scatter + k_sample_sorted_cells.
+__global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, const float4* __restrict__ cells, int w,
+                                   int h, int d, float4* __restrict__ rec, uint32_t* __restrict__ key,
+                                   int32_t* __restrict__ counts, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  const uint64_t base = 3ull * uint64_t(batch) * uint64_t(ctl->it);
+  const int cw = w > 1 ? w - 1 : 1, chh = h > 1 ? h - 1 : 1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < batch; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t j = base + 3ull * uint64_t(i);
+    const uint64_t b0 = j >> 2, b1 = (j + 2) >> 2;
+    uint64_t wa[4], wb[4];
+    philox_block(b0 + 1, k0, k1, wa);
+    if (b1 != b0) philox_block(b1 + 1, k0, k1, wb);
+    double c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t jj = j + a;
+      const uint64_t word = ((jj >> 2) == b0) ? wa[jj & 3] : wb[jj & 3];
+      c[a] = add_rn(-1.0, mul_rn(2.0, word_to_double(word)));
+    }
+    const VolAxis ax = vol_axis(c[0], w), ay = vol_axis(c[1], h), az = vol_axis(c[2], d);
+    const int64_t cell = (int64_t(az.i0) * chh + ay.i0) * cw + ax.i0;
+    const float4 lo = __ldg(cells + 2 * cell), hi = __ldg(cells + 2 * cell + 1);
+    const double x00 = lerp_d(double(lo.x), double(lo.y), ax.f), x10 = lerp_d(double(lo.z), double(lo.w), ax.f);
+    const double x01 = lerp_d(double(hi.x), double(hi.y), ax.f), x11 = lerp_d(double(hi.z), double(hi.w), ax.f);
+    const float x = __double2float_rn(c[0]), y = __double2float_rn(c[1]), z = __double2float_rn(c[2]);
+    rec[i] = make_float4(x, y, z, __double2float_rn(lerp_d(lerp_d(x00, x10, ay.f), lerp_d(x01, x11, ay.f), az.f)));
+    const uint32_t k = bucket_of(x, y, z);
+    key[i] = k;
+    atomicAdd(&counts[k], 1);
+  }
+}
+
+__global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
+                                     int32_t* __restrict__ cursor, float* __restrict__ coords,
+                                     float* __restrict__ targets, const TrainCtl* ctl) {
+  if (ctl->skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pos = atomicAdd(&cursor[key[i]], 1);
+    const float4 r = rec[i];
+    coords[3 * pos] = r.x;
+    coords[3 * pos + 1] = r.y;
+    coords[3 * pos + 2] = r.z;
+    targets[pos] = r.w;
+  }
+}
+
 template __global__ void k_sample_sorted_cells<float>(const double*, int64_t, const float4*, int, int, int, float*,
                                                       float*, const TrainCtl*);
 template __global__ void k_sample_sorted_cells<double>(const double*, int64_t, const float4*, int, int, int, double*,

@@ -402,7 +402,7 @@ __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float
 // larger leader blocks pay there (the float sums inside a block run in lane order: still
 // deterministic once the batch order inside each bucket is fixed)
 #ifndef APMG_FX_GATHER_CAP
-#define APMG_FX_GATHER_CAP 3
+#define APMG_FX_GATHER_CAP 7
 #endif
 template <bool FX = false, int CAP = (FX ? APMG_FX_GATHER_CAP : APMG_GATHER_CAP)>  // FX: fixed-point gradient
 __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,

@@ -33,6 +33,12 @@ constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
                              uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
 __global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, const float4* __restrict__ cells, int w,
+                                   int h, int d, float4* __restrict__ rec, uint32_t* __restrict__ key,
+                                   int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
+                                     int32_t* __restrict__ cursor, float* __restrict__ coords,
+                                     float* __restrict__ targets, const TrainCtl* ctl);
 __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
                                  int32_t* __restrict__ cursor, double* __restrict__ c64_out,
                                  int32_t* __restrict__ perm, const TrainCtl* ctl);
@@ -419,7 +425,18 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
     }
   }
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
-  if (s->sort) {
+  const char* efb = getenv("APMG_FUSED_BATCH");
+  if (s->sort && sizeof(T) == 4 && s->vol_cells && !s->perm && !(efb && efb[0] == '0')) {
+    // float session, corner-replicated volume, default (float-RED) mode: targets sampled with the
+    // batch, (x, y, z, target) records bucketed straight into the recon inputs
+    APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
+    float4* rec = reinterpret_cast<float4*>(s->c64_raw);  // 16 of its 24 bytes per point
+    APMG_LAUNCH("batch_keys", k_batch_keys_cells, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B,
+                reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, rec, s->key, s->counts, s->ctl);
+    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
+    APMG_LAUNCH("bucket_scatter", k_bucket_scatter_rec, elementwise_grid(B, 8), 256, 0, st, rec, s->key, B,
+                s->counts, reinterpret_cast<float*>(s->coords), reinterpret_cast<float*>(s->targets), s->ctl);
+  } else if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
     APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
     APMG_LAUNCH("batch_keys", k_batch_keys, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->c64_raw, s->key,

@@ -777,3 +777,21 @@ def test_train_c1_300_baseline_parity():
     assert log0.iterations_run == 300 and log0.transform_stop_iteration == ens["unperturbed_log"][
         "transform_stop_iteration"]
     np.testing.assert_allclose(log0.l_rec[:8], ens["unperturbed_log"]["l_rec"][:8], rtol=2e-3)
+
+
+def test_fused_batch_sampling_matches_sorted_sampler(monkeypatch):
+    """Float sessions sample the fp64 targets while generating the batch and bucket (x, y, z, target)
+    records (k_batch_keys_cells + k_bucket_scatter_rec); the separate sorted sampler
+    (APMG_FUSED_BATCH=0) gives the same per-point values, so the first losses agree to the f64
+    summation order of points within a bucket."""
+    vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
+    logs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("APMG_FUSED_BATCH", fused)
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=2, batch_size=1 << 16, delay_start=0, seed=4, plateau_enabled=False,
+                            transform_hard_stop_fraction=1.0)
+        logs.append(P.train_single(m, vol, cfg)[1])
+    np.testing.assert_allclose(logs[0].l_rec[0], logs[1].l_rec[0], rtol=1e-12)
+    np.testing.assert_allclose(logs[0].l_density[0], logs[1].l_density[0], rtol=1e-9)
