@@ -583,7 +583,10 @@ __global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float*
                                                                  const double* __restrict__ stats, int ch,
                                                                  double* __restrict__ part, const TrainCtl* ctl) {
   if (ctl && (ctl->skip || !ctl->density_on)) return;
-  extern __shared__ float4 sP[];                                   // [ch <= kGradCH] (x0, x1, x2, d_rho)
+  // the chunk's points as lane pairs (i, i + 32) of each 64-point run, pre-paired so that the packed
+  // fp32x2 arithmetic reads its operand pairs straight from two 16-byte loads:
+  // sP[2 j] = (x0_a, x0_b, x1_a, x1_b), sP[2 j + 1] = (x2_a, x2_b, d_rho_a, d_rho_b)
+  extern __shared__ float4 sP[];                                   // [ch <= kGradCH] (2 float4 per pair)
   const double total = stats[0], S = stats[3];  // d_rho formed while staging (k_dens_drho32's value)
   double* s_acc = reinterpret_cast<double*>(sP + kGradCH);         // [M][13]
   float* s_tf = reinterpret_cast<float*>(s_acc + 13 * M);          // [M][13]
@@ -593,9 +596,15 @@ __global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float*
   for (int64_t c0 = int64_t(blockIdx.x) * ch; c0 < n; c0 += int64_t(gridDim.x) * ch) {
     const int cnt = int(min64(ch, n - c0));
     __syncthreads();  // previous chunk consumed, transforms / accumulators staged
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    float* sF = reinterpret_cast<float*>(sP);
+    for (int i = threadIdx.x; i < ((cnt + 63) & ~63); i += blockDim.x) {
       const int64_t g = c0 + i;
-      sP[i] = make_float4(x[3 * g], x[3 * g + 1], x[3 * g + 2], float((d_s[g] - S) / total));
+      const bool ok = i < cnt;  // d_rho 0 past the end: no share
+      const int j = (i >> 6) * 32 + (i & 31), h = (i >> 5) & 1;
+      sF[8 * j + h] = ok ? x[3 * g] : 0.f;
+      sF[8 * j + 2 + h] = ok ? x[3 * g + 1] : 0.f;
+      sF[8 * j + 4 + h] = ok ? x[3 * g + 2] : 0.f;
+      sF[8 * j + 6 + h] = ok ? float((d_s[g] - S) / total) : 0.f;
     }
     __syncthreads();
     // two grids per pass (m, m + nw): independent chains for the scheduler, one read of the points
@@ -614,10 +623,10 @@ __global__ void __launch_bounds__(kDensThreads, 2) k_dens_grad32cx2(const float*
 #pragma unroll
         for (int e = 0; e < 13; ++e) acc[k][e] = make_float2(0.f, 0.f);
       for (int i = lane; i < cnt; i += 64) {
-        const float4 q0 = sP[i];
-        const float4 q1 = i + 32 < cnt ? sP[i + 32] : make_float4(0.f, 0.f, 0.f, 0.f);  // d_rho 0: no share
-        const float2 X0 = make_float2(q0.x, q1.x), X1 = make_float2(q0.y, q1.y), X2 = make_float2(q0.z, q1.z);
-        const float2 W = make_float2(q0.w, q1.w);
+        const int j = (i >> 6) * 32 + lane;
+        const float4 q0 = sP[2 * j], q1 = sP[2 * j + 1];
+        const float2 X0 = make_float2(q0.x, q0.y), X1 = make_float2(q0.z, q0.w), X2 = make_float2(q1.x, q1.y);
+        const float2 W = make_float2(q1.z, q1.w);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           float2 b, l[3], lp[3];

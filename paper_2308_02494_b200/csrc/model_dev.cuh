@@ -377,7 +377,7 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
 // shuffles share the LSU data path with the shared-memory traffic and the gathers).  Lanes
 // of rank r = 0 mod (CAP + 1) in their cell group lead blocks of up to CAP + 1 lanes.
 #ifndef APMG_GATHER_CAP
-#define APMG_GATHER_CAP 1
+#define APMG_GATHER_CAP 2
 #endif
 // weights wx[c & 1] * (wy[(c >> 1) & 1] * wz[c >> 2]) formed in packed fp32x2 (same roundings as
 // the scalar products: (wy0, wy1) * wz, then (wx0, wx1) * wzy), contributions g * w
