@@ -278,6 +278,8 @@ int apmg_train_moments(apmg_train_state* s, void* main_m, void* main_v, void* tf
 int apmg_debug_infer_phases(long long* out);
 /* same for the bf16x3 recon kernel: [16 tiles][12 phases] (APMG_TC_STAMPS=1, tools/tc16_phases.py) */
 int apmg_debug_tc16_phases(long long* out);
+/* per warp of CTA 0: [16 tiles][16 warps][16 points] (APMG_TC_STAMPS=1, tools/tc16_warps.py) */
+int apmg_debug_tc16_warp_phases(long long* out);
 
 /* ---- host-side restatement hooks (unit tests of the scheduler on CPU) -------- */
 /* plateau_step (trainer.py:118-138) on the same code the device controller runs.

@@ -113,6 +113,7 @@ SIGNATURES = {
     "apmg_host_pairwise_sum": (_D, [C.POINTER(_D), _I64]),
     "apmg_debug_infer_phases": (C.c_int, [_P]),
     "apmg_debug_tc16_phases": (C.c_int, [_P]),
+    "apmg_debug_tc16_warp_phases": (C.c_int, [_P]),
 }
 
 _lib = None

@@ -220,7 +220,13 @@ __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, 
 __device__ __forceinline__ void interp_pairx_f32(const float4* __restrict__ gx, int W, int HW, int vbase, float fx,
                                                  float fy, float fz, float& o0, float& o1) {
   const float4* g = gx + vbase;
+#ifdef APMG_ABL_NOGATHER  // timing ablation only: no corner loads (wrong results)
+  const float q = __int_as_float(vbase & 0x3fffff);
+  const float4 b00 = make_float4(q, q, q, q), b01 = b00, b10 = b00, b11 = b00;
+  (void)g;
+#else
   const float4 b00 = __ldg(g), b01 = __ldg(g + W), b10 = __ldg(g + HW), b11 = __ldg(g + HW + W);
+#endif
   const float2 r = f2_lerp(f2_lerp(f2_lerp(make_float2(b00.x, b00.y), make_float2(b00.z, b00.w), fx),
                                    f2_lerp(make_float2(b01.x, b01.y), make_float2(b01.z, b01.w), fx), fy),
                            f2_lerp(f2_lerp(make_float2(b10.x, b10.y), make_float2(b10.z, b10.w), fx),
@@ -360,8 +366,12 @@ __device__ __forceinline__ void scatter_vertex_warp_agg(const ModelDev<float>& m
     float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
 #pragma unroll
     for (int c = 0; c < 8; c += 2)
+#ifdef APMG_ABL_NORED  // timing ablation only: no gradient REDs (wrong results)
+      if (v[c].x == 1.2345e-30f && v[c + 1].y == 1.2345e-30f) base[c] = make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y);
+#else
       atomicAdd(base + (c >> 2) * md.H * md.W + ((c >> 1) & 1) * md.W,
                 make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y));
+#endif
     return;
   }
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;
@@ -447,8 +457,12 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
     float4* base = reinterpret_cast<float4*>(dgrid) + vbase;
 #pragma unroll
     for (int c = 0; c < 8; c += 2)
+#ifdef APMG_ABL_NORED  // timing ablation only: no gradient REDs (wrong results)
+      if (v[c].x == 1.2345e-30f && v[c + 1].y == 1.2345e-30f) base[c] = make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y);
+#else
       atomicAdd(base + (c >> 2) * md.H * md.W + ((c >> 1) & 1) * md.W,
                 make_float4(v[c].x, v[c].y, v[c + 1].x, v[c + 1].y));
+#endif
     return;
   }
   const int sy = 2 * md.W, sz = 2 * md.H * md.W;

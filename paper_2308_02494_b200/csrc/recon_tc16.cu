@@ -68,14 +68,41 @@ constexpr uint32_t TC_A = 0, TC_B = 64, TC_DW1 = 128, TC_DW2 = 256, TC_CACHE = 3
 constexpr uint32_t CACHE_TILE = 96;
 static_assert(TC_CACHE + 2 * CACHE_TILE <= TMEM_COLS, "tensor memory budget");
 
-// where the scatter of tile t runs: SQ_I pairs interleaved with the encode of tile t+1, SQ_C in the
-// z2 wait and SQ_E in the dz1 || dW2 wait of tile t+1, the rest in its gF || dW1 wait
+// where the scatter of tile t runs: SQ_I pairs interleaved with the encode of tile t+1, SQ_Z in the
+// wait for its z1, SQ_C in its z2 wait and SQ_E in its dz1 || dW2 wait, the rest in its gF || dW1 wait
 #ifndef TC16_SQ_I
-#define TC16_SQ_I 3
-#define TC16_SQ_C 1
-#define TC16_SQ_E 1
+#define TC16_SQ_I 0
+#define TC16_SQ_Z 2
+#define TC16_SQ_C 2
+#define TC16_SQ_E 2
 #endif
-constexpr int SQ_I = TC16_SQ_I, SQ_C = TC16_SQ_C, SQ_E = TC16_SQ_E, SQ = 8;
+#ifndef TC16_FWD_Q
+#define TC16_FWD_Q 6  // forward products per GEMM: 6 (f32-level) or 3 (hh, hm, mh: ~2^-16)
+#endif
+constexpr int FWD_Q = TC16_FWD_Q;
+// dedicated MMA-issue warp (warp NW, lane 0; warps NW+1..NW+3 idle) instead of thread 0 of worker
+// warp 0: an issuing thread blocks while the tensor pipe's queue is full (~24 MMAs of ~51 cycles),
+// which made warp 0 the straggler at every barrier of the tile
+#ifndef TC16_MMA_WARP
+#define TC16_MMA_WARP 1
+#endif
+constexpr bool kMmaWarp = TC16_MMA_WARP != 0;
+constexpr int NT_LAUNCH = kMmaWarp ? NT + 128 : NT;
+// registers: launched at 96 per thread (640 threads); the helper warpgroup releases 64 per thread
+// (setmaxnreg.dec) and the workers take them (setmaxnreg.inc blocks until the CTA's pool holds
+// them: 16 x (112 - 96) = 4 x (96 - 32))
+#ifndef TC16_REG_WORK
+#define TC16_REG_WORK 112
+#define TC16_REG_HELP 32
+#endif
+constexpr int REG_WORK = TC16_REG_WORK, REG_HELP = TC16_REG_HELP;
+static_assert(!kMmaWarp || NW * (REG_WORK - 96) <= 4 * (96 - REG_HELP), "setmaxnreg.inc would wait forever");
+// named barriers: 1 MMA handoff / encode sync (workers + issuing warp), 2-5 lane-quarter head
+// exchange, 6 first-half z1 handoff, 7 workers only, 8 end of kernel (all warps)
+constexpr int BAR_MMA = 1, BAR_Z1A = 6, BAR_WORK = 7, BAR_END = 8;
+constexpr int FWD_PLANES = FWD_Q == 6 ? 3 : 2;
+constexpr int SQ_I = TC16_SQ_I, SQ_Z = TC16_SQ_Z, SQ_C = TC16_SQ_C, SQ_E = TC16_SQ_E, SQ = 8;
+constexpr int SQ1 = SQ_I + SQ_Z, SQ2 = SQ1 + SQ_C, SQ3 = SQ2 + SQ_E;  // cumulative pair boundaries
 
 // fractions in [0, 1] as 21-bit fixed point (resolution 2^-21; the scatter weights only)
 __device__ __forceinline__ void pack_cell(int vbase, float fx, float fy, float fz, uint32_t* w) {
@@ -102,6 +129,14 @@ __device__ long long g_tc16_stamp[16][12];
 #define TC16_STAMP(k)                                                                   \
   do {                                                                                  \
     if (a.stamps && blockIdx.x == 0 && tid == 0 && it < 16) g_tc16_stamp[it][k] = clock64(); \
+    TC16_WSTAMP(k);                                                                     \
+  } while (0)
+// the same per warp (lane 0 of every warp of CTA 0), with extra points inside the encode and
+// before the tensor-core waits (APMG_TC_STAMPS=1; profiling only)
+__device__ long long g_tc16_wstamp[16][16][16];
+#define TC16_WSTAMP(k)                                                                                          \
+  do {                                                                                                          \
+    if (a.stamps && blockIdx.x == 0 && (tid & 31) == 0 && it < 16) g_tc16_wstamp[it][tid >> 5][k] = clock64(); \
   } while (0)
 
 // gF [P][128] f32, 8-byte granules XOR-swizzled by row: f(p) maps p & 15 onto the even
@@ -139,6 +174,9 @@ __device__ __forceinline__ void load_tile(const Args& a, int64_t tile, float* sX
 template <bool FX>
 __device__ __forceinline__ void scatter_pairs(const ModelDev<float>& md, const Args& a, const float* GF,
                                               uint32_t tmem_cache, int q0, int q1, int cnt, int warp, int lane) {
+#ifdef TC16_ABL_NOSCATTER  // timing ablation only: no scatter at all (wrong results)
+  return;
+#endif
 #pragma unroll
   for (int jq = 0; jq < 2; ++jq) {
     if (q1 <= 4 * jq || q0 >= 4 * jq + 4) continue;  // warp-uniform
@@ -189,7 +227,7 @@ __device__ __forceinline__ float2 bump_p10x2(float2 l0, float2 l1, float2 l2) {
 }
 
 template <bool FX>  // FX: deterministic training (fixed-point grid gradient)
-__global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
+__global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
   extern __shared__ __align__(1024) unsigned char sm[];
   if (a.ctl && a.ctl->skip) return;
   const ModelDev<float>& md = a.md;
@@ -216,15 +254,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   const bool rho_on = md.rho_out && (!a.ctl || a.ctl->density_on);
 
   // ---- stage weights (bf16x3, rows = output unit) ----
-  for (int e = tid; e < 64 * 16; e += NT) {
+  for (int e = tid; e < 64 * 16 && tid < NT; e += NT) {
     const int r = e >> 4, c0 = (e & 15) * 8;
     umma::store_chunk3(W1, PL64x128, r, c0, 64, md.w1 + r * FE + c0);
   }
-  for (int e = tid; e < 64 * 8; e += NT) {
+  for (int e = tid; e < 64 * 8 && tid < NT; e += NT) {
     const int r = e >> 3, c0 = (e & 7) * 8;
     umma::store_chunk3(W2, PL64x64, r, c0, 64, md.w2 + r * HID + c0);
   }
-  for (int e = tid; e < 64 * 12; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
+  for (int e = tid; e < 64 * 12 && tid < NT; e += NT) sTF[e] = md.tf[16 * (e / 12) + (e % 12)];
   if (tid < HID) sW3[tid] = md.w3[tid];
   if (rho_on && tid < md.M) {  // |det A| in f64, as density.py:72-80 (stage_transforms32)
     const float* t = md.tf + 16 * tid;
@@ -268,6 +306,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   const uint32_t id_mm = umma::idesc_bf16(64, 64, true, true);        // A, B MN-major
   const uint32_t id_mm128 = umma::idesc_bf16(64, 128, true, true);
   const float coef = __fmul_rn(float(2.0 / double(a.n)), md.span);
+  const bool issuer = kMmaWarp ? (warp == NW && lane == 0) : (tid == 0);
 
   // M=64 accumulators are read with the 16x256b shape: thread t owns rows p0 = 16q + t/4 and
   // p1 = p0 + 8, columns ep_col0 + 8r + ec (+1) of each 8-column repetition r
@@ -284,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   // encode of grids 2 warp + 32 jq + {0, 1} for points lane, lane + 32: the two points of a grid
   // share its transform and run in packed fp32x2 arithmetic; the two grids' four features of a
   // point are adjacent in F (one 8-byte store per plane)
+  int it = 0;
   auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache, float2& racc) {
     const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
     const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
@@ -331,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     for (int h = 0; h < 2; ++h) {
       const uint32_t o = umma::cm16_offset(lane + 32 * h, 4 * warp + 64 * jq, 64);
 #pragma unroll
-      for (int pl = 0; pl < 3; ++pl)
+      for (int pl = 0; pl < FWD_PLANES; ++pl)
         *reinterpret_cast<uint2*>(F + pl * PL64x128 + o) = make_uint2(fw[0][h][pl], fw[1][h][pl]);
     }
     umma::tmem_st8(tmem_cache + 12 * jq, cache);
@@ -339,14 +379,75 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
   };
   // z1 = F W1^T over K-steps [k0, k1) (K = 16 each), committed when `last`
   auto issue_z1 = [&](int k0, int k1, bool last) {
-    if (tid != 0) return;
+    if (!issuer) return;
     umma::fence_after_sync();
+#pragma unroll 1
     for (int kk = k0; kk < k1; ++kk)
 #pragma unroll
-      for (int q = 0; q < 6; ++q)
+      for (int q = 0; q < FWD_Q; ++q)
         umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_F + kPA(q) * PL64x128, 64, kk),
                          umma::kmajor_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kk, (kk | q) ? 1u : 0u);
     if (last) umma::commit(bar);
+  };
+  // z2 = h1 W2^T
+  auto issue_z2 = [&]() {
+    if (!issuer) return;
+    umma::fence_after_sync();
+#pragma unroll 1
+    for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+      for (int q = 0; q < FWD_Q; ++q)
+        umma::mma_bf16_c(TB, base16, umma::kmajor_c(OFF_H1 + kPA(q) * PL64x64, 64, kk),
+                         umma::kmajor_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
+    umma::commit(bar);
+  };
+  // dz1 = dz2 W2 (-> acc A), dW2 += dz2^T h1 (-> TMEM sum)
+  auto issue_dz1_dw2 = [&]() {
+    if (!issuer) return;
+    umma::fence_after_sync();
+#pragma unroll 1
+    for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
+                         umma::mnmajor16_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kmn, (kk | q) ? 1u : 0u);
+#pragma unroll 1
+    for (int kk = 0; kk < P / 16; ++kk)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        umma::mma_bf16_c(TDW2, base16, umma::mnmajor16_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
+                         umma::mnmajor16_c(OFF_H1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
+    umma::commit(bar);
+  };
+  // gF = dz1 W1 (-> acc A|B, N=128), dW1 += dz1^T F (-> TMEM sum)
+  auto issue_gf_dw1 = [&]() {
+    if (!issuer) return;
+    umma::fence_after_sync();
+#pragma unroll 1
+    for (int kk = 0; kk < HID / 16; ++kk)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
+                         umma::mnmajor16_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
+#pragma unroll 1
+    for (int kk = 0; kk < P / 16; ++kk)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        umma::mma_bf16_c(TDW1, base16, umma::mnmajor16_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
+                         umma::mnmajor16_c(OFF_F + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
+    umma::commit(bar);
+  };
+  // operands of the next products are in shared memory: release the issuing thread (the
+  // workers arrive and go on; without the MMA warp, warp 0 waits and issues)
+  auto handoff = [&](int id) {
+    if constexpr (kMmaWarp) {
+      umma::named_arrive(id, NT + 32);
+    } else {
+      if (warp == 0) umma::named_sync(id, NT); else umma::named_arrive(id, NT);
+    }
+  };
+  auto worker_sync = [&]() {
+    if constexpr (kMmaWarp) umma::named_sync(BAR_WORK, NT); else __syncthreads();
   };
   // encode of a tile into cache buffer `cache_enc`, with pairs [0, SQ_I) of the previous tile's
   // scatter (cache buffer `cache_sc`, scatter_cnt points; < 0: none) interleaved group by group
@@ -371,16 +472,14 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       if (scatter_cnt >= 0)
         scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
       encode_group(cX, jq, cache_enc, racc);
+      TC16_WSTAMP(9 + 2 * jq);
       if (jq == 0) {
-        // features k < 64 (grids 0-31) complete: first half of z1.  Only warp 0 (which issues)
-        // waits for the other warps; they signal the named barrier and carry on with group 1
+        // features k < 64 (grids 0-31) complete: first half of z1.  Only the issuing warp waits
+        // for the others; they signal the named barrier and carry on with group 1
         umma::fence_async_smem();
-        if (warp == 0) {
-          umma::named_sync(1, NT);
-          issue_z1(0, FE / 32, false);
-        } else {
-          umma::named_arrive(1, NT);
-        }
+        handoff(BAR_Z1A);
+        if constexpr (!kMmaWarp) issue_z1(0, FE / 32, false);
+        TC16_WSTAMP(10);
       }
     }
     umma::tmem_st_wait();
@@ -397,11 +496,43 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
-    __syncthreads();  // F complete; every warp's scatter of the previous tile has read gF
-    issue_z1(FE / 32, FE / 16, true);
+    // F complete; every warp's scatter of the previous tile has read gF (with the MMA warp: a
+    // barrier of the workers and the issuing warp, which then issues the second half of z1)
+    if constexpr (kMmaWarp) umma::named_sync(BAR_MMA, NT + 32); else __syncthreads();
+    TC16_WSTAMP(12);
+    if constexpr (!kMmaWarp) issue_z1(FE / 32, FE / 16, true);
   };
 
-  int it = 0;
+  if constexpr (kMmaWarp) {
+    if (warp >= NW) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_HELP));
+      if (warp == NW) {  // the issuing warp: the workers' handoffs, in their order
+        if (int64_t(blockIdx.x) < tiles) {
+          umma::named_sync(BAR_Z1A, NT + 32);
+          issue_z1(0, FE / 32, false);
+          umma::named_sync(BAR_MMA, NT + 32);
+          issue_z1(FE / 32, FE / 16, true);
+        }
+        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+          umma::named_sync(BAR_MMA, NT + 32);
+          issue_z2();
+          umma::named_sync(BAR_MMA, NT + 32);
+          issue_dz1_dw2();
+          umma::named_sync(BAR_MMA, NT + 32);
+          issue_gf_dw1();
+          if (tile + gridDim.x < tiles) {
+            umma::named_sync(BAR_Z1A, NT + 32);
+            issue_z1(0, FE / 32, false);
+            umma::named_sync(BAR_MMA, NT + 32);
+            issue_z1(FE / 32, FE / 16, true);
+          }
+        }
+      }
+      umma::named_sync(BAR_END, NT_LAUNCH);  // the workers' final barrier (TMEM dealloc after it)
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_WORK));
+  }
   if (int64_t(blockIdx.x) < tiles) encode_tile(sX, tmem_cache0, tmem_cache0, -1, int64_t(blockIdx.x) + gridDim.x, 1);
   int cnt_prev = -1;  // the previous tile's scatter pairs [SQ_I, SQ) run in this tile's tensor-core waits
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
@@ -409,6 +540,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     const float* cT = sT + (it & 1) * P;
     const uint32_t cache_cur = tmem_cache0 + (it & 1) * CACHE_TILE, cache_prev = tmem_cache0 + ((it + 1) & 1) * CACHE_TILE;
     TC16_STAMP(0);
+    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I, SQ1, cnt_prev, warp, lane);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -436,27 +568,26 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        umma::store_pair3(H1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
-        umma::store_pair3(H1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
+        if constexpr (FWD_PLANES == 3) {
+          umma::store_pair3(H1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
+          umma::store_pair3(H1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
+        } else {
+          umma::store_pair2(H1, PL64x64, p0, ep_col0 + 8 * r + ec, 64, v[4 * r], v[4 * r + 1]);
+          umma::store_pair2(H1, PL64x64, p1, ep_col0 + 8 * r + ec, 64, v[4 * r + 2], v[4 * r + 3]);
+        }
       }
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
     // only the issuing warp waits for the stores; the others go on to their share of the
-    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
-    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
+    // previous tile's scatter
+    handoff(BAR_MMA);
     umma::fence_after_sync();
     TC16_STAMP(2);
     // ---- z2 = h1 W2^T ----
-    if (tid == 0) {
-      for (int kk = 0; kk < HID / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 6; ++q)
-          umma::mma_bf16_c(TB, base16, umma::kmajor_c(OFF_H1 + kPA(q) * PL64x64, 64, kk),
-                           umma::kmajor_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kk, (kk | q) ? 1u : 0u);
-      umma::commit(bar);
-    }
-    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I, SQ_I + SQ_C, cnt_prev, warp, lane);
+    if constexpr (!kMmaWarp) issue_z2();
+    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ1, SQ2, cnt_prev, warp, lane);
+    TC16_WSTAMP(13);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -527,26 +658,15 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_async_smem();
     umma::fence_before_sync();
     // only the issuing warp waits for the stores; the others go on to their share of the
-    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
-    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
+    // previous tile's scatter
+    handoff(BAR_MMA);
     umma::fence_after_sync();
     TC16_STAMP(4);
     // ---- dz1 = dz2 W2 (-> acc A), dW2 += dz2^T h1 (-> TMEM sum) ----
-    if (tid == 0) {
-      for (int kk = 0; kk < HID / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
-                           umma::mnmajor16_c(OFF_W2 + kPB(q) * PL64x64, 64, kk), id_kmn, (kk | q) ? 1u : 0u);
-      for (int kk = 0; kk < P / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          umma::mma_bf16_c(TDW2, base16, umma::mnmajor16_c(OFF_DZ2 + kPA(q) * PL64x64, 64, kk),
-                           umma::mnmajor16_c(OFF_H1 + kPB(q) * PL64x64, 64, kk), id_mm, 1u);
-      umma::commit(bar);
-    }
+    if constexpr (!kMmaWarp) issue_dz1_dw2();
     if (cnt_prev >= 0)
-      scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I + SQ_C, SQ_I + SQ_C + SQ_E, cnt_prev, warp, lane);
+      scatter_pairs<FX>(md, a, GF, cache_prev, SQ2, SQ3, cnt_prev, warp, lane);
+    TC16_WSTAMP(14);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
@@ -567,30 +687,19 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     umma::fence_async_smem();
     umma::fence_before_sync();
     // only the issuing warp waits for the stores; the others go on to their share of the
-    // previous tile's scatter (named barrier 1: 15 warps arrive, warp 0 syncs)
-    if (warp == 0) umma::named_sync(1, NT); else umma::named_arrive(1, NT);
+    // previous tile's scatter
+    handoff(BAR_MMA);
     umma::fence_after_sync();
     TC16_STAMP(6);
     // ---- gF = dz1 W1 (-> acc A|B, N=128), dW1 += dz1^T F (-> TMEM sum) ----
-    if (tid == 0) {
-      for (int kk = 0; kk < HID / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
-                           umma::mnmajor16_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
-      for (int kk = 0; kk < P / 16; ++kk)
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          umma::mma_bf16_c(TDW1, base16, umma::mnmajor16_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
-                           umma::mnmajor16_c(OFF_F + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
-      umma::commit(bar);
-    }
-    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ_I + SQ_C + SQ_E, SQ, cnt_prev, warp, lane);
+    if constexpr (!kMmaWarp) issue_gf_dw1();
+    if (cnt_prev >= 0) scatter_pairs<FX>(md, a, GF, cache_prev, SQ3, SQ, cnt_prev, warp, lane);
+    TC16_WSTAMP(15);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
     umma::fence_after_sync();
     umma::fence_before_sync();
-    __syncthreads();  // every warp's scatter of the previous tile has read gF before it is overwritten
+    worker_sync();  // every warp's scatter of the previous tile has read gF before it is overwritten
     umma::fence_after_sync();
     TC16_STAMP(7);
     // ---- gF epilogue: 32 columns per warp -> gF[p][k] ----
@@ -605,7 +714,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
       }
     }
     umma::fence_before_sync();
-    __syncthreads();
+    worker_sync();
     TC16_STAMP(8);
     // ---- encode of the next tile with the first SQ_I pairs of this tile's scatter interleaved;
     // the rest of the scatter runs in the next tile's tensor-core waits ----
@@ -620,7 +729,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
 
   // ---- flush per-CTA partials: [dW1 (64x128) | dW2 (64x64) | dW3 (64)] from TMEM ----
   umma::fence_before_sync();
-  __syncthreads();
+  worker_sync();
   umma::fence_after_sync();
   float* dst = a.part_dw + int64_t(blockIdx.x) * (HID * FE + HID * HID + HID);
   {
@@ -653,9 +762,23 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     v += __shfl_xor_sync(0xffffffffu, v, 16);
     if (lane < 4) sDW3[quarter * HID + ep_col0 + 8 * (c >> 1) + ec + (c & 1)] = v;  // one writer per slot
   }
-  const double bl = block_sum(loss, red);  // contains __syncthreads
+  // CTA sum over the worker warps (block_sum with the workers' barrier)
+  auto worker_sum = [&](double v) {
+    v = warp_sum(v);
+    worker_sync();
+    if (lane == 0) red[warp] = v;
+    worker_sync();
+    double t = (tid < NW) ? red[tid] : 0.0;
+    if (warp == 0) t = warp_sum(t);
+    if (tid == 0) red[0] = t;
+    worker_sync();
+    const double r = red[0];
+    worker_sync();
+    return r;
+  };
+  const double bl = worker_sum(loss);
   if (rho_on) {
-    const double br = block_sum(srho, red);
+    const double br = worker_sum(srho);
     if (tid == 0) {  // the rho pass's (sum rho, sum sq_err) partials, one pair per CTA
       md.rho_part[2 * blockIdx.x] = br;
       md.rho_part[2 * blockIdx.x + 1] = bl;
@@ -665,7 +788,7 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
     dst[HID * FE + HID * HID + tid] = ((sDW3[tid] + sDW3[HID + tid]) + sDW3[2 * HID + tid]) + sDW3[3 * HID + tid];
   if (tid == 0) a.part_loss[blockIdx.x] = bl;
   umma::fence_before_sync();
-  __syncthreads();
+  if constexpr (kMmaWarp) umma::named_sync(BAR_END, NT_LAUNCH); else __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, TMEM_COLS);
 }
 
@@ -673,6 +796,10 @@ __global__ void __launch_bounds__(NT, 1) k_recon_tc16(Args a) {
 
 extern "C" int apmg_debug_tc16_phases(long long* out) {
   APMG_CUDA_TRY(cudaMemcpyFromSymbol(out, tc16::g_tc16_stamp, sizeof(tc16::g_tc16_stamp)));
+  return APMG_OK;
+}
+extern "C" int apmg_debug_tc16_warp_phases(long long* out) {  // [16 tiles][16 warps][16 points]
+  APMG_CUDA_TRY(cudaMemcpyFromSymbol(out, tc16::g_tc16_wstamp, sizeof(tc16::g_tc16_wstamp)));
   return APMG_OK;
 }
 
@@ -702,9 +829,9 @@ int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords,
                (es && es[0] == '1') ? 1 : 0};
   if (md.dgrid_fx) a.aggregate = 2;  // the fixed-point (deterministic) scatter lives in the gather variant
   if (md.dgrid_fx)
-    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<true>, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
+    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<true>, grid, tc16::NT_LAUNCH, tc16::SMEM_BYTES, st, a);
   else
-    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<false>, grid, tc16::NT, tc16::SMEM_BYTES, st, a);
+    APMG_LAUNCH("recon_fwd_bwd_tc", tc16::k_recon_tc16<false>, grid, tc16::NT_LAUNCH, tc16::SMEM_BYTES, st, a);
   return APMG_OK;
 }
 

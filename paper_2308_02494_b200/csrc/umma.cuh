@@ -135,6 +135,9 @@ __host__ __device__ constexpr DescC mnmajor16_c(uint32_t off, int R, int kk) {
 }
 __device__ __forceinline__ void mma_bf16_c(uint32_t d_tmem, uint32_t base16, DescC a, DescC b, uint32_t idesc,
                                            uint32_t accumulate) {
+#ifdef APMG_ABL_NOMMA  // timing ablation only: no tensor-core work (wrong results)
+  if (idesc != 0xffffffffu) return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"

@@ -214,6 +214,7 @@ class TrainSession:
         # allocator (reused by back-to-back sessions, released by torch under memory pressure)
         need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
         self.ws = L.workspace((need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d))
+        t3 = time.perf_counter()
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()
         L.check(L.lib().apmg_train_create(C.byref(st), C.byref(self.dm.desc), L.ptr(self.main), L.ptr(self.tf),
@@ -223,8 +224,8 @@ class TrainSession:
         self.state = st
         self._torch = t
         # host-side setup split (ms): parameters, volume upload, workspace + create (synchronised)
-        self.setup_ms = {"params": 1e3 * (t1 - t0), "volume": 1e3 * (t2 - t1),
-                         "create": 1e3 * (time.perf_counter() - t2)}
+        self.setup_ms = {"params": 1e3 * (t1 - t0), "volume": 1e3 * (t2 - t1), "workspace": 1e3 * (t3 - t2),
+                         "create": 1e3 * (time.perf_counter() - t3)}
 
     def run(self, n: int) -> None:
         L.check(L.lib().apmg_train_run(self.state, int(n), L.stream_handle()), "train_run")
