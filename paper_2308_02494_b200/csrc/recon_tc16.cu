@@ -338,7 +338,11 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
       const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
       const float2 l2 = local_coord2(X0, X1, X2, tf[8], tf[9], tf[10], tf[11]);
       if (rho_on) {
+#ifdef TC16_ABL_NOBUMP  // timing ablation only: bump 1 (rho stays positive, training stays finite)
+        const float2 b = make_float2(1.f, 1.f);
+#else
         const float2 b = bump_p10x2(l0, l1, l2);
+#endif
         racc = make_float2(fmaf(sDET[m], b.x, racc.x), fmaf(sDET[m], b.y, racc.y));
       }
       int ix[2], iy[2], iz[2];

@@ -471,6 +471,14 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                            grad + s->off[2],
                            grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);
   if (rc) return rc;
+#ifdef APMG_ABL_FREEZE  // timing builds only: parameters frozen (no Adam, no density step), so
+  // ablated kernels computing wrong values cannot change later iterations' inputs
+  if (m.grids > 0) {
+    APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
+                s->plat_ring, s->trig);
+    return APMG_OK;
+  }
+#endif
   APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
               static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
               reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx), s->gfx,
