@@ -44,8 +44,14 @@ constexpr uint32_t OFF_W2 = OFF_W1 + 3 * PL64x128;      // [64 j][64 i] x3
 constexpr uint32_t OFF_F = OFF_W2 + 3 * PL64x64;        // [64 p][128 k] x3
 constexpr uint32_t OFF_H1 = OFF_F + 3 * PL64x128;       // [64 p][64 i] x3
 constexpr uint32_t OFF_DZ2 = OFF_H1 + 3 * PL64x64;      // [64 p][64 j] x2 (the backward products use h, m)
-constexpr uint32_t OFF_DZ1 = OFF_DZ2 + 2 * PL64x64;     // [64 p][64 i] x2
-constexpr uint32_t OFF_GF = OFF_DZ1 + 2 * PL64x64;      // f32 [64][128]: lives until the next tile's gF
+#ifndef TC16_DZ1_ALIAS
+#define TC16_DZ1_ALIAS 1
+#endif
+// dz1 reuses h1's buffer: h1's last readers (z2, dW2) complete before the dz1 epilogue writes it,
+// and the next h1 is written after the gF || dW1 products have read dz1 -- the 16 KB go to L1,
+// which holds the encoder's gather reuse (the kernel is bound by L2 requests per SM)
+constexpr uint32_t OFF_DZ1 = TC16_DZ1_ALIAS ? OFF_H1 : OFF_DZ2 + 2 * PL64x64;  // [64 p][64 i] x2
+constexpr uint32_t OFF_GF = OFF_DZ2 + (TC16_DZ1_ALIAS ? 2 : 4) * PL64x64;  // f32 [64][128]: lives until the next tile's gF
 constexpr uint32_t OFF_X = OFF_GF + P * FE * 4;         // [2][P][3]
 constexpr uint32_t OFF_T = OFF_X + 2 * P * 3 * 4;       // [2][P]
 constexpr uint32_t OFF_HEAD = OFF_T + 2 * P * 4;        // [WQ][P] partial heads per lane-quarter warp
