@@ -28,6 +28,11 @@ struct TrainCtl {
   double l_rec, l_dens;
   double lr_main_t, bc1_main, bc2_main;  // this iteration's Adam scalars (main group)
   double lr_tf_t, bc1_tf, bc2_tf;        // this iteration's Adam scalars (transform group)
+  // batch generated one iteration ahead on the session's side stream (float sessions with the
+  // corner-replicated volume): its iteration index and skip flag, written by ctl_begin
+  int64_t gen_it;
+  int32_t gen_skip;
+  int32_t pad_;
 };
 
 template <typename T>

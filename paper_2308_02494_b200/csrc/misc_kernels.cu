@@ -162,8 +162,8 @@ __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __
 // in-place exclusive scan of kBuckets counts: one block of 1024 threads, 32 consecutive
 // counts per thread (vector loads), warp shuffles + one smem pass across warps
 constexpr int kBuckets = 32768;
-__global__ void __launch_bounds__(1024) k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl) {
-  if (ctl->skip) return;
+__global__ void __launch_bounds__(1024) k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl, int ahead) {
+  if (ahead ? ctl->gen_skip : ctl->skip) return;
   __shared__ int32_t wsum[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   int4* c4 = reinterpret_cast<int4*>(counts) + 8 * t;
@@ -351,9 +351,9 @@ __global__ void k_sample_sorted_cells(const double* __restrict__ c64, int64_t n,
 // pass.  Same values as k_batch_keys + k_bucket_scatter + k_sample_sorted_cells.
 __global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, const float4* __restrict__ cells, int w,
                                    int h, int d, float4* __restrict__ rec, uint32_t* __restrict__ key,
-                                   int32_t* __restrict__ counts, const TrainCtl* ctl) {
-  if (ctl->skip) return;
-  const uint64_t base = 3ull * uint64_t(batch) * uint64_t(ctl->it);
+                                   int32_t* __restrict__ counts, const TrainCtl* ctl, int ahead) {
+  if (ahead ? ctl->gen_skip : ctl->skip) return;
+  const uint64_t base = 3ull * uint64_t(batch) * uint64_t(ahead ? ctl->gen_it : ctl->it);
   const int cw = w > 1 ? w - 1 : 1, chh = h > 1 ? h - 1 : 1;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < batch; i += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t j = base + 3ull * uint64_t(i);
@@ -383,8 +383,8 @@ __global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, cons
 
 __global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
                                      int32_t* __restrict__ cursor, float* __restrict__ coords,
-                                     float* __restrict__ targets, const TrainCtl* ctl) {
-  if (ctl->skip) return;
+                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead) {
+  if (ahead ? ctl->gen_skip : ctl->skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pos = atomicAdd(&cursor[key[i]], 1);
     const float4 r = rec[i];

@@ -32,13 +32,13 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
 constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
                              uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
-__global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl);
+__global__ void k_bucket_scan(int32_t* __restrict__ counts, const TrainCtl* ctl, int ahead);
 __global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, const float4* __restrict__ cells, int w,
                                    int h, int d, float4* __restrict__ rec, uint32_t* __restrict__ key,
-                                   int32_t* __restrict__ counts, const TrainCtl* ctl);
+                                   int32_t* __restrict__ counts, const TrainCtl* ctl, int ahead);
 __global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
                                      int32_t* __restrict__ cursor, float* __restrict__ coords,
-                                     float* __restrict__ targets, const TrainCtl* ctl);
+                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead);
 __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
                                  int32_t* __restrict__ cursor, double* __restrict__ c64_out,
                                  int32_t* __restrict__ perm, const TrainCtl* ctl);
@@ -77,10 +77,13 @@ __global__ void k_ctl_begin(TrainCtl* ctl, CtlParams P, const double* __restrict
   if (threadIdx.x != 0) return;
   if (ctl->finished) {
     ctl->skip = 1;
+    ctl->gen_skip = 1;
     return;
   }
   ctl->skip = 0;
   const int64_t it = ctl->it;
+  ctl->gen_it = it + 1;
+  ctl->gen_skip = it + 1 >= P.iterations ? 1 : 0;
   const int64_t tm = ++ctl->t_main;
   ctl->lr_main_t = P.lr_main * ctl->lr_scale;
   ctl->bc1_main = bias[2 * (tm - 1)];
@@ -169,6 +172,17 @@ struct apmg_train_state {
   bool vol_owned = false;  // from the block cache (returned at destroy), else part of the workspace
   bool vol_cells = false;  // vol_bricked holds the corner-replicated cell copy (k_cell_volume)
   int nbx = 0, nby = 0;
+  // fused batch path (float session, corner-replicated volume, float REDs): the next iteration's
+  // batch is generated on a side stream while this iteration's Adam and density steps run, into
+  // the other of two (coords, targets) buffers (the second carved from c64_sorted, unused there)
+  bool fused = false, pipe = false;
+  void* coords_b[2] = {nullptr, nullptr};
+  void* targets_b[2] = {nullptr, nullptr};
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool batch_ready = false;  // the batch of the next iteration to run is in coords_b[host_it & 1]
+  int64_t host_it = 0;       // run_one calls so far (buffer parity)
+  int64_t graph_parity = 0;  // host_it & 1 when the graph was captured
 };
 
 constexpr int64_t kGraphIters = 8;
@@ -362,6 +376,22 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
       }
     }  // else no copy (sorting off, APMG_BRICKED=0, or no room): sample the row-major volume
   }
+  {
+    const char* efb = getenv("APMG_FUSED_BATCH");
+    const char* ep = getenv("APMG_BATCH_AHEAD");
+    s->fused = s->sort && shape->dtype == APMG_F32 && s->vol_cells && !s->perm && !(efb && efb[0] == '0');
+    s->pipe = s->fused && !(ep && ep[0] == '0');
+    s->coords_b[0] = s->coords;
+    s->targets_b[0] = s->targets;
+    if (s->pipe) {
+      const int64_t B = cfg->batch_size;
+      s->coords_b[1] = s->c64_sorted;                                   // 12 B of its 24 B per point
+      s->targets_b[1] = reinterpret_cast<float*>(s->c64_sorted) + 3 * B;  // + 4 B
+      APMG_CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+      APMG_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+      APMG_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+  }
   CtlParams& P = s->P;
   P.iterations = cfg->iterations;
   P.delay_start = cfg->delay_start;
@@ -425,23 +455,33 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
     }
   }
   APMG_LAUNCH("ctl_begin", k_ctl_begin, 1, 32, 0, st, s->ctl, s->P, s->dens_hist, s->bias);
-  const char* efb = getenv("APMG_FUSED_BATCH");
-  if (s->sort && sizeof(T) == 4 && s->vol_cells && !s->perm && !(efb && efb[0] == '0')) {
-    // float session, corner-replicated volume, default (float-RED) mode: targets sampled with the
-    // batch, (x, y, z, target) records bucketed straight into the recon inputs
-    APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
+  // this iteration's batch buffers (two alternate when the next batch is generated ahead)
+  const int cur = s->pipe ? int(s->host_it & 1) : 0;
+  T* coords = static_cast<T*>(s->coords_b[cur]);
+  T* targets = static_cast<T*>(s->targets_b[cur]);
+  // float session, corner-replicated volume, default (float-RED) mode: targets sampled with the
+  // batch, (x, y, z, target) records bucketed straight into the recon inputs; ahead = 1 generates
+  // the batch of iteration it + 1 (TrainCtl::gen_it)
+  auto fused_batch = [&](cudaStream_t bs, int ahead, void* cx, void* tx) -> int {
+    APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, bs));
     float4* rec = reinterpret_cast<float4*>(s->c64_raw);  // 16 of its 24 bytes per point
-    APMG_LAUNCH("batch_keys", k_batch_keys_cells, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B,
-                reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, rec, s->key, s->counts, s->ctl);
-    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
-    APMG_LAUNCH("bucket_scatter", k_bucket_scatter_rec, elementwise_grid(B, 8), 256, 0, st, rec, s->key, B,
-                s->counts, reinterpret_cast<float*>(s->coords), reinterpret_cast<float*>(s->targets), s->ctl);
+    APMG_LAUNCH("batch_keys", k_batch_keys_cells, elementwise_grid(B, 8), 256, 0, bs, c.key0, c.key1, B,
+                reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, rec, s->key, s->counts, s->ctl,
+                ahead);
+    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, bs, s->counts, s->ctl, ahead);
+    APMG_LAUNCH("bucket_scatter", k_bucket_scatter_rec, elementwise_grid(B, 8), 256, 0, bs, rec, s->key, B,
+                s->counts, static_cast<float*>(cx), static_cast<float*>(tx), s->ctl, ahead);
+    return APMG_OK;
+  };
+  if (s->fused && sizeof(T) == 4) {
+    if (!(s->pipe && s->batch_ready))
+      if (int rc = fused_batch(st, 0, coords, targets)) return rc;
   } else if (s->sort) {
     // batch -> spatial buckets (Morton order) -> permuted batch consumed by recon and density
     APMG_CUDA_TRY(cudaMemsetAsync(s->counts, 0, sizeof(int32_t) * kBuckets, st));
     APMG_LAUNCH("batch_keys", k_batch_keys, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->c64_raw, s->key,
                 s->counts, s->ctl);
-    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl);
+    APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, st, s->counts, s->ctl, 0);
     APMG_LAUNCH("bucket_scatter", k_bucket_scatter, elementwise_grid(B, 8), 256, 0, st, s->c64_raw, s->key, B,
                 s->counts, s->c64_sorted, s->perm, s->ctl);
     const double* sorted = s->c64_sorted;
@@ -452,46 +492,58 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
     }
     if (s->vol_cells)
       APMG_LAUNCH("train_batch", k_sample_sorted_cells<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
-                  reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, static_cast<T*>(s->coords),
-                  static_cast<T*>(s->targets), s->ctl);
+                  reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, coords,
+                  targets, s->ctl);
     else if (s->vol_bricked)
       APMG_LAUNCH("train_batch", k_sample_sorted_bricked<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
-                  s->vol_bricked, s->w, s->h, s->d, s->nbx, s->nby, static_cast<T*>(s->coords),
-                  static_cast<T*>(s->targets), s->ctl);
+                  s->vol_bricked, s->w, s->h, s->d, s->nbx, s->nby, coords,
+                  targets, s->ctl);
     else
       APMG_LAUNCH("train_batch", k_sample_sorted<T>, elementwise_grid(B, 8), 256, 0, st, sorted, B,
-                  s->volume, s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+                  s->volume, s->w, s->h, s->d, coords, targets, s->ctl);
   } else {
     APMG_LAUNCH("train_batch", k_train_batch<T>, elementwise_grid(B, 8), 256, 0, st, c.key0, c.key1, B, s->volume,
-                s->w, s->h, s->d, static_cast<T*>(s->coords), static_cast<T*>(s->targets), s->ctl);
+                s->w, s->h, s->d, coords, targets, s->ctl);
   }
-  int rc = launch_recon<T>(md, B, static_cast<const T*>(s->coords), static_cast<const T*>(s->targets),
+  int rc = launch_recon<T>(md, B, coords, targets,
                            static_cast<T*>(s->sq), nullptr,
                            s->gradx ? reinterpret_cast<T*>(s->gradx) : grad + s->off[0], grad + s->off[1],
                            grad + s->off[2],
                            grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);
   if (rc) return rc;
-#ifdef APMG_ABL_FREEZE  // timing builds only: parameters frozen (no Adam, no density step), so
-  // ablated kernels computing wrong values cannot change later iterations' inputs
-  if (m.grids > 0) {
+  if (s->pipe && sizeof(T) == 4) {  // the next iteration's batch, concurrent with Adam + density
+    APMG_CUDA_TRY(cudaEventRecord(s->ev_fork, st));
+    APMG_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    if (int rc2 = fused_batch(s->side, 1, s->coords_b[cur ^ 1], s->targets_b[cur ^ 1])) return rc2;
+    APMG_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
+  }
+  // end of the iteration: controller, then join the side stream (the next iteration's recon
+  // reads the batch it generated)
+  auto finish = [&]() -> int {
     APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
                 s->plat_ring, s->trig);
+    if (s->pipe && sizeof(T) == 4) {
+      APMG_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_join, 0));
+      s->batch_ready = true;
+    }
+    ++s->host_it;
     return APMG_OK;
-  }
+  };
+#ifdef APMG_ABL_FREEZE  // timing builds only: parameters frozen (no Adam, no density step), so
+  // ablated kernels computing wrong values cannot change later iterations' inputs
+  if (m.grids > 0) return finish();
 #endif
   APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
               static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
               reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx), s->gfx,
               s->fx_elems);
   if (c.train_transforms) {
-    rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, static_cast<const T*>(s->coords),
+    rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, coords,
                               static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),
                               static_cast<T*>(s->tv), s->dens_ws, s->dens_wsb, s->ctl, st, pre_nb);
     if (rc) return rc;
   }
-  APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
-              s->plat_ring, s->trig);
-  return APMG_OK;
+  return finish();
 }
 
 static int run_direct(apmg_train_state* s, cudaStream_t st) {
@@ -522,6 +574,7 @@ extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
       APMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       APMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
       const uint64_t c0 = launch_counter().load();
+      s->graph_parity = s->host_it & 1;
       for (int64_t i = 0; i < kGraphIters && rc == 0; ++i) rc = run_direct(s, cs);
       cudaGraph_t g = nullptr;
       const cudaError_t ec = cudaStreamEndCapture(cs, &g);
@@ -544,9 +597,16 @@ extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
         return APMG_E_CUDA;
       }
     }
-    for (; n - done >= kGraphIters; done += kGraphIters) {
+    // the graph's buffer parity is fixed at capture (kGraphIters is even): one direct iteration
+    // realigns after an odd number of direct ones
+    if (s->pipe && (s->host_it & 1) != s->graph_parity && n - done > kGraphIters) {
+      if (int rc = run_direct(s, st)) return rc;
+      ++done;
+    }
+    for (; n - done >= kGraphIters && (!s->pipe || (s->host_it & 1) == s->graph_parity); done += kGraphIters) {
       APMG_CUDA_TRY(cudaGraphLaunch(s->graph, st));
       launch_counter().fetch_add(s->graph_launches);
+      s->host_it += kGraphIters;
     }
   }
   for (; done < n; ++done) {
@@ -605,6 +665,12 @@ extern "C" int apmg_train_log(apmg_train_state* s, double* l_rec, double* l_dens
 
 extern "C" int apmg_train_destroy(apmg_train_state* s) {
   if (s && s->graph) cudaGraphExecDestroy(s->graph);
+  if (s && s->side) {
+    cudaStreamSynchronize(s->side);
+    cudaStreamDestroy(s->side);
+  }
+  if (s && s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s && s->ev_join) cudaEventDestroy(s->ev_join);
   if (s && s->vol_bricked && s->vol_owned) {
     cudaDeviceSynchronize();  // as cudaFree would: no launch may still read the block
     pool_free(s->vol_bricked, s->vol_bricked_bytes);

@@ -45,7 +45,16 @@ def full_capture(rep):
             "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors",
             "lts__t_sectors_srcunit_tex_op_red.sum": "l2_red_sectors",
             "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum": "l1_ld_hit_sectors",
-            "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum": "l1_ld_sectors"}
+            "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum": "l1_ld_sectors",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "l1_shared_wavefronts",
+            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "tc_smem_wavefront_pct",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
+            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_sb",
+            "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio": "stall_short_sb",
+            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio": "stall_barrier",
+            "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait"}
     idx = {k: hdr.index(k) for k in want if k in hdr}
     scale = {"sector": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
              "msecond": 1e-3, "second": 1}
@@ -62,6 +71,10 @@ def full_capture(rep):
             except ValueError:
                 continue
             d[want[k]] = f * scale.get(units[i], 1)
+        if d.get("dur") and d.get("l2_sectors"):  # achieved L2 throughput (all lts__t sectors x 32 B)
+            d["l2_GBps"] = 32.0 * d["l2_sectors"] / (d["dur"] * 1e-3) / 1e9  # dur in ms (ncu unit)
+        if d.get("dur") and d.get("dram_read") is not None:
+            d["dram_GBps"] = (d["dram_read"] + d.get("dram_write", 0.0)) / (d["dur"] * 1e-3) / 1e9
         out.append(d)
     return out
 
