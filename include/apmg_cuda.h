@@ -97,6 +97,13 @@ int apmg_composite_rgba(const float* samples, const float* steps, int64_t nr, in
  * copy of apmg_train_create).  No reference counterpart (memory management of the CUDA
  * path). */
 int apmg_release_cached(void);
+/* Page-lock an existing host range in place (cudaHostRegister) so uploads from it are single DMA
+ * transfers, and undo it.  Host plumbing for Volume.device_data / to_device (volume.py:225-241
+ * loads the volume the reference samples in trainer.py:189); not part of the reference API. */
+int apmg_host_register(void* ptr, size_t bytes);
+int apmg_host_unregister(void* ptr);
+/* host -> device copy on `stream` (cudaMemcpyAsync; a DMA when the host range is page-locked) */
+int apmg_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int apmg_kernel_timing_enable(int on);
 /* copies up to `cap` records (name, total_ms, launches); returns count.  Synchronises. */
 int apmg_kernel_timing_read(char* names /* cap*64 bytes */, double* total_ms, int64_t* launches, int cap);

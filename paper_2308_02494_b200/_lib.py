@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -53,6 +54,9 @@ SIGNATURES = {
     "apmg_device_sm_count": (C.c_int, []),
     "apmg_launch_count": (C.c_uint64, []),
     "apmg_release_cached": (C.c_int, []),
+    "apmg_host_register": (C.c_int, [_P, C.c_size_t]),
+    "apmg_host_unregister": (C.c_int, [_P]),
+    "apmg_copy_h2d": (C.c_int, [_P, _P, C.c_size_t, _P]),
     "apmg_forward_tc": (C.c_int, [_MP, _P, _I64, _P, _P]),
     "apmg_generate_rays": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int32, _P, _P]),
     "apmg_ray_box_hits": (C.c_int, [C.POINTER(C.c_double), _P, _I64, _P, _P, _P, _P]),
@@ -205,6 +209,19 @@ def _staging():
     return _stage
 
 
+def _ramped_chunks(n: int):
+    """(offset, size) pieces of an n-byte transfer: sizes doubling from 2 MiB up to the slot size,
+    so the first DMA starts after a short host copy instead of a full-slot one (the pipeline's
+    start-up latency was a quarter of a 512 MiB upload)."""
+    out, o, m = [], 0, min(2 << 20, _STAGE_BYTES)
+    while o < n:
+        k = min(m, n - o)
+        out.append((o, k))
+        o += k
+        m = min(2 * m, _STAGE_BYTES)
+    return out
+
+
 def __upload_staged_locked(a: np.ndarray, out) -> None:
     """Pageable host array -> device tensor through the pinned ring: host threads fill the
     slots (numpy copies release the GIL) while the copy engine drains the filled ones, so
@@ -215,7 +232,7 @@ def __upload_staged_locked(a: np.ndarray, out) -> None:
     src = a.reshape(-1).view(np.uint8)
     dst = out.view(-1).view(t.uint8)
     n = src.size
-    chunks = [(o, min(_STAGE_BYTES, n - o)) for o in range(0, n, _STAGE_BYTES)]
+    chunks = _ramped_chunks(n)
     st = t.cuda.current_stream()
 
     def fill(slot, o, m):
@@ -294,14 +311,62 @@ def _upload_view_locked(view: np.ndarray, out) -> None:
     st.synchronize()
 
 
-def to_device(arr: np.ndarray, dtype=None):
+# Host arrays of PIN_MIN bytes and more (a volume) are page-locked in place on their first upload
+# (cudaHostRegister) and unregistered when numpy frees them: later uploads of the same array are
+# one DMA at the link rate instead of the staging ring's host copy + DMA pipeline.  APMG_PIN_HOST=0
+# keeps every upload on the ring.
+_PIN_MIN = 64 << 20
+_pinned = {}  # data pointer -> nbytes of the ranges registered by pin_host
+_pin_lock = __import__("threading").Lock()
+
+
+def _owner(a: np.ndarray):
+    while isinstance(a, np.ndarray) and a.base is not None:
+        a = a.base
+    return a
+
+
+def _unpin(ptr: int) -> None:
+    with _pin_lock:
+        if _pinned.pop(ptr, None) is not None and _lib is not None:
+            _lib.apmg_host_unregister(ptr)
+
+
+def pin_host(a: np.ndarray) -> bool:
+    """Page-lock the memory of a C-contiguous array that owns (a whole range of) its buffer;
+    False when it cannot be (a memory map, a foreign owner, the driver refused)."""
+    if not env_flag_default("APMG_PIN_HOST", True) or not a.flags.c_contiguous or a.nbytes < _PIN_MIN:
+        return False
+    ptr = a.ctypes.data
+    with _pin_lock:
+        if ptr in _pinned:
+            return _pinned[ptr] >= a.nbytes
+    own = _owner(a)
+    if not isinstance(own, np.ndarray) or isinstance(own, np.memmap) or own.ctypes.data != ptr or own.nbytes != a.nbytes:
+        return False
+    if lib().apmg_host_register(ptr, a.nbytes) != 0:
+        return False
+    with _pin_lock:
+        _pinned[ptr] = a.nbytes
+    weakref.finalize(own, _unpin, ptr)
+    return True
+
+
+def to_device(arr: np.ndarray, dtype=None, sync: bool = True):
     """Host numpy -> contiguous CUDA tensor (plumbing only); arrays of 4 MiB and more go
-    through the pinned staging ring."""
+    through the pinned staging ring, or -- page-locked in place (pin_host) -- as one DMA.
+    sync=False returns while that DMA may still run (stream-ordered for device consumers; the
+    caller keeps the host array unchanged until the stream passes the copy)."""
     t = require_cuda()
     a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
     if a.nbytes >= (4 << 20):
         out = t.empty(a.shape, dtype=t.from_numpy(a[:0].reshape(-1)).dtype, device=device())
-        _upload_staged(a, out)
+        if pin_host(a):
+            check(lib().apmg_copy_h2d(ptr(out), a.ctypes.data, a.nbytes, stream_handle()), "copy_h2d")
+            if sync or a is not arr:  # a temporary (converted) copy must outlive the DMA
+                t.cuda.current_stream().synchronize()
+        else:
+            _upload_staged(a, out)
         return out
     return t.from_numpy(a).to(device(), non_blocking=False)
 
@@ -332,7 +397,10 @@ def _download_into_locked(dev, out: np.ndarray) -> None:
         raise ValueError(f"download_into: {src.numel()} device bytes into a {n}-byte host array")
     bufs, events, pool = _staging()
     st = t.cuda.current_stream()
-    chunks = [(o, min(_STAGE_BYTES, n - o)) for o in range(0, n, _STAGE_BYTES)]
+    # sizes ramping DOWN to 2 MiB at the end: the last host drain (not overlapped) stays short
+    sizes = [k for _, k in _ramped_chunks(n)][::-1]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64) if sizes else []
+    chunks = [(int(o), int(k)) for o, k in zip(offs, sizes)]
     futs = [None] * _STAGE_SLOTS
 
     def drain(slot, ev, o, m):
@@ -382,6 +450,11 @@ def exported_symbols() -> list[str]:
 
 def env_flag(name: str) -> bool:
     return os.environ.get(name, "") not in ("", "0", "false", "False")
+
+
+def env_flag_default(name: str, default: bool) -> bool:
+    v = os.environ.get(name)
+    return default if v is None or v == "" else v not in ("0", "false", "False")
 
 
 def _upload_staged(*args, **kw):

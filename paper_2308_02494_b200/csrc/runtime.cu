@@ -156,6 +156,24 @@ void stream_free(void* p, cudaStream_t st) {
 
 using namespace apmg;
 
+extern "C" int apmg_host_register(void* ptr, size_t bytes) {
+  APMG_ARG_CHECK(ptr != nullptr && bytes > 0, "null or empty host range");
+  APMG_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return APMG_OK;
+}
+
+extern "C" int apmg_host_unregister(void* ptr) {
+  APMG_ARG_CHECK(ptr != nullptr, "null host pointer");
+  APMG_CUDA_TRY(cudaHostUnregister(ptr));
+  return APMG_OK;
+}
+
+extern "C" int apmg_copy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  APMG_ARG_CHECK(dst != nullptr && src != nullptr, "null pointer");
+  APMG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  return APMG_OK;
+}
+
 extern "C" int apmg_release_cached(void) {
   release_pool();
   return APMG_OK;

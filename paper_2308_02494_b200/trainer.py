@@ -170,8 +170,43 @@ class hold_block_cache:
 
     def __exit__(self, *exc):
         _cache_holders[0] -= 1
-        if _cache_holders[0] == 0 and L._lib is not None:  # nothing cached before the library loads
-            L.lib().apmg_release_cached()
+        if _cache_holders[0] == 0:
+            release_parked_workspace()
+            if L._lib is not None:  # nothing cached before the library loads
+                L.lib().apmg_release_cached()
+
+
+# One parked session workspace (the largest buffer of a session: ~4 GiB at C2 with the sampler's
+# corner-replicated volume copy): inside hold_block_cache a closing session parks it and the next
+# one takes it when it is large enough, so back-to-back sessions (repeated train_single calls, the
+# bricks of train_decomposed) skip the allocation whatever the caching allocator's state; outside
+# it the workspace goes back to torch at close.  Concurrent sessions allocate their own.
+_ws_park = {"t": None}
+_ws_lock = __import__("threading").Lock()
+
+
+def _take_workspace(nbytes: int):
+    with _ws_lock:
+        t = _ws_park["t"]
+        if t is not None and t.numel() >= nbytes:
+            _ws_park["t"] = None
+            return t[:nbytes]
+    return L.workspace(nbytes)
+
+
+def _park_workspace(t) -> None:
+    if t is None or _cache_holders[0] == 0:  # parked only inside hold_block_cache
+        return
+    base = t._base if t._base is not None else t
+    with _ws_lock:
+        cur = _ws_park["t"]
+        if cur is None or cur.numel() < base.numel():
+            _ws_park["t"] = base
+
+
+def release_parked_workspace() -> None:
+    with _ws_lock:
+        _ws_park["t"] = None
 
 
 class TrainSession:
@@ -186,6 +221,10 @@ class TrainSession:
         if dt not in (np.float32, np.float64):
             raise TypeError(f"unsupported model dtype {dt}")
         self.dt = dt
+        # the volume goes first: from page-locked host memory its DMA runs while the parameters
+        # are staged and uploaded behind it on the same stream (setup_ms["volume"] = issue + wait)
+        self.vol = volume.device_data(sync=False)
+        tv = time.perf_counter()
         self.dm = DeviceModel.upload(model)
         off = (C.c_int64 * 5)()
         L.check(L.lib().apmg_main_layout(C.byref(self.dm.desc), off), "main_layout")
@@ -198,7 +237,6 @@ class TrainSession:
         self.main[o[3]:o[3] + self.dm.w3.numel()].copy_(self.dm.w3.reshape(-1))
         self.tf = self.dm.transforms
         t1 = time.perf_counter()
-        self.vol = volume.device_data()
         t.cuda.current_stream().synchronize()
         t2 = time.perf_counter()
         key = np.random.Philox(cfg.seed).state["state"]["key"]
@@ -213,7 +251,7 @@ class TrainSession:
         # session workspace + the sampler's private copy of the volume, both from torch's caching
         # allocator (reused by back-to-back sessions, released by torch under memory pressure)
         need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
-        self.ws = L.workspace((need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d))
+        self.ws = _take_workspace((need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d))
         t3 = time.perf_counter()
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()
@@ -224,7 +262,7 @@ class TrainSession:
         self.state = st
         self._torch = t
         # host-side setup split (ms): parameters, volume upload, workspace + create (synchronised)
-        self.setup_ms = {"params": 1e3 * (t1 - t0), "volume": 1e3 * (t2 - t1), "workspace": 1e3 * (t3 - t2),
+        self.setup_ms = {"params": 1e3 * (t1 - tv), "volume": 1e3 * ((tv - t0) + (t2 - t1)), "workspace": 1e3 * (t3 - t2),
                          "create": 1e3 * (time.perf_counter() - t3)}
 
     def run(self, n: int) -> None:
@@ -309,6 +347,10 @@ class TrainSession:
         if self.state:
             L.lib().apmg_train_destroy(self.state)
             self.state = None
+        # the workspace (incl. the sampler's 8x volume copy) is parked for the next session now, not
+        # released when the garbage collector gets to this one
+        _park_workspace(getattr(self, "ws", None))
+        self.ws = None
 
     def __del__(self):
         try:

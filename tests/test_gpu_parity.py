@@ -826,3 +826,28 @@ def test_batch_ahead_pipeline_matches_inline(monkeypatch):
         got = run("1", splits)
         np.testing.assert_allclose(got[0], ref[0], rtol=2e-4)
         np.testing.assert_allclose(got[1], ref[1], rtol=2e-3)
+
+
+@pytest.mark.gpu
+def test_pinned_in_place_upload(monkeypatch):
+    """Host arrays of 64 MiB and more are page-locked in place on upload (pin_host) and copied as
+    one DMA; the device copy is bit-exact, views that do not own their buffer and APMG_PIN_HOST=0
+    go through the staging ring, and freeing the array unregisters its pages."""
+    import gc
+    a = np.random.default_rng(3).random((80, 512, 512), dtype=np.float32)  # 80 MiB
+    ptr = a.ctypes.data
+    d = L.to_device(a)
+    assert ptr in L._pinned
+    assert np.array_equal(L.to_host(d), a)
+    assert np.array_equal(L.to_host(L.to_device(a)), a)  # second upload: already registered
+    v = a[1:]  # a view: not registered itself, staged
+    assert np.array_equal(L.to_host(L.to_device(v)), v)
+    assert v.ctypes.data not in L._pinned
+    del v, d
+    del a
+    gc.collect()
+    assert ptr not in L._pinned
+    monkeypatch.setenv("APMG_PIN_HOST", "0")
+    b = np.random.default_rng(4).random((80, 512, 512), dtype=np.float32)
+    assert np.array_equal(L.to_host(L.to_device(b)), b)
+    assert b.ctypes.data not in L._pinned
