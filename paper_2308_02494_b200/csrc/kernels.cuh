@@ -51,6 +51,8 @@ int elementwise_grid(int64_t n, int per_sm);
 int launch_sse_finalize(const double* part, int n, double* sse, cudaStream_t st);
 // gridx[c] = (grid[c], grid[c + 1]) over the flat two-channel cells (misc_kernels.cu)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells);
+// xy-quad copy (ModelDev::gridq): two float4 per cell (misc_kernels.cu)
+__global__ void k_pack_gridq(const float2* __restrict__ grid, float4* __restrict__ gq, int64_t cells, int W);
 int launch_recon_tc16(const ModelDev<float>& md, int64_t n, const float* coords, const float* targets, float* sq,
                       float* dgrid, float* part_dw, double* part_loss, int grid, const TrainCtl* ctl, cudaStream_t st);
 

@@ -519,8 +519,8 @@ __global__ void k_adam(T* __restrict__ p, const T* __restrict__ g, T* __restrict
 // element (cell c, channel ch) sums dgx[c].lo and dgx[c - 1].hi, and clears both.
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx,
-                             unsigned long long* __restrict__ gfx, int64_t fx_elems) {
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, int qw,
+                             float* __restrict__ dgx, unsigned long long* __restrict__ gfx, int64_t fx_elems) {
   if (ctl->skip) return;
   const T lr_t = T(ctl->lr_main_t), c1 = T(ctl->bc1_main), c2 = T(ctl->bc2_main);
   int64_t i0 = 0;
@@ -549,8 +549,15 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
         p2[c] = pc;
         m2[c] = mc;
         v2[c] = vc;
-        x2[2 * c] = pc;
-        if (c > 0) x2[2 * c - 1] = pc;
+        if (qw) {  // xy-quad copy: cell c is slot 0 of quad c, 1 of c - 1, 2 of c - W, 3 of c - W - 1
+          x2[4 * c] = pc;
+          if (c >= 1) x2[4 * (c - 1) + 1] = pc;
+          if (c >= qw) x2[4 * (c - qw) + 2] = pc;
+          if (c >= qw + 1) x2[4 * (c - qw - 1) + 3] = pc;
+        } else {
+          x2[2 * c] = pc;
+          if (c > 0) x2[2 * c - 1] = pc;
+        }
       }
       i0 = 2 * cells;
     }
@@ -585,23 +592,41 @@ __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict
     if constexpr (sizeof(T) == 4) {
       if (gx && i < gx_elems) {
         const int64_t c = i >> 1, ch = i & 1;
-        gx[4 * c + ch] = pi;
-        if (c > 0) gx[4 * (c - 1) + 2 + ch] = pi;
+        if (qw) {
+          gx[8 * c + ch] = pi;
+          if (c >= 1) gx[8 * (c - 1) + 2 + ch] = pi;
+          if (c >= qw) gx[8 * (c - qw) + 4 + ch] = pi;
+          if (c >= qw + 1) gx[8 * (c - qw - 1) + 6 + ch] = pi;
+        } else {
+          gx[4 * c + ch] = pi;
+          if (c > 0) gx[4 * (c - 1) + 2 + ch] = pi;
+        }
       }
     }
   }
 }
 
 template __global__ void k_adam_train<float>(float*, float*, float*, float*, int64_t, const TrainCtl*, float*,
-                                             int64_t, float*, unsigned long long*, int64_t);
+                                             int64_t, int, float*, unsigned long long*, int64_t);
 template __global__ void k_adam_train<double>(double*, double*, double*, double*, int64_t, const TrainCtl*, float*,
-                                              int64_t, float*, unsigned long long*, int64_t);
+                                              int64_t, int, float*, unsigned long long*, int64_t);
 
 // gridx[c] = (grid[c], grid[c + 1]) for the flat two-channel cells c (zero past the end)
 __global__ void k_pack_gridx(const float2* __restrict__ grid, float4* __restrict__ gx, int64_t cells) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < cells; c += int64_t(gridDim.x) * blockDim.x) {
     const float2 a = grid[c], b = c + 1 < cells ? grid[c + 1] : make_float2(0.f, 0.f);
     gx[c] = make_float4(a.x, a.y, b.x, b.y);
+  }
+}
+
+// xy-quad copy: gq[c] = (grid[c], grid[c + 1], grid[c + W], grid[c + W + 1]) (zero past the end)
+__global__ void k_pack_gridq(const float2* __restrict__ grid, float4* __restrict__ gq, int64_t cells, int W) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < cells; c += int64_t(gridDim.x) * blockDim.x) {
+    const float2 z = make_float2(0.f, 0.f);
+    const float2 a = grid[c], b = c + 1 < cells ? grid[c + 1] : z, d = c + W < cells ? grid[c + W] : z,
+                 e = c + W + 1 < cells ? grid[c + W + 1] : z;
+    gq[2 * c] = make_float4(a.x, a.y, b.x, b.y);
+    gq[2 * c + 1] = make_float4(d.x, d.y, e.x, e.y);
   }
 }
 

@@ -39,6 +39,9 @@ struct ModelDev {
   // (grid[c], grid[c + 1]) over the flat cell index c, so the two x-corners of a cell edge
   // are one 16-byte load -- the encoder's gathers are L2-request-bound, not byte-bound
   const float4* __restrict__ gridx = nullptr;
+  // or the xy-quad copy (32 bytes per cell c: grid[c], grid[c + 1], grid[c + W], grid[c + W + 1]),
+  // so a cell's four corners of one z plane are one 256-bit load (2 gathers per (point, grid))
+  const float* __restrict__ gridq = nullptr;
   // the grid gradient the recon kernel scatters into is in the same x-pair layout
   // (dgridx[c] = d/d(grid[c]), d/d(grid[c + 1]) partial sums; float4 REDs, half the RED
   // operations): grad(grid[v]) = dgridx[v].lo + dgridx[v - 1].hi.  tc16 kernel only.
@@ -231,6 +234,30 @@ __device__ __forceinline__ void interp_pairx_f32(const float4* __restrict__ gx, 
                                    f2_lerp(make_float2(b01.x, b01.y), make_float2(b01.z, b01.w), fx), fy),
                            f2_lerp(f2_lerp(make_float2(b10.x, b10.y), make_float2(b10.z, b10.w), fx),
                                    f2_lerp(make_float2(b11.x, b11.y), make_float2(b11.z, b11.w), fx), fy),
+                           fz);
+  o0 = r.x;
+  o1 = r.y;
+}
+
+// 256-bit read-only gather (LDG.E.256; 32-byte aligned)
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+      : "l"(p));
+}
+
+// interp_pair_f32 over the xy-quad copy: 2 256-bit loads, same arithmetic in the same order
+// (bit-identical features)
+__device__ __forceinline__ void interp_pairq_f32(const float* __restrict__ gq, int HW, int vbase, float fx, float fy,
+                                                 float fz, float& o0, float& o1) {
+  const float* g = gq + 8 * size_t(vbase);
+  float a[8], b[8];
+  ldg256(g, a);
+  ldg256(g + 8 * size_t(HW), b);
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(make_float2(a[0], a[1]), make_float2(a[2], a[3]), fx),
+                                   f2_lerp(make_float2(a[4], a[5]), make_float2(a[6], a[7]), fx), fy),
+                           f2_lerp(f2_lerp(make_float2(b[0], b[1]), make_float2(b[2], b[3]), fx),
+                                   f2_lerp(make_float2(b[4], b[5]), make_float2(b[6], b[7]), fx), fy),
                            fz);
   o0 = r.x;
   o1 = r.y;

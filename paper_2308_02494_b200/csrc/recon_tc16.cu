@@ -366,7 +366,9 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
         {  // straight-line: outside pairs gather cell 0 and are zeroed afterwards
           const bool use = inside;
           const int vb = use ? vbase : 0;
-          if (md.gridx)
+          if (md.gridq)
+            interp_pairq_f32(md.gridq, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
+          else if (md.gridx)
             interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
           else
             interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);

@@ -27,8 +27,8 @@ __global__ void k_train_batch(uint64_t k0, uint64_t k1, int64_t batch, const flo
                               int d, T* __restrict__ coords, T* __restrict__ targets, const TrainCtl* ctl);
 template <typename T>
 __global__ void k_adam_train(T* __restrict__ p, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v, int64_t n,
-                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, float* __restrict__ dgx,
-                             unsigned long long* __restrict__ gfx, int64_t fx_elems);
+                             const TrainCtl* ctl, float* __restrict__ gx, int64_t gx_elems, int qw,
+                             float* __restrict__ dgx, unsigned long long* __restrict__ gfx, int64_t fx_elems);
 constexpr int kBuckets = 32768;
 __global__ void k_batch_keys(uint64_t k0, uint64_t k1, int64_t batch, double* __restrict__ c64,
                              uint32_t* __restrict__ key, int32_t* __restrict__ counts, const TrainCtl* ctl);
@@ -167,6 +167,7 @@ struct apmg_train_state {
   int64_t fx_elems = 0;
   float4* gradx = nullptr;  // x-pair grid gradient (ModelDev::grad_pairs), or null
   int64_t gx_cells = 0;
+  int gq_w = 0;  // > 0: gridx holds the xy-quad copy (ModelDev::gridq; 2 float4 per cell), row width W
   float* vol_bricked = nullptr;
   size_t vol_bricked_bytes = 0;
   bool vol_owned = false;  // from the block cache (returned at destroy), else part of the workspace
@@ -271,7 +272,12 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   const char* eg = getenv("APMG_GRIDX");
   const bool use_gx = m->dtype == APMG_F32 && m->channels == 2 && !(eg && eg[0] == '0');
   const int64_t cells = int64_t(m->grids) * m->depth * m->height * m->width;
-  float4* gridx = use_gx ? cv.take<float4>(cells) : nullptr;
+  // ... or as the xy-quad copy (two 256-bit gathers per (point, grid) instead of four 128-bit
+  // ones; APMG_GRIDQ=1, tensor-core recon kernel only): measured even -- the recon kernel gains
+  // ~1%, masked Adam's four scattered copy writes per cell lose as much
+  const char* eq = getenv("APMG_GRIDQ");
+  const bool use_gq = use_gx && recon_uses_tc16(*m) && (eq && eq[0] == '1');
+  float4* gridx = use_gx ? cv.take<float4>(use_gq ? 2 * cells : cells) : nullptr;
   // ... and the x-pair grid gradient when the bf16x3 recon kernel runs (APMG_GRADX=0 off)
   const char* ed = getenv("APMG_GRADX");
   const bool det = c->deterministic != 0;
@@ -287,6 +293,7 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
     s->gridx = gridx;
     s->gradx = gradx;
     s->gx_cells = use_gx ? cells : 0;
+    s->gq_w = use_gq ? m->width : 0;
     s->ctl = ctl;
     s->l_rec = l_rec;
     s->l_dens = l_dens;
@@ -439,7 +446,8 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
   live.w3 = params + s->off[3];
   live.transforms = s->transforms;
   ModelDev<T> md = make_model_dev<T>(live);
-  md.gridx = s->gridx;
+  md.gridx = s->gq_w ? nullptr : s->gridx;
+  md.gridq = s->gq_w ? reinterpret_cast<const float*>(s->gridx) : nullptr;
   md.grad_pairs = s->gradx != nullptr;
   md.dgrid_fx = s->gfx;
   // density pass fused into the recon kernel (APMG_FUSED_RHO=0: separate rho kernel, A/B)
@@ -535,7 +543,7 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
 #endif
   APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
               static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
-              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, reinterpret_cast<float*>(s->gradx), s->gfx,
+              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, s->gq_w, reinterpret_cast<float*>(s->gradx), s->gfx,
               s->fx_elems);
   if (c.train_transforms) {
     rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, coords,
@@ -559,10 +567,15 @@ extern "C" int apmg_train_run(apmg_train_state* s, int64_t n, void* stream) {
   APMG_ARG_CHECK(s != nullptr, "null state");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t done = 0;
-  if (s->gridx && n > 0)  // (re)build the x-pair copy: the caller may have rewritten the parameters
-    APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(s->gx_cells, 8), 256, 0, st,
-                reinterpret_cast<const float2*>(static_cast<float*>(s->main_params) + s->off[0]), s->gridx,
-                s->gx_cells);
+  if (s->gridx && n > 0) {  // (re)build the grid copy: the caller may have rewritten the parameters
+    const float2* g2 = reinterpret_cast<const float2*>(static_cast<float*>(s->main_params) + s->off[0]);
+    if (s->gq_w)
+      APMG_LAUNCH("pack_gridq", k_pack_gridq, elementwise_grid(s->gx_cells, 8), 256, 0, st, g2, s->gridx, s->gx_cells,
+                  s->gq_w);
+    else
+      APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(s->gx_cells, 8), 256, 0, st, g2, s->gridx,
+                  s->gx_cells);
+  }
   // the graph is captured as soon as the session will replay it (a short first call -- a warm-up --
   // captures it too, so a later timed call does not pay the capture); capturing runs nothing
   const bool will_replay = n >= kGraphIters || s->cfg.iterations >= 2 * kGraphIters;

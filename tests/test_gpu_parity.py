@@ -804,8 +804,10 @@ def test_batch_ahead_pipeline_matches_inline(monkeypatch):
     into the other of two buffers (APMG_BATCH_AHEAD, default on).  Against inline generation
     (APMG_BATCH_AHEAD=0), and across run() splits that exercise the direct iterations, the graph
     capture and the buffer-parity realignment (1 + 8 captured, then 3 direct, then 8 / 8), every
-    iteration sees the same batch: the losses agree to float-RED noise (a wrong or stale batch moves
-    l_rec by orders of magnitude more)."""
+    iteration sees the same batch: the losses agree to float-RED noise.  The grid gradient is summed
+    with float REDs, so two runs differ in the last bits from iteration 0 and the difference grows
+    along the trajectory (measured: 2.8e-4 relative by iteration 28 between two correct runs); the
+    gate is the per-tensor gradient gate, 2e-3; a wrong or stale batch moves l_rec by far more."""
     vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
 
     def run(ahead, splits):
@@ -824,7 +826,7 @@ def test_batch_ahead_pipeline_matches_inline(monkeypatch):
     ref = run("0", [28])
     for splits in ([28], [9, 3, 8, 8], [1, 1, 9, 17]):
         got = run("1", splits)
-        np.testing.assert_allclose(got[0], ref[0], rtol=2e-4)
+        np.testing.assert_allclose(got[0], ref[0], rtol=2e-3)
         np.testing.assert_allclose(got[1], ref[1], rtol=2e-3)
 
 
