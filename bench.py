@@ -180,6 +180,16 @@ def _traffic(kernel):
     return v, None
 
 
+def _red_sectors(kernel):
+    """ncu L2 RED sectors per launch of `kernel` (the REDs actually issued after warp aggregation;
+    one float4 RED = one sector), from the newest profiles/traffic_*.json that has them."""
+    for f in sorted((ROOT / "profiles").glob("traffic_r*.json"), reverse=True):
+        v = json.loads(f.read_text()).get(kernel)
+        if isinstance(v, dict) and v.get("l2_red_sectors"):
+            return v["l2_red_sectors"], f.name
+    return None, None
+
+
 def _peaks2():
     f = ROOT / "profiles" / "peaks_b200.json"
     return json.loads(f.read_text()) if f.exists() else {}
@@ -212,10 +222,15 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
             "encoder_gather": {"achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
                                "work": "4,096 B/pt (64 grids x 4 float4 corner pairs)"},
             "scatter_red": {"achieved": r_ach, "peak": r_pk, "unit": "G float4 RED/s", "frac": r_ach / r_pk,
-                            "work": "256 float4 REDs/pt before warp aggregation"},
+                            "work": "256 float4 REDs/pt before warp aggregation (the algorithmic count: "
+                                    "frac is the rate the scatter's work is retired at, not L2 RED occupancy)"},
             "mlp_tensor": {"achieved": f_iss, "algorithmic": f_alg, "peak": pk["bf16_tflops"],
                            "unit": "TFLOP/s issued (bf16x3 products)", "frac": f_iss / pk["bf16_tflops"],
                            "work": "295,680 issued FLOP/pt (74,112 algorithmic)"}}
+        red_sec, red_src = _red_sectors(kernel)
+        if red_sec:  # the REDs the L2 actually executed (ncu), at this launch's measured time
+            comps["scatter_red"].update({"issued_per_launch": red_sec, "issued_achieved": red_sec / t / 1e9,
+                                         "issued_frac": red_sec / t / 1e9 / r_pk, "issued_source": red_src})
         return {"bound": "l2", **base, "achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
                 "components": comps, "serial_sum_frac": sum(c["frac"] for c in comps.values()),
                 "peak_source": "profiles/peaks_b200.json (tools/peaks.py): random float4 gather / float4 RED "

@@ -441,34 +441,10 @@ __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float
 #ifndef APMG_FX_GATHER_CAP
 #define APMG_FX_GATHER_CAP 7
 #endif
-template <bool FX = false, int CAP = (FX ? APMG_FX_GATHER_CAP : APMG_GATHER_CAP)>  // FX: fixed-point gradient
-__device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,
-                                                          bool valid, int vbase, float fx, float fy, float fz,
-                                                          float g0, float g1) {
-  const int lane = threadIdx.x & 31;
-  const int key = valid ? vbase : -1 - lane;
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  const int rank = __popc(peers & ((1u << lane) - 1u));
-  const bool leader = valid && (rank % (CAP + 1)) == 0;
-  float2 v[8];
-  // members of a leader: the next CAP set bits of peers above it, fetched one per round in
-  // straight-line code (no vote loop), so the compiler can interleave the shuffles and corner
-  // terms of consecutive pairs; a round without a member adds zeros
-  {
-    unsigned above = peers & (0xfffffffeu << lane);
-    corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
-#pragma unroll
-    for (int k = 0; k < CAP; ++k) {
-      const bool has = leader && above != 0u;
-      const int src = has ? __ffs(above) - 1 : lane;
-      above &= above - 1u;
-      const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
-      const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
-                  ez = __shfl_sync(0xffffffffu, fz, src);
-      corner_terms(has ? make_float2(h0, h1) : make_float2(0.f, 0.f), ex, ey, ez, v, true);
-    }
-  }
-  if (!leader) return;
+// the REDs of one aggregated cell: 8 corners x 2 channels (x-pair float4, fixed point or float2)
+template <bool FX>
+__device__ __forceinline__ void emit_cell_reds(const ModelDev<float>& md, float* __restrict__ dgrid, int vbase,
+                                               const float2* v) {
   if constexpr (FX) {
     unsigned long long* base = md.dgrid_fx + (size_t(vbase) << 1);
     const int sy = 2 * md.W, sz = 2 * md.H * md.W;
@@ -497,6 +473,39 @@ __device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>
 #pragma unroll
   for (int c = 0; c < 8; ++c) atomic_add2(base + (c >> 2) * sz + ((c >> 1) & 1) * sy + 2 * (c & 1), v[c].x, v[c].y);
 }
+
+template <bool FX = false, int CAP = (FX ? APMG_FX_GATHER_CAP : APMG_GATHER_CAP)>  // FX: fixed-point gradient
+__device__ __forceinline__ void scatter_vertex_warp_gather(const ModelDev<float>& md, float* __restrict__ dgrid,
+                                                          bool valid, int vbase, float fx, float fy, float fz,
+                                                          float g0, float g1) {
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? vbase : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  const bool leader = valid && (rank % (CAP + 1)) == 0;
+  float2 v[8];
+  // members of a leader: the next CAP set bits of peers above it, fetched one per round in
+  // straight-line code (no vote loop), so the compiler can interleave the shuffles and corner
+  // terms of consecutive pairs; a round without a member adds zeros
+  {
+    unsigned above = peers & (0xfffffffeu << lane);
+    corner_terms(make_float2(g0, g1), fx, fy, fz, v, false);
+#pragma unroll
+    for (int k = 0; k < CAP; ++k) {
+      const bool has = leader && above != 0u;
+      const int src = has ? __ffs(above) - 1 : lane;
+      above &= above - 1u;
+      const float h0 = __shfl_sync(0xffffffffu, g0, src), h1 = __shfl_sync(0xffffffffu, g1, src);
+      const float ex = __shfl_sync(0xffffffffu, fx, src), ey = __shfl_sync(0xffffffffu, fy, src),
+                  ez = __shfl_sync(0xffffffffu, fz, src);
+      corner_terms(has ? make_float2(h0, h1) : make_float2(0.f, 0.f), ex, ey, ez, v, true);
+    }
+  }
+  if (!leader) return;
+  emit_cell_reds<FX>(md, dgrid, vbase, v);
+}
+
+
 
 template <typename T>
 __device__ __forceinline__ void scatter_grid_point(const ModelDev<T>& md, T* __restrict__ dgrid, int m, T x0, T x1,
