@@ -159,6 +159,10 @@ def workload_config(world):
             "l2": "inputs larger than L2 (~540 MB brick volume per session)"}
 
 
+# untimed train_single calls before the timed e2e call (the allocator reaches its steady state --
+# the timed call's blocks all come from its cache -- after the second)
+E2E_WARM = int(os.environ.get("APMG_E2E_WARM", "2"))
+
 # algorithmic work per training point -> per-kernel roofline rows
 ENC_BYTES = 8 * M * CH * 4          # 4,096 B of corner data gathered per point (encoder fwd)
 SCAT_BYTES = 8 * M * CH * 4         # 4,096 B of corner gradients reduced per point (encoder bwd)
@@ -428,7 +432,7 @@ def main():
         m2 = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
         cfg2 = PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0, transform_hard_stop_fraction=1.0,
                               plateau_enabled=False, seed=seed)
-        # one untimed warm-up call (first-use costs: staging ring, allocator pools, graph build);
+        # E2E_WARM untimed warm-up calls (first-use costs: staging ring, allocator pools, graph build);
         # train_single hands its large blocks back at return, so the timed call allocates afresh
         # (same iteration count as the timed call, so its workspace has the timed call's size and
         # torch's caching allocator hands the same block back)
@@ -436,11 +440,12 @@ def main():
         # repeated train_single calls (the timed call reuses the warm-up's workspace); the host
         # volume is page-locked in place by its first upload (pin_host), as a pinned input buffer.
         with PT.hold_block_cache():
-            mw = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
-            PT.train_single(mw, PV.Volume(dims=DIMS1, data=host_vol.data),
-                            PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0,
-                                           transform_hard_stop_fraction=1.0, plateau_enabled=False, seed=seed))
-            del mw
+            for _ in range(E2E_WARM):
+                mw = PM.init_model(PM.ModelConfig(M, CH, RES), seed=seed, vmin=vol.vmin, vmax=vol.vmax)
+                PT.train_single(mw, PV.Volume(dims=DIMS1, data=host_vol.data),
+                                PT.TrainConfig(iterations=K, batch_size=BATCH, delay_start=0,
+                                               transform_hard_stop_fraction=1.0, plateau_enabled=False, seed=seed))
+                del mw
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             _, log2 = PT.train_single(m2, host_vol, cfg2)
@@ -452,8 +457,8 @@ def main():
                "d2h_bytes_per_step": int((params_b + 24 * K) / K),
                "setup_ms": round(1e3 * log2.setup_seconds, 2), "setup_split_ms": log2.setup_ms,
                "loop_ms": round(log2.loop_ms, 2), "wall_ms": round(1e3 * dt, 2),
-               "note": f"paper_2308_02494_b200.train_single(host model, host Volume, iterations={K}) after one "
-                       f"untimed call, both inside hold_block_cache: volume upload (one DMA from the page-locked "
+               "note": f"paper_2308_02494_b200.train_single(host model, host Volume, iterations={K}) after "
+                       f"{E2E_WARM} untimed calls, all inside hold_block_cache: volume upload (one DMA from the page-locked "
                        f"host array) + parameter upload, device loop, parameter + log download; bound: "
                        f"loop / (loop + volume bytes / link rate)"}
 

@@ -221,9 +221,11 @@ class TrainSession:
         if dt not in (np.float32, np.float64):
             raise TypeError(f"unsupported model dtype {dt}")
         self.dt = dt
-        # parameters first (17 MiB at the flagship shape, staged through the pinned ring), then the
-        # volume's DMA is issued and left in flight: the workspace and the session's host-side setup
-        # run behind it, and apmg_train_create (stream-ordered after the DMA) returns synchronised
+        # parameters first (17 MiB at the flagship shape, staged through the pinned ring; behind a
+        # volume DMA already in flight they would wait for it), then the volume's DMA from the
+        # page-locked host array is issued and left in flight: the workspace and the session's
+        # host-side setup run behind it, and apmg_train_create (stream-ordered after the DMA)
+        # returns synchronised
         tv = t0
         self.dm = DeviceModel.upload(model)
         off = (C.c_int64 * 5)()
