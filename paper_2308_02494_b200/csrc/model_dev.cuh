@@ -218,6 +218,31 @@ __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, 
   o1 = r.y;
 }
 
+// the two halves of interp_pairx_f32, so a caller can issue several cells' corner loads before
+// the first lerp (memory-level parallelism); same arithmetic in the same order
+__device__ __forceinline__ void gather_pairx_f32(const float4* __restrict__ gx, int W, int HW, int vbase, float4* b) {
+  const float4* g = gx + vbase;
+#ifdef APMG_ABL_NOGATHER  // timing ablation only: no corner loads (wrong results)
+  const float q = __int_as_float(vbase & 0x3fffff);
+  b[0] = b[1] = b[2] = b[3] = make_float4(q, q, q, q);
+  (void)g;
+#else
+  b[0] = __ldg(g);
+  b[1] = __ldg(g + W);
+  b[2] = __ldg(g + HW);
+  b[3] = __ldg(g + HW + W);
+#endif
+}
+__device__ __forceinline__ void lerp_pairx_f32(const float4* b, float fx, float fy, float fz, float& o0, float& o1) {
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(make_float2(b[0].x, b[0].y), make_float2(b[0].z, b[0].w), fx),
+                                   f2_lerp(make_float2(b[1].x, b[1].y), make_float2(b[1].z, b[1].w), fx), fy),
+                           f2_lerp(f2_lerp(make_float2(b[2].x, b[2].y), make_float2(b[2].z, b[2].w), fx),
+                                   f2_lerp(make_float2(b[3].x, b[3].y), make_float2(b[3].z, b[3].w), fx), fy),
+                           fz);
+  o0 = r.x;
+  o1 = r.y;
+}
+
 // interp_pair_f32 over the x-pair copy: 4 float4 loads instead of 8 float2, same
 // arithmetic in the same order (bit-identical features)
 __device__ __forceinline__ void interp_pairx_f32(const float4* __restrict__ gx, int W, int HW, int vbase, float fx,

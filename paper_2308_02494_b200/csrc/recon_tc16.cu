@@ -82,6 +82,11 @@ static_assert(TC_CACHE + 2 * CACHE_TILE <= TMEM_COLS, "tensor memory budget");
 #define TC16_SQ_C 2
 #define TC16_SQ_E 2
 #endif
+// corner loads issued per batch in the encode before their lerps: 4 (a group's 2 grids x 2 points,
+// 16 float4 in flight), 2 (per grid) or 1 (per (grid, point): load -> lerp, the round-1 order)
+#ifndef TC16_ENC_BATCH
+#define TC16_ENC_BATCH 4
+#endif
 #ifndef TC16_FWD_Q
 #define TC16_FWD_Q 6  // forward products per GEMM: 6 (f32-level) or 3 (hh, hm, mh: ~2^-16)
 #endif
@@ -336,8 +341,10 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
     const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
     uint32_t cache[12];
     uint32_t fw[2][2][3];  // [grid jj][point h][plane]
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
+    int vbs[2][2];            // [jj][h] base vertex (-1 outside)
+    float fxs[2][2], fys[2][2], fzs[2][2];
+    // cell terms of grid jj for both points (packed fp32x2), the fused density bump
+    auto cells = [&](int jj) {
       const int m = 2 * warp + 32 * jq + jj;
       const float* tf = sTF + 12 * m;
       const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
@@ -352,31 +359,73 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
         racc = make_float2(fmaf(sDET[m], b.x, racc.x), fmaf(sDET[m], b.y, racc.y));
       }
       int ix[2], iy[2], iz[2];
-      float fx[2], fy[2], fz[2];
-      axis_term2(l0, md.W, ix[0], ix[1], fx[0], fx[1]);
-      axis_term2(l1, md.H, iy[0], iy[1], fy[0], fy[1]);
-      axis_term2(l2, md.D, iz[0], iz[1], fz[0], fz[1]);
+      axis_term2(l0, md.W, ix[0], ix[1], fxs[jj][0], fxs[jj][1]);
+      axis_term2(l1, md.H, iy[0], iy[1], fys[jj][0], fys[jj][1]);
+      axis_term2(l2, md.D, iz[0], iz[1], fzs[jj][0], fzs[jj][1]);
       const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int u = 2 * jj + h, p = lane + 32 * h;
         const bool inside = (fabsf(la[h][0]) <= 1.f) && (fabsf(la[h][1]) <= 1.f) && (fabsf(la[h][2]) <= 1.f);
-        const int vbase = inside ? ((m * md.D + iz[h]) * md.H + iy[h]) * md.W + ix[h] : -1;
-        float f0 = 0.f, f1 = 0.f;
-        {  // straight-line: outside pairs gather cell 0 and are zeroed afterwards
-          const bool use = inside;
-          const int vb = use ? vbase : 0;
+        vbs[jj][h] = inside ? ((m * md.D + iz[h]) * md.H + iy[h]) * md.W + ix[h] : -1;
+      }
+    };
+    // features of (jj, h) from its gathered corners (straight-line: outside pairs gathered cell 0
+    // and are zeroed here), cell cache words, bf16x3 split
+    auto finish = [&](int jj, int h, const float4* b) {
+      const int u = 2 * jj + h;
+      const bool use = vbs[jj][h] >= 0;
+      float f0, f1;
+      lerp_pairx_f32(b, fxs[jj][h], fys[jj][h], fzs[jj][h], f0, f1);
+      f0 = use ? f0 : 0.f;
+      f1 = use ? f1 : 0.f;
+      pack_cell(vbs[jj][h], fxs[jj][h], fys[jj][h], fzs[jj][h], cache + 3 * u);
+      umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
+    };
+    if (md.gridx && !md.gridq && TC16_ENC_BATCH == 4) {
+      // every corner load of the group issued before the first lerp: 16 float4 gathers in flight
+      // per thread instead of 4 (the encode waited one L2 round trip per (grid, point))
+      cells(0);
+      cells(1);
+      float4 b[2][2][4];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) gather_pairx_f32(md.gridx, md.W, md.H * md.W, max(vbs[jj][h], 0), b[jj][h]);
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) finish(jj, h, b[jj][h]);
+    } else if (md.gridx && !md.gridq && TC16_ENC_BATCH == 2) {
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        cells(jj);
+        float4 b[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) gather_pairx_f32(md.gridx, md.W, md.H * md.W, max(vbs[jj][h], 0), b[h]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) finish(jj, h, b[h]);
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        cells(jj);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int u = 2 * jj + h;
+          const bool use = vbs[jj][h] >= 0;
+          const int vb = use ? vbs[jj][h] : 0;
+          float f0 = 0.f, f1 = 0.f;
           if (md.gridq)
-            interp_pairq_f32(md.gridq, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
+            interp_pairq_f32(md.gridq, md.H * md.W, vb, fxs[jj][h], fys[jj][h], fzs[jj][h], f0, f1);
           else if (md.gridx)
-            interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
+            interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fxs[jj][h], fys[jj][h], fzs[jj][h], f0, f1);
           else
-            interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[h], fy[h], fz[h], f0, f1);
+            interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fxs[jj][h], fys[jj][h], fzs[jj][h], f0, f1);
           f0 = use ? f0 : 0.f;
           f1 = use ? f1 : 0.f;
+          pack_cell(vbs[jj][h], fxs[jj][h], fys[jj][h], fzs[jj][h], cache + 3 * u);
+          umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
         }
-        pack_cell(vbase, fx[h], fy[h], fz[h], cache + 3 * u);
-        umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
       }
     }
 #pragma unroll
