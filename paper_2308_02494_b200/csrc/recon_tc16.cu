@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
   // share its transform and run in packed fp32x2 arithmetic; the two grids' four features of a
   // point are adjacent in F (one 8-byte store per plane)
   int it = 0;
-  auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache, float2& racc) {
+  // mid(jj): work with no dependence on the gathers (the previous tile's scatter pairs), run
+  // between the issue of grid jj's corner loads and their lerps
+  auto encode_group = [&](const float* cX, int jq, uint32_t tmem_cache, float2& racc, auto&& mid) {
     const float2 X0 = make_float2(cX[3 * lane], cX[3 * (lane + 32)]);
     const float2 X1 = make_float2(cX[3 * lane + 1], cX[3 * (lane + 32) + 1]);
     const float2 X2 = make_float2(cX[3 * lane + 2], cX[3 * (lane + 32) + 2]);
@@ -391,6 +393,8 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
       for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
         for (int h = 0; h < 2; ++h) gather_pairx_f32(md.gridx, md.W, md.H * md.W, max(vbs[jj][h], 0), b[jj][h]);
+      mid(0);
+      mid(1);
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
@@ -402,12 +406,14 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
         float4 b[2][4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) gather_pairx_f32(md.gridx, md.W, md.H * md.W, max(vbs[jj][h], 0), b[h]);
+        mid(jj);
 #pragma unroll
         for (int h = 0; h < 2; ++h) finish(jj, h, b[h]);
       }
     } else {
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
+        mid(jj);
         cells(jj);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -530,9 +536,13 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
     }
 #pragma unroll
     for (int jq = 0; jq < GPW / 2; ++jq) {
-      if (scatter_cnt >= 0)
-        scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * jq / 2, SQ_I * (jq + 1) / 2, scatter_cnt, warp, lane);
-      encode_group(cX, jq, cache_enc, racc);
+      // pairs [SQ_I (2 jq + jj) / 4, SQ_I (2 jq + jj + 1) / 4) of the previous tile's scatter run while
+      // grid jj's gathers are in flight
+      encode_group(cX, jq, cache_enc, racc, [&](int jj) {
+        if (SQ_I > 0 && scatter_cnt >= 0)
+          scatter_pairs<FX>(md, a, GF, cache_sc, SQ_I * (2 * jq + jj) / 4, SQ_I * (2 * jq + jj + 1) / 4, scatter_cnt,
+                            warp, lane);
+      });
       TC16_WSTAMP(9 + 2 * jq);
       if (jq == 0) {
         // features k < 64 (grids 0-31) complete: first half of z1.  Only the issuing warp waits
