@@ -177,6 +177,7 @@ struct apmg_train_state {
   // batch is generated on a side stream while this iteration's Adam and density steps run, into
   // the other of two (coords, targets) buffers (the second carved from c64_sorted, unused there)
   bool fused = false, pipe = false;
+  bool adam_side = false;  // masked Adam of the main group on the side stream (pipe only)
   void* coords_b[2] = {nullptr, nullptr};
   void* targets_b[2] = {nullptr, nullptr};
   cudaStream_t side = nullptr;
@@ -388,6 +389,8 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
     const char* ep = getenv("APMG_BATCH_AHEAD");
     s->fused = s->sort && shape->dtype == APMG_F32 && s->vol_cells && !s->perm && !(efb && efb[0] == '0');
     s->pipe = s->fused && !(ep && ep[0] == '0');
+    const char* ea = getenv("APMG_ADAM_SIDE");
+    s->adam_side = s->pipe && !(ea && ea[0] == '0');
     s->coords_b[0] = s->coords;
     s->targets_b[0] = s->targets;
     if (s->pipe) {
@@ -519,32 +522,48 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                            grad + s->off[2],
                            grad + s->off[3], s->recon_ws, s->recon_wsb, s->ctl, s->l_rec, st);
   if (rc) return rc;
-  if (s->pipe && sizeof(T) == 4) {  // the next iteration's batch, concurrent with Adam + density
+  auto adam_main = [&](cudaStream_t as) -> int {
+    APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, as, params, grad,
+                static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
+                reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, s->gq_w, reinterpret_cast<float*>(s->gradx),
+                s->gfx, s->fx_elems);
+    return APMG_OK;
+  };
+  bool adam_done = false;
+#ifdef APMG_ABL_FREEZE  // timing builds only: parameters frozen (no Adam, no density step), so
+  // ablated kernels computing wrong values cannot change later iterations' inputs
+  adam_done = m.grids > 0;
+#endif
+  if (s->pipe && sizeof(T) == 4) {
+    // side stream, after the recon (and its finalize: the gradients): the next iteration's batch,
+    // then masked Adam on the main group -- both concurrent with the density step on this stream
+    // (Adam reads nothing the density step writes; it is memory-bound, the density gradient FP32)
     APMG_CUDA_TRY(cudaEventRecord(s->ev_fork, st));
     APMG_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
     if (int rc2 = fused_batch(s->side, 1, s->coords_b[cur ^ 1], s->targets_b[cur ^ 1])) return rc2;
+    if (!adam_done && s->adam_side) {
+      if (int rc2 = adam_main(s->side)) return rc2;
+      adam_done = true;
+    }
     APMG_CUDA_TRY(cudaEventRecord(s->ev_join, s->side));
   }
-  // end of the iteration: controller, then join the side stream (the next iteration's recon
-  // reads the batch it generated)
+  // end of the iteration: join the side stream (the next iteration's recon reads the batch and
+  // the parameters it wrote; the controller may change the learning rate Adam read), controller
   auto finish = [&]() -> int {
-    APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
-                s->plat_ring, s->trig);
     if (s->pipe && sizeof(T) == 4) {
       APMG_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_join, 0));
       s->batch_ready = true;
     }
+    APMG_LAUNCH("ctl_end", k_ctl_end, 1, 32, 0, st, s->ctl, s->P, s->l_rec, s->l_dens, s->lr, s->dens_hist,
+                s->plat_ring, s->trig);
     ++s->host_it;
     return APMG_OK;
   };
-#ifdef APMG_ABL_FREEZE  // timing builds only: parameters frozen (no Adam, no density step), so
-  // ablated kernels computing wrong values cannot change later iterations' inputs
+#ifdef APMG_ABL_FREEZE
   if (m.grids > 0) return finish();
 #endif
-  APMG_LAUNCH("adam_main", k_adam_train<T>, elementwise_grid(s->off[4], 8), 256, 0, st, params, grad,
-              static_cast<T*>(s->am), static_cast<T*>(s->av), s->off[4], s->ctl,
-              reinterpret_cast<float*>(s->gridx), 2 * s->gx_cells, s->gq_w, reinterpret_cast<float*>(s->gradx), s->gfx,
-              s->fx_elems);
+  if (!adam_done)
+    if (int rc2 = adam_main(st)) return rc2;
   if (c.train_transforms) {
     rc = launch_density<T, T>(static_cast<T*>(s->transforms), m.grids, m.flat_top_p, coords,
                               static_cast<const T*>(s->sq), B, nullptr, nullptr, nullptr, static_cast<T*>(s->tm),
