@@ -541,7 +541,7 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
     APMG_CUDA_TRY(cudaEventRecord(s->ev_fork, st));
     APMG_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
     if (int rc2 = fused_batch(s->side, 1, s->coords_b[cur ^ 1], s->targets_b[cur ^ 1])) return rc2;
-    if (!adam_done && s->adam_side) {
+    if (!adam_done && s->adam_side && !kernel_timing_on()) {  // per-kernel timing: inline (its own time)
       if (int rc2 = adam_main(s->side)) return rc2;
       adam_done = true;
     }

@@ -19,7 +19,7 @@ def main(tag, *summaries):
                 if k["kernel"].startswith(pre) and name not in out:
                     out[name] = {"dram": float(k["dram_read"]) + float(k["dram_write"]),
                                  "l2": 32.0 * float(k.get("l2_sectors", 0.0)) or None,
-                                 "l2_red_sectors": float(k["l2_red_sectors"]) if k.get("l2_red_sectors") else None}
+                                 "l2_red_sectors": float(k["l2_red_sectors"]) if float(k.get("l2_red_sectors") or 0) > 0 else None}
     (ROOT / "profiles" / f"traffic_{tag}.json").write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
