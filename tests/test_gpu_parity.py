@@ -853,3 +853,31 @@ def test_pinned_in_place_upload(monkeypatch):
     b = np.random.default_rng(4).random((80, 512, 512), dtype=np.float32)
     assert np.array_equal(L.to_host(L.to_device(b)), b)
     assert b.ctypes.data not in L._pinned
+
+
+@pytest.mark.gpu
+def test_grid_copy_scatter_and_adam_variants_agree(monkeypatch):
+    """The A/B alternatives of the flagship training path against the default: the xy-quad grid
+    copy (APMG_GRIDQ=1, 256-bit gathers of the same values: bit-identical features), the scatter's
+    plain / tree-reduced aggregation (APMG_SCATTER_AGG=0 / 1) and inline masked Adam
+    (APMG_ADAM_SIDE=0).  Iteration 0's loss depends on the forward only and is bit-equal; the
+    later ones differ by the float-RED summation order of the grid gradient, within the gradient
+    gate."""
+    vol = PV.synth_volume((48, 40, 32), C1_BLOBS)
+
+    def run(var, val):
+        monkeypatch.setenv(var, val)
+        m = PM.init_model(PM.ModelConfig(grids=64, channels=2, resolution=(32, 32, 32)), seed=0, vmin=vol.vmin,
+                          vmax=vol.vmax)
+        cfg = P.TrainConfig(iterations=12, batch_size=1 << 16, delay_start=4, seed=7, plateau_enabled=False,
+                            transform_hard_stop_fraction=1.0)
+        log = P.train_single(m, vol, cfg)[1]
+        monkeypatch.delenv(var)
+        return np.array(log.l_rec)
+
+    ref = run("APMG_GRIDQ", "0")
+    for var, val in (("APMG_GRIDQ", "1"), ("APMG_SCATTER_AGG", "0"), ("APMG_SCATTER_AGG", "1"),
+                     ("APMG_ADAM_SIDE", "0")):
+        got = run(var, val)
+        assert got[0] == ref[0], (var, val)
+        np.testing.assert_allclose(got, ref, rtol=2e-3, err_msg=f"{var}={val}")
