@@ -59,7 +59,7 @@ constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [4 quarters][64]: dW3
 constexpr uint32_t OFF_RED = OFF_DW3 + 4 * HID * 4;     // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
 constexpr uint32_t OFF_TM = OFF_BAR + 8;
-constexpr uint32_t OFF_TF = OFF_TM + 8;                 // [64][12]
+constexpr uint32_t OFF_TF = (OFF_TM + 8 + 15) & ~15u;   // [64][12], 16-B aligned (3 LDS.128 per grid)
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
 constexpr uint32_t OFF_DET = OFF_W3 + 64 * 4;          // [64] |det A| (fused density)
 constexpr uint32_t OFF_RHO = OFF_DET + 64 * 4;         // [NW][P] per-warp partial rho (fused density)
@@ -348,10 +348,11 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
     // cell terms of grid jj for both points (packed fp32x2), the fused density bump
     auto cells = [&](int jj) {
       const int m = 2 * warp + 32 * jq + jj;
-      const float* tf = sTF + 12 * m;
-      const float2 l0 = local_coord2(X0, X1, X2, tf[0], tf[1], tf[2], tf[3]);
-      const float2 l1 = local_coord2(X0, X1, X2, tf[4], tf[5], tf[6], tf[7]);
-      const float2 l2 = local_coord2(X0, X1, X2, tf[8], tf[9], tf[10], tf[11]);
+      const float4* tf4 = reinterpret_cast<const float4*>(sTF + 12 * m);  // warp-uniform: 3 broadcasts
+      const float4 ta = tf4[0], tb = tf4[1], tc = tf4[2];
+      const float2 l0 = local_coord2(X0, X1, X2, ta.x, ta.y, ta.z, ta.w);
+      const float2 l1 = local_coord2(X0, X1, X2, tb.x, tb.y, tb.z, tb.w);
+      const float2 l2 = local_coord2(X0, X1, X2, tc.x, tc.y, tc.z, tc.w);
       if (rho_on) {
 #ifdef TC16_ABL_NOBUMP  // timing ablation only: bump 1 (rho stays positive, training stays finite)
         const float2 b = make_float2(1.f, 1.f);

@@ -212,12 +212,31 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Waiting threads suspend inside try_wait until the phase completes (suspend-time hint 10 ms) rather
-// than re-issuing the probe: every CTA warp waits here while the tensor core runs, and spinning
-// probes take issue slots from the warps that still have CUDA-core work (APMG_MBAR_SPIN=1: no hint)
+// Every CTA warp waits here while the tensor core runs; probes take issue slots and shared-memory
+// wavefronts from the warps that still have CUDA-core work. Default: probe, then sleep 32 ns between
+// probes. A/B: APMG_MBAR_SLEEP=0 -> try_wait with a suspend-time hint (10 ms; in practice it returns
+// after a short time, ~20 probes per wait), APMG_MBAR_SPIN=1 -> plain spin.
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
-#if defined(APMG_MBAR_SPIN) && APMG_MBAR_SPIN
+#ifndef APMG_MBAR_SLEEP
+#define APMG_MBAR_SLEEP 32
+#endif
+#if APMG_MBAR_SLEEP > 0  // poll, back off APMG_MBAR_SLEEP ns between probes (-DAPMG_MBAR_SLEEP=0: the
+                         // suspend-hint wait below): +0.6% on the recon kernel, whose 16 worker warps'
+                         // probes were ~6% of its instructions and its shared-memory wavefronts
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(APMG_MBAR_SLEEP);
+  }
+#elif defined(APMG_MBAR_SPIN) && APMG_MBAR_SPIN
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
