@@ -297,18 +297,33 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
             axis_term2(l1, md.H, iy[0], iy[1], fy[0], fy[1]);
             axis_term2(l2, md.D, iz[0], iz[1], fz[0], fz[1]);
             const float la[2][3] = {{l0.x, l1.x, l2.x}, {l0.y, l1.y, l2.y}};
+            bool ins[2];
+            int vb[2];
   #pragma unroll
             for (int k = 0; k < 2; ++k) {
-              const bool inside = (fabsf(la[k][0]) <= 1.f) && (fabsf(la[k][1]) <= 1.f) && (fabsf(la[k][2]) <= 1.f);
+              ins[k] = (fabsf(la[k][0]) <= 1.f) && (fabsf(la[k][1]) <= 1.f) && (fabsf(la[k][2]) <= 1.f);
               // straight-line: an outside pair gathers cell 0 and is zeroed afterwards
-              const int vb = inside ? ((m * md.D + iz[k]) * md.H + iy[k]) * md.W + ix[k] : 0;
-              float f0, f1;
-              if (md.gridx)
-                interp_pairx_f32(md.gridx, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
-              else
-                interp_pair_f32(md.grid, md.W, md.H * md.W, vb, fx[k], fy[k], fz[k], f0, f1);
-              fv[k][2 * g] = inside ? f0 : 0.f;
-              fv[k][2 * g + 1] = inside ? f1 : 0.f;
+              vb[k] = ins[k] ? ((m * md.D + iz[k]) * md.H + iy[k]) * md.W + ix[k] : 0;
+            }
+            // both points' corner loads issued before the first lerp
+            float f0[2], f1[2];
+            if (md.gridx) {
+              float4 b[2][4];
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) gather_pairx_f32(md.gridx, md.W, md.H * md.W, vb[k], b[k]);
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) lerp_pairx_f32(b[k], fx[k], fy[k], fz[k], f0[k], f1[k]);
+            } else {
+              float2 b[2][8];
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) gather_pair_f32(md.grid, md.W, md.H * md.W, vb[k], b[k]);
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) lerp_pair_f32(b[k], fx[k], fy[k], fz[k], f0[k], f1[k]);
+            }
+  #pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              fv[k][2 * g] = ins[k] ? f0[k] : 0.f;
+              fv[k][2 * g + 1] = ins[k] ? f1[k] : 0.f;
             }
           }
           umma::store_chunk3(F, F_PLANE, pa, 8 * warp, P, fv[0]);

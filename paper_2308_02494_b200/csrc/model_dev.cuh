@@ -218,6 +218,25 @@ __device__ __forceinline__ void interp_pair_f32(const float* __restrict__ grid, 
   o1 = r.y;
 }
 
+// the two halves of interp_pair_f32 (8 float2 corner loads; lerps), same arithmetic and order
+__device__ __forceinline__ void gather_pair_f32(const float* __restrict__ grid, int W, int HW, int vbase, float2* a) {
+  const float2* g = reinterpret_cast<const float2*>(grid) + vbase;
+  a[0] = __ldg(g);
+  a[1] = __ldg(g + 1);
+  a[2] = __ldg(g + W);
+  a[3] = __ldg(g + W + 1);
+  a[4] = __ldg(g + HW);
+  a[5] = __ldg(g + HW + 1);
+  a[6] = __ldg(g + HW + W);
+  a[7] = __ldg(g + HW + W + 1);
+}
+__device__ __forceinline__ void lerp_pair_f32(const float2* a, float fx, float fy, float fz, float& o0, float& o1) {
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(a[0], a[1], fx), f2_lerp(a[2], a[3], fx), fy),
+                           f2_lerp(f2_lerp(a[4], a[5], fx), f2_lerp(a[6], a[7], fx), fy), fz);
+  o0 = r.x;
+  o1 = r.y;
+}
+
 // the two halves of interp_pairx_f32, so a caller can issue several cells' corner loads before
 // the first lerp (memory-level parallelism); same arithmetic in the same order
 __device__ __forceinline__ void gather_pairx_f32(const float4* __restrict__ gx, int W, int HW, int vbase, float4* b) {
