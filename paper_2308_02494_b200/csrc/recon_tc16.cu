@@ -58,7 +58,7 @@ constexpr uint32_t OFF_HEAD = OFF_T + 2 * P * 4;        // [WQ][P] partial heads
 constexpr uint32_t OFF_DW3 = OFF_HEAD + WQ * P * 4;     // [4 quarters][64]: dW3 per lane quarter, summed in order
 constexpr uint32_t OFF_RED = OFF_DW3 + 4 * HID * 4;     // [32] doubles
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;
-constexpr uint32_t OFF_TM = OFF_BAR + 8;
+constexpr uint32_t OFF_TM = OFF_BAR + 16;               // [bar | bar_dw1]
 constexpr uint32_t OFF_TF = (OFF_TM + 8 + 15) & ~15u;   // [64][12], 16-B aligned (3 LDS.128 per grid)
 constexpr uint32_t OFF_W3 = OFF_TF + 64 * 12 * 4;       // [64]
 constexpr uint32_t OFF_DET = OFF_W3 + 64 * 4;          // [64] |det A| (fused density)
@@ -98,6 +98,12 @@ constexpr int FWD_Q = TC16_FWD_Q;
 #define TC16_MMA_WARP 1
 #endif
 constexpr bool kMmaWarp = TC16_MMA_WARP != 0;
+// gF and dW1 committed to separate mbarriers: the gF epilogue starts when gF is done while dW1
+// (needed only once the next tile overwrites F, and at the flush) still runs
+#ifndef TC16_SPLIT_DW1
+#define TC16_SPLIT_DW1 1
+#endif
+constexpr bool kSplitDW1 = TC16_SPLIT_DW1 != 0;
 constexpr int NT_LAUNCH = kMmaWarp ? NT + 128 : NT;
 // registers: launched at 96 per thread (640 threads); the helper warpgroup releases 64 per thread
 // (setmaxnreg.dec) and the workers take them (setmaxnreg.inc blocks until the CTA's pool holds
@@ -284,6 +290,7 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
   if (warp == 0) umma::tmem_alloc(tm_slot, TMEM_COLS);
   if (tid == 0) {
     umma::mbar_init(bar, 1);
+    umma::mbar_init(bar + 1, 1);
     umma::fence_mbar_init();
   }
   const int64_t tiles = ceil_div(a.n, P);
@@ -329,6 +336,8 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
   double loss = 0.0;
   double srho = 0.0;  // fused density: sum of this CTA's rho
   uint32_t phase = 0;
+  uint32_t phase_dw1 = 0;    // bar + 1 (dW1 products of the previous tile)
+  bool dw1_pending = false;  // a tile's dW1 has been issued and not yet waited for
   uint32_t h1pos = 0;  // [h1 > 0] bits of this thread's 8 elements (epilogue 1 -> dz1 epilogue)
 
   // encode of grids 2 warp + 32 jq + {0, 1} for points lane, lane + 32: the two points of a grid
@@ -435,6 +444,11 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
         }
       }
     }
+    if (kSplitDW1 && jq == 0 && dw1_pending) {  // F is the previous tile's dW1 operand until it is done
+      umma::mbar_wait(bar + 1, phase_dw1);
+      phase_dw1 ^= 1;
+      dw1_pending = false;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t o = umma::cm16_offset(lane + 32 * h, 4 * warp + 64 * jq, 64);
@@ -497,13 +511,14 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
       for (int q = 0; q < 3; ++q)
         umma::mma_bf16_c(TA, base16, umma::kmajor_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
                          umma::mnmajor16_c(OFF_W1 + kPB(q) * PL64x128, 64, kk), id_kmn128, (kk | q) ? 1u : 0u);
+    if constexpr (kSplitDW1) umma::commit(bar);  // the gF epilogue waits for gF only
 #pragma unroll 1
     for (int kk = 0; kk < P / 16; ++kk)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
         umma::mma_bf16_c(TDW1, base16, umma::mnmajor16_c(OFF_DZ1 + kPA(q) * PL64x64, 64, kk),
                          umma::mnmajor16_c(OFF_F + kPB(q) * PL64x128, 64, kk), id_mm128, 1u);
-    umma::commit(bar);
+    umma::commit(kSplitDW1 ? bar + 1 : bar);  // dW1: before the next tile's F stores / the flush
   };
   // operands of the next products are in shared memory: release the issuing thread (the
   // workers arrive and go on; without the MMA warp, warp 0 waits and issues)
@@ -769,6 +784,7 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
     TC16_WSTAMP(15);
     umma::mbar_wait(bar, phase);
     phase ^= 1;
+    dw1_pending = kSplitDW1;  // this tile's dW1 completes on bar + 1
     umma::fence_after_sync();
     umma::fence_before_sync();
     worker_sync();  // every warp's scatter of the previous tile has read gF before it is overwritten
@@ -800,6 +816,10 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
   }
 
   // ---- flush per-CTA partials: [dW1 (64x128) | dW2 (64x64) | dW3 (64)] from TMEM ----
+  if (dw1_pending) {  // the last tile's dW1
+    umma::mbar_wait(bar + 1, phase_dw1);
+    phase_dw1 ^= 1;
+  }
   umma::fence_before_sync();
   worker_sync();
   umma::fence_after_sync();
