@@ -61,4 +61,6 @@ def main(tag, *subs):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:] or ["r02"]))
+    if len(sys.argv) < 2:
+        sys.exit(__doc__)  # a tag is required: a run without one must not overwrite a committed summary
+    main(*sys.argv[1:])
