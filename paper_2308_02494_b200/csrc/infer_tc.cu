@@ -307,7 +307,13 @@ __global__ void __launch_bounds__(NTA, 1) k_infer_tc(FwdArgs<float> a, const flo
             }
             // both points' corner loads issued before the first lerp
             float f0[2], f1[2];
-            if (md.gridx) {
+            if (md.gridq) {
+              float b[2][16];
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) gather_pairq_f32(md.gridq, md.H * md.W, vb[k], b[k]);
+  #pragma unroll
+              for (int k = 0; k < 2; ++k) lerp_pairq_f32(b[k], fx[k], fy[k], fz[k], f0[k], f1[k]);
+            } else if (md.gridx) {
               float4 b[2][4];
   #pragma unroll
               for (int k = 0; k < 2; ++k) gather_pairx_f32(md.gridx, md.W, md.H * md.W, vb[k], b[k]);
@@ -386,8 +392,8 @@ bool infer_tc_eligible(const FwdArgs<float>& a) {
 }
 
 int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
-  // per-call scratch, stream-ordered: per-axis coordinate tables (lattice sweeps), the x-pair
-  // grid copy (point lists), the per-CTA SSE partials
+  // per-call scratch, stream-ordered: per-axis coordinate tables (lattice sweeps), the grid copy
+  // (xy-quad, or x-pair), the per-CTA SSE partials
   StreamScratch tab_s, gx_s, sse_s;
   float* tab = nullptr;
   if (a.mode == kFwdLattice) {
@@ -397,19 +403,26 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
     APMG_ARG_CHECK(tab != nullptr, "out of device memory for the sweep tables");
     APMG_LAUNCH("infer_axis_tables", itc::k_axis_tables, int(ceil_div(need, 256)), 256, 0, st, a, tab);
   }
-  // x-pair copy of the grid (ModelDev::gridx): 4 float4 corner loads per (point, grid) for
-  // point lists (renderer samples: 19.1 vs 21.6 ms per 512^2 x 128 frame); lattice sweeps hit
-  // L1 for most corners already and measured 2% slower with it, so they read the grid itself
   const int64_t cells = int64_t(a.md.M) * a.md.D * a.md.H * a.md.W;
   const char* eg = getenv("APMG_GRIDX");
-  const bool use_gx = a.mode != kFwdLattice && !(eg && eg[0] == '0');
+  const char* eq = getenv("APMG_INFER_GRIDQ");
+  // the xy-quad copy (ModelDev::gridq): 2 256-bit corner loads per (point, grid); measured against
+  // the grid itself (lattice sweeps, 8 float2 loads: 2.57 vs 2.37 G voxels/s over 1024^3) and the
+  // x-pair copy (point lists, 4 float4 loads: 512^2 x 128 render 18.0 vs 19.6 ms).
+  // APMG_INFER_GRIDQ=0: those layouts (APMG_GRIDX=0: the grid itself for point lists too)
+  const bool use_gq = !(eq && eq[0] == '0');
+  const bool use_gx = !use_gq && a.mode != kFwdLattice && !(eg && eg[0] == '0');
   float4* gx = nullptr;
-  if (use_gx) {
-    gx_s = StreamScratch(sizeof(float4) * cells, st);
+  if (use_gx || use_gq) {
+    gx_s = StreamScratch(sizeof(float4) * (use_gq ? 2 * cells : cells), st);
     gx = gx_s.as<float4>();
-    APMG_ARG_CHECK(gx != nullptr, "out of device memory for the x-pair grid copy");
-    APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(cells, 8), 256, 0, st,
-                reinterpret_cast<const float2*>(a.md.grid), gx, cells);
+    APMG_ARG_CHECK(gx != nullptr, "out of device memory for the grid copy");
+    if (use_gq)
+      APMG_LAUNCH("pack_gridq", k_pack_gridq, elementwise_grid(cells, 8), 256, 0, st,
+                  reinterpret_cast<const float2*>(a.md.grid), gx, cells, a.md.W);
+    else
+      APMG_LAUNCH("pack_gridx", k_pack_gridx, elementwise_grid(cells, 8), 256, 0, st,
+                  reinterpret_cast<const float2*>(a.md.grid), gx, cells);
   }
   static bool attr = false;
   if (!attr) {
@@ -422,7 +435,8 @@ int launch_infer_tc(const FwdArgs<float>& a, cudaStream_t st) {
   const char* es = getenv("APMG_INFER_STAMPS");
   FwdArgs<float> b = a;
   b.stamps = es && es[0] == '1';
-  b.md.gridx = gx;
+  b.md.gridx = use_gq ? nullptr : gx;
+  b.md.gridq = use_gq ? reinterpret_cast<const float*>(gx) : nullptr;
   const bool sse = a.mode == kFwdLattice && a.truth;
   if (sse) {
     sse_s = StreamScratch(sizeof(double) * grid, st);

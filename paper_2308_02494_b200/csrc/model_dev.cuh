@@ -307,6 +307,24 @@ __device__ __forceinline__ void interp_pairq_f32(const float* __restrict__ gq, i
   o1 = r.y;
 }
 
+// the two halves of interp_pairq_f32 (2 256-bit loads; lerps), same arithmetic and order
+__device__ __forceinline__ void gather_pairq_f32(const float* __restrict__ gq, int HW, int vbase, float* a) {
+  const float* g = gq + 8 * size_t(vbase);
+  float (&lo)[8] = *reinterpret_cast<float(*)[8]>(a);
+  float (&hi)[8] = *reinterpret_cast<float(*)[8]>(a + 8);
+  ldg256(g, lo);
+  ldg256(g + 8 * size_t(HW), hi);
+}
+__device__ __forceinline__ void lerp_pairq_f32(const float* a, float fx, float fy, float fz, float& o0, float& o1) {
+  const float2 r = f2_lerp(f2_lerp(f2_lerp(make_float2(a[0], a[1]), make_float2(a[2], a[3]), fx),
+                                   f2_lerp(make_float2(a[4], a[5]), make_float2(a[6], a[7]), fx), fy),
+                           f2_lerp(f2_lerp(make_float2(a[8], a[9]), make_float2(a[10], a[11]), fx),
+                                   f2_lerp(make_float2(a[12], a[13]), make_float2(a[14], a[15]), fx), fy),
+                           fz);
+  o0 = r.x;
+  o1 = r.y;
+}
+
 // Encode point (x0,x1,x2) in grid m into out[0..C) (zero outside the grid).
 template <typename T>
 __device__ __forceinline__ void encode_grid_point(const ModelDev<T>& md, int m, T x0, T x1, T x2, T* out,
