@@ -393,7 +393,31 @@ __global__ void __launch_bounds__(NT_LAUNCH, 1) k_recon_tc16(Args a) {
       pack_cell(vbs[jj][h], fxs[jj][h], fys[jj][h], fzs[jj][h], cache + 3 * u);
       umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
     };
-    if (md.gridx && !md.gridq && TC16_ENC_BATCH == 4) {
+    if (md.gridq && TC16_ENC_BATCH == 4) {
+      // the xy-quad copy: 2 256-bit loads per (grid, point), the group's 8 issued before its lerps
+      cells(0);
+      cells(1);
+      float b[2][2][16];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) gather_pairq_f32(md.gridq, md.H * md.W, max(vbs[jj][h], 0), b[jj][h]);
+      mid(0);
+      mid(1);
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int u = 2 * jj + h;
+          const bool use = vbs[jj][h] >= 0;
+          float f0, f1;
+          lerp_pairq_f32(b[jj][h], fxs[jj][h], fys[jj][h], fzs[jj][h], f0, f1);
+          f0 = use ? f0 : 0.f;
+          f1 = use ? f1 : 0.f;
+          pack_cell(vbs[jj][h], fxs[jj][h], fys[jj][h], fzs[jj][h], cache + 3 * u);
+          umma::split2_bf16x3(f0, f1, fw[jj][h][0], fw[jj][h][1], fw[jj][h][2]);
+        }
+    } else if (md.gridx && !md.gridq && TC16_ENC_BATCH == 4) {
       // every corner load of the group issued before the first lerp: 16 float4 gathers in flight
       // per thread instead of 4 (the encode waited one L2 round trip per (grid, point))
       cells(0);

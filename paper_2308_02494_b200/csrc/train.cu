@@ -273,11 +273,12 @@ static size_t carve_train(apmg_train_state* s, const apmg_model* m, const apmg_t
   const char* eg = getenv("APMG_GRIDX");
   const bool use_gx = m->dtype == APMG_F32 && m->channels == 2 && !(eg && eg[0] == '0');
   const int64_t cells = int64_t(m->grids) * m->depth * m->height * m->width;
-  // ... or as the xy-quad copy (two 256-bit gathers per (point, grid) instead of four 128-bit
-  // ones; APMG_GRIDQ=1, tensor-core recon kernel only): measured even -- the recon kernel gains
-  // ~1%, masked Adam's four scattered copy writes per cell lose as much
+  // ... as the xy-quad copy where the tensor-core recon kernel reads it (two 256-bit gathers per
+  // (point, grid) instead of four 128-bit ones, a group's 8 in flight: 1.413 -> 1.369 ms per
+  // launch; masked Adam's four copy writes per cell run on the side stream, hidden behind the
+  // density step). APMG_GRIDQ=0: the x-pair copy
   const char* eq = getenv("APMG_GRIDQ");
-  const bool use_gq = use_gx && recon_uses_tc16(*m) && (eq && eq[0] == '1');
+  const bool use_gq = use_gx && recon_uses_tc16(*m) && !(eq && eq[0] == '0');
   float4* gridx = use_gx ? cv.take<float4>(use_gq ? 2 * cells : cells) : nullptr;
   // ... and the x-pair grid gradient when the bf16x3 recon kernel runs (APMG_GRADX=0 off)
   const char* ed = getenv("APMG_GRADX");

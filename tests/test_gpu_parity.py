@@ -857,8 +857,8 @@ def test_pinned_in_place_upload(monkeypatch):
 
 @pytest.mark.gpu
 def test_grid_copy_scatter_and_adam_variants_agree(monkeypatch):
-    """The A/B alternatives of the flagship training path against the default: the xy-quad grid
-    copy (APMG_GRIDQ=1, 256-bit gathers of the same values: bit-identical features), the scatter's
+    """The A/B alternatives of the flagship training path against the default: the x-pair grid
+    copy (APMG_GRIDQ=0, 128-bit gathers of the same values: bit-identical features), the scatter's
     plain / tree-reduced aggregation (APMG_SCATTER_AGG=0 / 1) and inline masked Adam
     (APMG_ADAM_SIDE=0).  Iteration 0's loss depends on the forward only and is bit-equal; the
     later ones differ by the float-RED summation order of the grid gradient, within the gradient
@@ -875,8 +875,8 @@ def test_grid_copy_scatter_and_adam_variants_agree(monkeypatch):
         monkeypatch.delenv(var)
         return np.array(log.l_rec)
 
-    ref = run("APMG_GRIDQ", "0")
-    for var, val in (("APMG_GRIDQ", "1"), ("APMG_SCATTER_AGG", "0"), ("APMG_SCATTER_AGG", "1"),
+    ref = run("APMG_GRIDQ", "1")
+    for var, val in (("APMG_GRIDQ", "0"), ("APMG_SCATTER_AGG", "0"), ("APMG_SCATTER_AGG", "1"),
                      ("APMG_ADAM_SIDE", "0")):
         got = run(var, val)
         assert got[0] == ref[0], (var, val)
