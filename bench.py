@@ -203,9 +203,10 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
     """Roofline of one kernel from its average device time per launch (CUDA events inside the
     bench) and its ALGORITHMIC work per launch (SURVEY 8d per-point figure x 2^20 points).
 
-    k_recon_tc16 (encode -> tcgen05 MLP -> scatter): the 16 MiB grids and their x-pair copies are
-    L2-resident, so the encoder is bound by L2 gather bandwidth (the kernel issues float4 gathers:
-    peak = the random float4 gather probe) and the scatter by L2 RED throughput (float4 RED probe);
+    k_recon_tc16 (encode -> tcgen05 MLP -> scatter): the 16 MiB grids and their 64 MiB xy-quad copy
+    are L2-resident, so the encoder is bound by L2 gather bandwidth (the kernel issues 32-byte
+    gathers: peak = the random 32-byte gather probe over a 64 MiB table; float4 with the x-pair
+    copy) and the scatter by L2 RED throughput (float4 RED probe);
     the MLP by the tensor pipe.  The primary (`bound: l2`) is the encoder gather, SURVEY 8d's and
     north_star's metric; `components` gives all three and `serial_sum_frac` = sum of each part's
     time at its peak / measured time (> 1 means the parts overlap or L1 serves part of them)."""
@@ -216,7 +217,11 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
             "traffic_source": "ncu --set full: dram__bytes_read+write.sum (l2_traffic: 32 x lts__t_sectors.sum) per launch, "
                               "profiles/traffic_r*.json"}
     if kernel.startswith("recon_fwd_bwd") and pk2:
-        g_pk = pk2["l2_gather_float4_GBps_16MiB"]
+        # the gather's peak for the access the kernel issues: 32-byte random loads from the 64 MiB
+        # xy-quad copy (default), or float4 from the 32 MiB x-pair copy (APMG_GRIDQ=0)
+        quad = os.environ.get("APMG_GRIDQ", "1") != "0"
+        g_key = "l2_gather_32B_GBps_64MiB" if quad else "l2_gather_float4_GBps_16MiB"
+        g_pk = pk2.get(g_key) or pk2["l2_gather_float4_GBps_16MiB"]
         r_pk = pk2.get("l2_red_float4_Gops_16MiB") or pk2["l2_red_float2_Gops_16MiB"]
         g_ach = BATCH * ENC_BYTES / t / 1e9
         r_ach = BATCH * RED4_PER_PT / t / 1e9
@@ -224,7 +229,9 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
         f_iss = BATCH * MLP_ISSUED / t / 1e12
         comps = {
             "encoder_gather": {"achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
-                               "work": "4,096 B/pt (64 grids x 4 float4 corner pairs)"},
+                               "peak_probe": g_key,
+                               "work": "4,096 B/pt of corner data (64 grids x 2 x 32 B xy-quad records; "
+                                       "x-pair: 4 x 16 B)"},
             "scatter_red": {"achieved": r_ach, "peak": r_pk, "unit": "G float4 RED/s", "frac": r_ach / r_pk,
                             "work": "256 float4 REDs/pt before warp aggregation (the algorithmic count: "
                                     "frac is the rate the scatter's work is retired at, not L2 RED occupancy)"},
@@ -237,8 +244,9 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
                                          "issued_frac": red_sec / t / 1e9 / r_pk, "issued_source": red_src})
         return {"bound": "l2", **base, "achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
                 "components": comps, "serial_sum_frac": sum(c["frac"] for c in comps.values()),
-                "peak_source": "profiles/peaks_b200.json (tools/peaks.py): random float4 gather / float4 RED "
-                               "over a 16 MiB table; MEASURED_PEAKS.json bf16 dense"}
+                "peak_source": "profiles/peaks_b200.json (tools/peaks.py): random 32-byte gather over a 64 MiB "
+                               "table (float4 over 16 MiB with APMG_GRIDQ=0) / float4 RED over a 16 MiB table; "
+                               "MEASURED_PEAKS.json bf16 dense"}
     if kernel == "density_grad" and pk2:
         a = BATCH * DENS_GRAD_FLOP / t / 1e12
         return {"bound": "fp32", **base, "achieved": a, "peak": pk2["fp32_tflops"], "unit": "TFLOP/s",

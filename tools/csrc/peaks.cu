@@ -16,6 +16,7 @@
 //           over 4 accumulators (table_bytes = 1):
 //           the per-instruction cost of the small products the MLP kernels issue; work = FLOP
 //   kind 8  L2 RED of random float4 (red.global.add.v4.f32); work = float4 REDs issued
+//   kind 10 L2 gather of random 32-byte elements (ld.global.nc.v8.f32, LDG.E.ENL2.256); work = bytes
 //   kind 6  shared-memory float atomic adds (red.shared.add.f32), 32 distinct banks per
 //           instruction; work = atomic instructions (per warp)
 #include "common.cuh"
@@ -62,6 +63,29 @@ __global__ void __launch_bounds__(256) k_peak_gather4(const float4* __restrict__
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 12345.678f) sink[0] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_peak_gather8(const float* __restrict__ t, uint32_t mask, int iters,
+                                                      float* __restrict__ sink) {
+  uint32_t s = mix32(blockIdx.x * blockDim.x + threadIdx.x + 31u);
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    float v[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s = s * 1664525u + 1013904223u;
+      const float* p = t + 8 * size_t(mix32(s) & mask);
+      asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3]), "=f"(v[u][4]), "=f"(v[u][5]),
+                     "=f"(v[u][6]), "=f"(v[u][7])
+                   : "l"(p));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += v[u][e];
   }
   if (acc == 12345.678f) sink[0] = acc;
 }
@@ -260,6 +284,15 @@ extern "C" int apmg_peak_probe(int32_t kind, void* table, int64_t table_bytes, i
       APMG_LAUNCH("peak_gather4", k_peak_gather4, grid, block, 0, st, static_cast<const float4*>(table),
                   uint32_t(table_bytes / 16 - 1), iters, sink);
       *work = double(grid) * block * iters * 8 * 16;
+      return APMG_OK;
+    }
+    case 10: {
+      APMG_ARG_CHECK(table && table_bytes >= 32 && (table_bytes & (table_bytes - 1)) == 0,
+                     "table_bytes must be a power of two");
+      const int grid = sms * 8, block = 256;
+      APMG_LAUNCH("peak_gather8", k_peak_gather8, grid, block, 0, st, static_cast<const float*>(table),
+                  uint32_t(table_bytes / 32 - 1), iters, sink);
+      *work = double(grid) * block * iters * 8 * 32;
       return APMG_OK;
     }
     case 8: {

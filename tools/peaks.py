@@ -39,6 +39,8 @@ def main():
         out[f"l2_gather_float2_GBps_{mib}MiB"] = g / 1e9
         g4, dt = probe(7, t, mib << 20, 256)
         out[f"l2_gather_float4_GBps_{mib}MiB"] = g4 / 1e9
+        g8, dt = probe(10, t, mib << 20, 256)
+        out[f"l2_gather_32B_GBps_{mib}MiB"] = g8 / 1e9
         r, dt = probe(1, t, mib << 20, 64)
         out[f"l2_red_float2_Gops_{mib}MiB"] = r / 1e9
         r4, dt = probe(8, t, mib << 20, 64)
@@ -61,8 +63,8 @@ def main():
     out["shfl_per_clk_per_sm"] = out["shfl_Ginstr_per_s"] * 1e9 / (out["sms"] * 1.965e9)
     out["atoms_f32_Ginstr_per_s"] = probe(6, sink, 64, 1024)[0] / 1e9
     out["atoms_per_clk_per_sm"] = out["atoms_f32_Ginstr_per_s"] * 1e9 / (out["sms"] * 1.965e9)
-    out["how"] = ("csrc/peaks.cu via tools/peaks.py: best of 5 launches, CUDA events; gather/RED = random float2 "
-                  "over a power-of-two table (16/64 MiB stay in the 126 MB L2), 8 independent accesses in flight "
+    out["how"] = ("csrc/peaks.cu via tools/peaks.py: best of 5 launches, CUDA events; gather/RED = random float2 / float4 / "
+                  "32-byte (ld.global.nc.v8.f32) elements over a power-of-two table (16/64 MiB stay in the 126 MB L2), 8 independent accesses in flight "
                   "per thread, 148x8 CTAs of 256; FP32/FP64 = 8 independent FMA chains per thread; tf32 = "
                   "back-to-back tcgen05.mma M=128 N=256 K=8 from one thread per SM; shfl = 4 independent "
                   "__shfl_sync chains per thread (warp instructions/s)")
