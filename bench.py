@@ -232,18 +232,21 @@ def roofline_for(kernel: str, ms_per_launch: float, pk: dict):
                                "peak_probe": g_key,
                                "work": "4,096 B/pt of corner data (64 grids x 2 x 32 B xy-quad records; "
                                        "x-pair: 4 x 16 B)"},
-            "scatter_red": {"achieved": r_ach, "peak": r_pk, "unit": "G float4 RED/s", "frac": r_ach / r_pk,
-                            "work": "256 float4 REDs/pt before warp aggregation (the algorithmic count: "
-                                    "frac is the rate the scatter's work is retired at, not L2 RED occupancy)"},
+            "scatter_red": {"achieved": None, "peak": r_pk, "unit": "G float4 RED/s", "frac": None,
+                            "algorithmic_equiv": r_ach,
+                            "work": "256 float4 REDs/pt before warp aggregation; achieved / frac count the REDs "
+                                    "the L2 executed after aggregation (ncu RED sectors per launch); "
+                                    "algorithmic_equiv is the pre-aggregation count per second (not bounded by "
+                                    "the peak)"},
             "mlp_tensor": {"achieved": f_iss, "algorithmic": f_alg, "peak": pk["bf16_tflops"],
                            "unit": "TFLOP/s issued (bf16x3 products)", "frac": f_iss / pk["bf16_tflops"],
                            "work": "295,680 issued FLOP/pt (74,112 algorithmic)"}}
         red_sec, red_src = _red_sectors(kernel)
         if red_sec:  # the REDs the L2 actually executed (ncu), at this launch's measured time
-            comps["scatter_red"].update({"issued_per_launch": red_sec, "issued_achieved": red_sec / t / 1e9,
-                                         "issued_frac": red_sec / t / 1e9 / r_pk, "issued_source": red_src})
+            comps["scatter_red"].update({"issued_per_launch": red_sec, "achieved": red_sec / t / 1e9,
+                                         "frac": red_sec / t / 1e9 / r_pk, "issued_source": red_src})
         return {"bound": "l2", **base, "achieved": g_ach, "peak": g_pk, "unit": "GB/s", "frac": g_ach / g_pk,
-                "components": comps, "serial_sum_frac": sum(c["frac"] for c in comps.values()),
+                "components": comps, "serial_sum_frac": sum(c["frac"] or 0.0 for c in comps.values()),
                 "peak_source": "profiles/peaks_b200.json (tools/peaks.py): random 32-byte gather over a 64 MiB "
                                "table (float4 over 16 MiB with APMG_GRIDQ=0) / float4 RED over a 16 MiB table; "
                                "MEASURED_PEAKS.json bf16 dense"}
