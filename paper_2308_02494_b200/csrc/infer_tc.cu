@@ -40,7 +40,10 @@ constexpr uint32_t OFF_X = OFF_H1 + 3 * H1_PLANE;     // [2][P][3] (tile parity)
 constexpr uint32_t OFF_TRU = OFF_X + 2 * P * 3 * 4;   // [3][P] truth values (tile index mod 3)
 constexpr uint32_t OFF_HEAD = OFF_TRU + 3 * P * 4;    // [WQ][P]
 constexpr uint32_t OFF_RED = OFF_HEAD + WQ * P * 4;   // [32] doubles
-constexpr int NQ = 4;  // z1 is issued in NQ K-slices, each as soon as its NW / NQ encoding warps are done
+#ifndef ITC_NQ
+#define ITC_NQ 4
+#endif
+constexpr int NQ = ITC_NQ;  // z1 is issued in NQ K-slices, each as soon as its NW / NQ encoding warps are done
 constexpr uint32_t OFF_BAR = OFF_RED + 32 * 8;        // mbarriers: z1 done, z2 done, h1 ready, F slice 0..NQ-1 ready
 constexpr uint32_t OFF_TM = OFF_BAR + 8 * (3 + NQ);
 constexpr uint32_t OFF_W3 = OFF_TM + 16;              // [64]
