@@ -25,6 +25,11 @@ constexpr double kFxScale = 17592186044416.0, kFxInv = 1.0 / 17592186044416.0;
 __device__ __forceinline__ void red_fx(unsigned long long* addr, double v) {
   atomicAdd(addr, static_cast<unsigned long long>(__double2ll_rn(v * kFxScale)));
 }
+// the same for a float: v * 2^44 is exact in float, so rounding it to int64 there gives the double
+// path's integer without the f64 conversions
+__device__ __forceinline__ void red_fx(unsigned long long* addr, float v) {
+  atomicAdd(addr, static_cast<unsigned long long>(__float2ll_rn(v * 17592186044416.0f)));
+}
 
 template <typename T>
 struct ModelDev {
