@@ -506,7 +506,7 @@ __device__ __forceinline__ void corner_terms(float2 g, float fx, float fy, float
 // larger leader blocks pay there (the float sums inside a block run in lane order: still
 // deterministic once the batch order inside each bucket is fixed)
 #ifndef APMG_FX_GATHER_CAP
-#define APMG_FX_GATHER_CAP 7
+#define APMG_FX_GATHER_CAP 5  // blocks of 6: 425.6 M points/s (blocks of 4 / 5 / 7 / 8: 401 / 419 / 423 / 417)
 #endif
 // the REDs of one aggregated cell: 8 corners x 2 channels (x-pair float4, fixed point or float2)
 template <bool FX>
