@@ -381,17 +381,57 @@ __global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, cons
   }
 }
 
+// perm != nullptr (deterministic mode): the records go to the (tA, tB) halves with their batch
+// index, for k_bucket_stable_rec to put each bucket back in batch order
 __global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
                                      int32_t* __restrict__ cursor, float* __restrict__ coords,
-                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead) {
+                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead,
+                                     float2* __restrict__ tA, float2* __restrict__ tB, int32_t* __restrict__ perm) {
   if (ahead ? ctl->gen_skip : ctl->skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pos = atomicAdd(&cursor[key[i]], 1);
     const float4 r = rec[i];
+    if (perm) {
+      tA[pos] = make_float2(r.x, r.y);
+      tB[pos] = make_float2(r.z, r.w);
+      perm[pos] = int32_t(i);
+      continue;
+    }
     coords[3 * pos] = r.x;
     coords[3 * pos + 1] = r.y;
     coords[3 * pos + 2] = r.z;
     targets[pos] = r.w;
+  }
+}
+
+// k_bucket_stable for the fused records: each bucket's (tA, tB) records in batch order into the
+// recon inputs (one warp per bucket; rank = number of the bucket's points with a smaller index)
+__global__ void k_bucket_stable_rec(const float2* __restrict__ tA, const float2* __restrict__ tB,
+                                    const int32_t* __restrict__ perm, const int32_t* __restrict__ end, int nbuckets,
+                                    float* __restrict__ coords, float* __restrict__ targets, const TrainCtl* ctl,
+                                    int ahead) {
+  if (ahead ? ctl->gen_skip : ctl->skip) return;
+  const int lane = threadIdx.x & 31;
+  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbuckets; b += (gridDim.x * blockDim.x) >> 5) {
+    const int lo = b ? end[b - 1] : 0, n = end[b] - lo;
+    for (int k0 = 0; k0 < n; k0 += 32) {  // warp-uniform loops: every lane reaches the shuffles
+      const int k = k0 + lane;
+      const int pk = k < n ? perm[lo + k] : 0x7fffffff;
+      int rank = 0;
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int pj = j0 + lane < n ? perm[lo + j0 + lane] : 0x7fffffff;
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) rank += __shfl_sync(0xffffffffu, pj, t) < pk;
+      }
+      if (k < n) {
+        const int64_t src = lo + k, dst = lo + rank;
+        const float2 a = tA[src], c = tB[src];
+        coords[3 * dst] = a.x;
+        coords[3 * dst + 1] = a.y;
+        coords[3 * dst + 2] = c.x;
+        targets[dst] = c.y;
+      }
+    }
   }
 }
 

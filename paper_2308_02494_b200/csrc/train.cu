@@ -38,7 +38,12 @@ __global__ void k_batch_keys_cells(uint64_t k0, uint64_t k1, int64_t batch, cons
                                    int32_t* __restrict__ counts, const TrainCtl* ctl, int ahead);
 __global__ void k_bucket_scatter_rec(const float4* __restrict__ rec, const uint32_t* __restrict__ key, int64_t n,
                                      int32_t* __restrict__ cursor, float* __restrict__ coords,
-                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead);
+                                     float* __restrict__ targets, const TrainCtl* ctl, int ahead,
+                                     float2* __restrict__ tA, float2* __restrict__ tB, int32_t* __restrict__ perm);
+__global__ void k_bucket_stable_rec(const float2* __restrict__ tA, const float2* __restrict__ tB,
+                                    const int32_t* __restrict__ perm, const int32_t* __restrict__ end, int nbuckets,
+                                    float* __restrict__ coords, float* __restrict__ targets, const TrainCtl* ctl,
+                                    int ahead);
 __global__ void k_bucket_scatter(const double* __restrict__ c64, const uint32_t* __restrict__ key, int64_t n,
                                  int32_t* __restrict__ cursor, double* __restrict__ c64_out,
                                  int32_t* __restrict__ perm, const TrainCtl* ctl);
@@ -388,7 +393,8 @@ extern "C" int apmg_train_create(apmg_train_state** out, const apmg_model* shape
   {
     const char* efb = getenv("APMG_FUSED_BATCH");
     const char* ep = getenv("APMG_BATCH_AHEAD");
-    s->fused = s->sort && shape->dtype == APMG_F32 && s->vol_cells && !s->perm && !(efb && efb[0] == '0');
+    // (deterministic sessions too: their batch is put back in batch order inside each bucket)
+    s->fused = s->sort && shape->dtype == APMG_F32 && s->vol_cells && !(efb && efb[0] == '0');
     s->pipe = s->fused && !(ep && ep[0] == '0');
     const char* ea = getenv("APMG_ADAM_SIDE");
     s->adam_side = s->pipe && !(ea && ea[0] == '0');
@@ -481,8 +487,20 @@ static int run_one(apmg_train_state* s, cudaStream_t st) {
                 reinterpret_cast<const float4*>(s->vol_bricked), s->w, s->h, s->d, rec, s->key, s->counts, s->ctl,
                 ahead);
     APMG_LAUNCH("bucket_scan", k_bucket_scan, 1, 1024, 0, bs, s->counts, s->ctl, ahead);
+    if (s->perm) {
+      // deterministic mode: records and batch indices into the unused tails of the two c64 buffers
+      // (floats [4B, 6B) of each; the records use [0, 4B) of c64_raw, the ahead batch [0, 4B) of
+      // c64_sorted), then each bucket back in batch order into the recon inputs
+      float2* tA = reinterpret_cast<float2*>(reinterpret_cast<float*>(s->c64_raw) + 4 * B);
+      float2* tB = reinterpret_cast<float2*>(reinterpret_cast<float*>(s->c64_sorted) + 4 * B);
+      APMG_LAUNCH("bucket_scatter", k_bucket_scatter_rec, elementwise_grid(B, 8), 256, 0, bs, rec, s->key, B,
+                  s->counts, nullptr, nullptr, s->ctl, ahead, tA, tB, s->perm);
+      APMG_LAUNCH("bucket_stable", k_bucket_stable_rec, int(ceil_div(int64_t(kBuckets) * 32, 256)), 256, 0, bs, tA,
+                  tB, s->perm, s->counts, kBuckets, static_cast<float*>(cx), static_cast<float*>(tx), s->ctl, ahead);
+      return APMG_OK;
+    }
     APMG_LAUNCH("bucket_scatter", k_bucket_scatter_rec, elementwise_grid(B, 8), 256, 0, bs, rec, s->key, B,
-                s->counts, static_cast<float*>(cx), static_cast<float*>(tx), s->ctl, ahead);
+                s->counts, static_cast<float*>(cx), static_cast<float*>(tx), s->ctl, ahead, nullptr, nullptr, nullptr);
     return APMG_OK;
   };
   if (s->fused && sizeof(T) == 4) {
