@@ -221,13 +221,29 @@ class TrainSession:
         if dt not in (np.float32, np.float64):
             raise TypeError(f"unsupported model dtype {dt}")
         self.dt = dt
-        # parameters first (17 MiB at the flagship shape, staged through the pinned ring; behind a
-        # volume DMA already in flight they would wait for it), then the volume's DMA from the
-        # page-locked host array is issued and left in flight: the workspace and the session's
-        # host-side setup run behind it, and apmg_train_create (stream-ordered after the DMA)
-        # returns synchronised
+        # the session plan first (workspace size; the sampler-copy budget queries free device memory,
+        # which took 0.3-70 ms while a DMA was in flight), then the parameters (17 MiB at the flagship
+        # shape, staged through the pinned ring; behind a volume DMA already in flight they would
+        # wait for it), then the volume's DMA from the page-locked host array is issued and left in
+        # flight: the workspace and the session's host-side setup run behind it, and
+        # apmg_train_create (stream-ordered after the DMA) returns synchronised
         tv = t0
+        key = np.random.Philox(cfg.seed).state["state"]["key"]
+        self.ccfg = L.ApmgTrainConfigC(
+            cfg.iterations, cfg.batch_size, cfg.lr_main, cfg.lr_transform, cfg.delay_start,
+            cfg.transform_ma_window, cfg.transform_improve_threshold, cfg.hard_stop_iteration,
+            cfg.plateau_window, cfg.plateau_threshold, cfg.plateau_factor, cfg.plateau_max_triggers,
+            int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)),
+            int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"),
+            1 if getattr(_concurrency, "no_graph", False) else 0)
+        w, h, d = volume.dims
         self.dm = DeviceModel.upload(model)
+        tu = time.perf_counter()
+        # session workspace + the sampler's private copy of the volume, both from torch's caching
+        # allocator (reused by back-to-back sessions, released by torch under memory pressure)
+        need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
+        need = (need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d)
+        tp = time.perf_counter()
         off = (C.c_int64 * 5)()
         L.check(L.lib().apmg_main_layout(C.byref(self.dm.desc), off), "main_layout")
         self.off = [int(v) for v in off]
@@ -241,19 +257,7 @@ class TrainSession:
         t1 = time.perf_counter()
         self.vol = volume.device_data(sync=False)
         t2 = time.perf_counter()
-        key = np.random.Philox(cfg.seed).state["state"]["key"]
-        self.ccfg = L.ApmgTrainConfigC(
-            cfg.iterations, cfg.batch_size, cfg.lr_main, cfg.lr_transform, cfg.delay_start,
-            cfg.transform_ma_window, cfg.transform_improve_threshold, cfg.hard_stop_iteration,
-            cfg.plateau_window, cfg.plateau_threshold, cfg.plateau_factor, cfg.plateau_max_triggers,
-            int(key[0]), int(key[1]), int(bool(cfg.train_transforms)), int(bool(cfg.plateau_enabled)),
-            int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"),
-            1 if getattr(_concurrency, "no_graph", False) else 0)
-        w, h, d = volume.dims
-        # session workspace + the sampler's private copy of the volume, both from torch's caching
-        # allocator (reused by back-to-back sessions, released by torch under memory pressure)
-        need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
-        self.ws = _take_workspace((need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d))
+        self.ws = _take_workspace(need)
         t3 = time.perf_counter()
         bias = _bias_table(cfg.iterations)
         st = C.c_void_p()
@@ -263,9 +267,10 @@ class TrainSession:
                                           L.stream_handle()), "train_create")
         self.state = st
         self._torch = t
-        # host-side setup split (ms): parameter upload, volume DMA issue, workspace, create (waits for
-        # the DMA, builds the sampler's volume copy; synchronised)
-        self.setup_ms = {"params": 1e3 * (t1 - tv), "volume": 1e3 * (t2 - t1), "workspace": 1e3 * (t3 - t2),
+        # host-side setup split (ms): parameter upload (incl. the plan), the plan alone, volume DMA
+        # issue, workspace, create (waits for the DMA, builds the sampler's volume copy; synchronised)
+        self.setup_ms = {"params": 1e3 * (t1 - tv), "plan": 1e3 * (tp - tu), "volume": 1e3 * (t2 - t1),
+                         "workspace": 1e3 * (t3 - t2),
                          "create": 1e3 * (time.perf_counter() - t3)}
 
     def run(self, n: int) -> None:
