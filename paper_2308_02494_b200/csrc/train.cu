@@ -210,9 +210,9 @@ static SamplerCopy sampler_copy_plan(int32_t w, int32_t h, int32_t d, bool sort)
   const char* ec = getenv("APMG_CELLVOL");
   const size_t cell_bytes = size_t(32) * size_t(w > 1 ? w - 1 : 1) * size_t(h > 1 ? h - 1 : 1) *
                             size_t(d > 1 ? d - 1 : 1);
-  // free device memory, re-queried at most once a second: cudaMemGetInfo took 0.3-70 ms (erratic)
+  // free device memory, re-queried at most every 5 s: cudaMemGetInfo took 0.3-70 ms (erratic)
   // when it ran with the session's volume DMA in flight, and this plan is made on every session
-  // setup (twice); a quarter of free memory is a coarse budget that a second-old value serves
+  // setup (twice); a quarter of free memory is a coarse budget that a few-seconds-old value serves
   static std::mutex mu;
   static size_t free_cached = 0;
   static std::chrono::steady_clock::time_point t_cached;
@@ -221,7 +221,7 @@ static SamplerCopy sampler_copy_plan(int32_t w, int32_t h, int32_t d, bool sort)
   {
     std::lock_guard<std::mutex> lk(mu);
     const auto now = std::chrono::steady_clock::now();
-    if (!have || now - t_cached > std::chrono::seconds(1)) {
+    if (!have || now - t_cached > std::chrono::seconds(5)) {
       size_t total_b = 0;
       if (cudaMemGetInfo(&free_cached, &total_b) != cudaSuccess) {
         cudaGetLastError();

@@ -222,11 +222,10 @@ class TrainSession:
             raise TypeError(f"unsupported model dtype {dt}")
         self.dt = dt
         # the session plan first (workspace size; the sampler-copy budget queries free device memory,
-        # which took 0.3-70 ms while a DMA was in flight), then the parameters (17 MiB at the flagship
-        # shape, staged through the pinned ring; behind a volume DMA already in flight they would
-        # wait for it), then the volume's DMA from the page-locked host array is issued and left in
-        # flight: the workspace and the session's host-side setup run behind it, and
-        # apmg_train_create (stream-ordered after the DMA) returns synchronised
+        # which took 0.3-70 ms while a DMA was in flight), then the volume's DMA from the page-locked
+        # host array is issued and left in flight; the parameters (17 MiB at the flagship shape)
+        # are staged through the pinned ring while it runs (their copies queue behind it), then the
+        # workspace; apmg_train_create (stream-ordered after both) returns synchronised
         tv = t0
         key = np.random.Philox(cfg.seed).state["state"]["key"]
         self.ccfg = L.ApmgTrainConfigC(
@@ -237,13 +236,15 @@ class TrainSession:
             int(bool(cfg.deterministic) or os.environ.get("APMG_DETERMINISTIC", "0") == "1"),
             1 if getattr(_concurrency, "no_graph", False) else 0)
         w, h, d = volume.dims
-        self.dm = DeviceModel.upload(model)
-        tu = time.perf_counter()
+        shape = DeviceModel.shape_of(model)
         # session workspace + the sampler's private copy of the volume, both from torch's caching
         # allocator (reused by back-to-back sessions, released by torch under memory pressure)
-        need = L.lib().apmg_train_workspace_bytes(C.byref(self.dm.desc), C.byref(self.ccfg))
+        need = L.lib().apmg_train_workspace_bytes(C.byref(shape), C.byref(self.ccfg))
         need = (need + 255) // 256 * 256 + L.lib().apmg_train_volume_bytes(w, h, d)
         tp = time.perf_counter()
+        self.vol = volume.device_data(sync=False)
+        t1 = time.perf_counter()
+        self.dm = DeviceModel.upload(model)
         off = (C.c_int64 * 5)()
         L.check(L.lib().apmg_main_layout(C.byref(self.dm.desc), off), "main_layout")
         self.off = [int(v) for v in off]
@@ -254,8 +255,6 @@ class TrainSession:
         self.main[o[2]:o[2] + self.dm.w2.numel()].copy_(self.dm.w2.reshape(-1))
         self.main[o[3]:o[3] + self.dm.w3.numel()].copy_(self.dm.w3.reshape(-1))
         self.tf = self.dm.transforms
-        t1 = time.perf_counter()
-        self.vol = volume.device_data(sync=False)
         t2 = time.perf_counter()
         self.ws = _take_workspace(need)
         t3 = time.perf_counter()
@@ -267,9 +266,9 @@ class TrainSession:
                                           L.stream_handle()), "train_create")
         self.state = st
         self._torch = t
-        # host-side setup split (ms): parameter upload (incl. the plan), the plan alone, volume DMA
-        # issue, workspace, create (waits for the DMA, builds the sampler's volume copy; synchronised)
-        self.setup_ms = {"params": 1e3 * (t1 - tv), "plan": 1e3 * (tp - tu), "volume": 1e3 * (t2 - t1),
+        # host-side setup split (ms): plan, volume DMA issue, parameter upload (behind the DMA),
+        # workspace, create (waits for the copies, builds the sampler's volume copy; synchronised)
+        self.setup_ms = {"plan": 1e3 * (tp - tv), "volume": 1e3 * (t1 - tp), "params": 1e3 * (t2 - t1),
                          "workspace": 1e3 * (t3 - t2),
                          "create": 1e3 * (time.perf_counter() - t3)}
 
